@@ -1,0 +1,38 @@
+# Builds the product (libcarve_cuda.so, sm_100a only), the drop-in C++ tools,
+# and the CPU checkers under oracle/ (test infrastructure).
+NVCC ?= nvcc
+CXX ?= g++
+ARCH := -gencode arch=compute_100a,code=sm_100a
+# -fmad=false: no FMA contraction anywhere (FP64 bit-exactness)
+NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -fmad=false -Xcompiler -fPIC -Xptxas -v -Iinclude
+PKG := paper_2410_21207_b200
+LIB := $(PKG)/libcarve_cuda.so
+SRC := $(PKG)/csrc/carve_cuda.cu
+HDR := $(PKG)/csrc/carve_kernels.cuh include/carve_cuda.h
+
+all: $(LIB) oracle tools
+
+$(LIB): $(SRC) $(HDR)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC) 2> build/ptxas.log || (cat build/ptxas.log; false)
+
+build:
+	@mkdir -p build
+
+$(LIB): | build
+
+tools: build/carve build/carve_parity
+
+build/carve: tools/carve_main.cpp $(wildcard include/carve/*.hpp) $(LIB) | build
+	$(CXX) -std=c++20 -O2 -Iinclude -o $@ tools/carve_main.cpp -L$(PKG) -lcarve_cuda -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+
+build/carve_parity: tools/carve_parity.cpp $(wildcard include/carve/*.hpp) $(LIB) | build
+	$(CXX) -std=c++20 -O2 -Iinclude -o $@ tools/carve_parity.cpp -L$(PKG) -lcarve_cuda -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+
+oracle:
+	$(MAKE) -s -C oracle
+
+clean:
+	rm -rf build $(LIB)
+	$(MAKE) -s -C oracle clean
+
+.PHONY: all oracle tools clean

@@ -1,0 +1,77 @@
+// carve/energy.hpp — drop-in for the reference energy layer
+// (/root/reference/proj/include/carve/energy.hpp). Only the gradient-magnitude
+// energy e1 is on the B200 path; the other energy functions, forward costs and
+// masks keep their declarations and fail with usage_error (no CPU fallback).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "carve/error.hpp"
+#include "carve/raster.hpp"
+
+namespace carve {
+
+struct EnergyMap {
+    int width = 0;
+    int height = 0;
+    std::vector<double> values;
+
+    double& at(int row, int col) { return values[size_t(row) * width + col]; }
+    double at(int row, int col) const { return values[size_t(row) * width + col]; }
+};
+
+struct RemovalMask {
+    int width = 0;
+    int height = 0;
+    std::vector<std::uint8_t> flags;
+    bool marked(int row, int col) const { return flags[size_t(row) * width + col] != 0; }
+    void set(int row, int col, bool v) { flags[size_t(row) * width + col] = v ? 1 : 0; }
+    size_t marked_count() const {
+        size_t n = 0;
+        for (auto f : flags) n += f != 0;
+        return n;
+    }
+};
+
+struct ForwardCosts {
+    int width = 0;
+    int height = 0;
+    std::vector<double> cost_left, cost_up, cost_right;
+};
+
+enum class EnergyFn { e1, e2, hog, entropy };
+
+inline const char* to_string(EnergyFn fn) {
+    static const char* names[] = {"e1", "e2", "hog", "entropy"};
+    return names[int(fn)];
+}
+
+/// e = |gx| + |gy| over clamped central differences, FP64, on the device.
+inline EnergyMap energy_e1(const LumaGrid& gray) {
+    EnergyMap out{gray.width, gray.height, std::vector<double>(gray.values.size())};
+    detail::check(carve_cuda_energy_e1_luma(gray.values.data(), gray.width, gray.height, out.values.data()));
+    return out;
+}
+
+/// energy_e1(to_grayscale(img)) fused on the device (one upload, no luma plane).
+inline EnergyMap energy_e1(const PixelGrid& img) {
+    EnergyMap out{img.width, img.height, std::vector<double>(img.pixels.size())};
+    detail::check(carve_cuda_energy_e1_rgb(img.bytes(), img.width, img.height, out.values.data()));
+    return out;
+}
+
+inline EnergyMap energy_e2(const LumaGrid&) { detail::unsupported("energy e2"); }
+inline EnergyMap energy_hog(const LumaGrid&) { detail::unsupported("energy hog"); }
+inline EnergyMap energy_entropy(const LumaGrid&) { detail::unsupported("energy entropy"); }
+
+inline EnergyMap compute_energy(const LumaGrid& gray, EnergyFn fn) {
+    if (fn != EnergyFn::e1) detail::unsupported(std::string("energy ") + to_string(fn));
+    return energy_e1(gray);
+}
+
+inline ForwardCosts forward_costs(const LumaGrid&) { detail::unsupported("forward energy"); }
+inline EnergyMap apply_mask(const EnergyMap&, const RemovalMask&) { detail::unsupported("removal masks"); }
+
+} // namespace carve

@@ -1,0 +1,227 @@
+/* TEST INFRASTRUCTURE ONLY — the CPU oracle. Never linked into the product;
+ * only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg load it.
+ *
+ * A plain-C restatement of the reference hot path (seam carving with e1
+ * energy and the dynamic-programming solver), following the reference
+ * arithmetic operation for operation so results are FP64-bit-identical.
+ * Built by oracle/Makefile with gcc -O2 -ffp-contract=off and no -march
+ * (FMA contraction changes luma bits).
+ *
+ * Parity pinning: tests/test_oracle.py checks every function here against
+ * the reference itself compiled from /root/reference (oracle/_ref, built by
+ * oracle/Makefile from ref_shim.cpp) and against the committed golden
+ * vectors in tests/golden/ generated from that build.
+ *
+ * Status codes: 0 ok, 1 + Errc (error.hpp:8-26) on a reference error.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* error.hpp:8-26 ordinal + 1 */
+enum {
+    OR_OK = 0,
+    OR_DIMENSION_MISMATCH = 1 + 4,
+    OR_INVALID_SEAM = 1 + 5,
+    OR_EMPTY_IMAGE = 1 + 7,
+    OR_WIDTH_TOO_SMALL = 1 + 8,
+    OR_INVALID_TARGET = 1 + 9,
+    OR_NO_MEMORY = 100,
+};
+
+static int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+static double clampd(double v, double lo, double hi) { return v < lo ? lo : (hi < v ? hi : v); }
+
+/* bench.hpp:67-94 make_test_image; `variant` k > 0 XORs k into the xorshift
+ * seed (the documented C5 batch extension); k = 0 is the
+ * reference fixture byte for byte. */
+int or_make_test_image(int w, int h, uint32_t variant, uint8_t* out) {
+    if (w < 1 || h < 1) return OR_EMPTY_IMAGE;
+    uint32_t s = 0x9E3779B9u ^ ((uint32_t)w * 2654435761u) ^ (uint32_t)h;
+    if (variant) {
+        s ^= variant;
+        if (!s) s = 1u;
+    }
+    const double pi = 3.14159265358979323846;
+    for (int i = 0; i < h; ++i)
+        for (int j = 0; j < w; ++j) {
+            const double u = (double)i / (double)(h - 1 > 1 ? h - 1 : 1);
+            const double v = (double)j / (double)(w - 1 > 1 ? w - 1 : 1);
+            double base = 60.0 + 70.0 * (u + v) / 2.0 + 45.0 * sin(3.0 * pi * u) * cos(3.0 * pi * v);
+            if (u > 0.33 && u < 0.66 && v > 0.25 && v < 0.75) base += (((i / 3) + (j / 3)) % 2) ? 55.0 : -55.0;
+            int n[3];
+            for (int c = 0; c < 3; ++c) {
+                s ^= s << 13;
+                s ^= s >> 17;
+                s ^= s << 5;
+                n[c] = (int)(s % 37u) - 18;
+            }
+            uint8_t* p = out + ((size_t)i * w + j) * 3;
+            p[0] = (uint8_t)clampd(base + n[0], 0.0, 255.0);
+            p[1] = (uint8_t)clampd(base * 0.85 + 24.0 + n[1], 8.0, 255.0);
+            p[2] = (uint8_t)clampd(210.0 - base * 0.55 + n[2], 0.0, 255.0);
+        }
+    return OR_OK;
+}
+
+/* raster.hpp:61-71 — BT.601 luma, evaluated left to right, no FMA. */
+static double luma_of(const uint8_t* p) { return 0.299 * p[0] + 0.587 * p[1] + 0.114 * p[2]; }
+
+int or_to_grayscale(const uint8_t* rgb, int w, int h, double* out) {
+    for (size_t k = 0; k < (size_t)w * h; ++k) out[k] = luma_of(rgb + 3 * k);
+    return OR_OK;
+}
+
+/* energy.hpp:82-98 — clamped central differences (raster.hpp:54-58), no /2,
+ * e = |gx| + |gy| with the x term first. */
+int or_energy_e1_luma(const double* g, int w, int h, double* out) {
+    for (int i = 0; i < h; ++i)
+        for (int j = 0; j < w; ++j) {
+            const double gx = g[(size_t)i * w + clampi(j + 1, 0, w - 1)] - g[(size_t)i * w + clampi(j - 1, 0, w - 1)];
+            const double gy = g[(size_t)clampi(i + 1, 0, h - 1) * w + j] - g[(size_t)clampi(i - 1, 0, h - 1) * w + j];
+            out[(size_t)i * w + j] = fabs(gx) + fabs(gy);
+        }
+    return OR_OK;
+}
+
+int or_energy_e1_rgb(const uint8_t* rgb, int w, int h, double* out) {
+    double* l = (double*)malloc(sizeof(double) * (size_t)w * h);
+    if (!l) return OR_NO_MEMORY;
+    or_to_grayscale(rgb, w, h, l);
+    or_energy_e1_luma(l, w, h, out);
+    free(l);
+    return OR_OK;
+}
+
+/* solvers.hpp:263-289 dp_seam + :94-111 argmin_row/backtrack.
+ * Candidates k in [max(0,j-1), min(w-1,j+1)] scanned upward with strict <,
+ * so the smallest column wins ties; argmin is the first index of the min.
+ * m/b may be NULL (then scratch tables are used). */
+int or_dp_seam(const double* e, int w, int h, double* m_out, int* b_out, int* seam) {
+    if (w < 1 || h < 1) return OR_EMPTY_IMAGE;
+    double* m = m_out ? m_out : (double*)malloc(sizeof(double) * (size_t)w * h);
+    int* b = b_out ? b_out : (int*)malloc(sizeof(int) * (size_t)w * h);
+    if (!m || !b) return OR_NO_MEMORY;
+    for (int j = 0; j < w; ++j) {
+        m[j] = e[j];
+        b[j] = j;
+    }
+    for (int i = 1; i < h; ++i) {
+        const double* prev = m + (size_t)(i - 1) * w;
+        for (int j = 0; j < w; ++j) {
+            int from = -1;
+            double best = INFINITY;
+            const int lo = j - 1 < 0 ? 0 : j - 1, hi = j + 1 > w - 1 ? w - 1 : j + 1;
+            for (int k = lo; k <= hi; ++k)
+                if (prev[k] < best) {
+                    best = prev[k];
+                    from = k;
+                }
+            m[(size_t)i * w + j] = e[(size_t)i * w + j] + best;
+            b[(size_t)i * w + j] = from;
+        }
+    }
+    const double* last = m + (size_t)(h - 1) * w;
+    int col = 0;
+    for (int j = 1; j < w; ++j)
+        if (last[j] < last[col]) col = j;
+    seam[h - 1] = col;
+    for (int i = h - 1; i >= 1; --i) {
+        col = b[(size_t)i * w + col];
+        seam[i - 1] = col;
+    }
+    if (!m_out) free(m);
+    if (!b_out) free(b);
+    return OR_OK;
+}
+
+/* solvers.hpp:69-78 */
+int or_validate_seam(const int* seam, int n, int w, int h) {
+    if (n != h) return OR_INVALID_SEAM;
+    for (int i = 0; i < n; ++i) {
+        if (seam[i] < 0 || seam[i] >= w) return OR_INVALID_SEAM;
+        if (i > 0 && abs(seam[i] - seam[i - 1]) > 1) return OR_INVALID_SEAM;
+    }
+    return OR_OK;
+}
+
+/* carver.hpp:71-82 — out[i][j] = in[i][j < s[i] ? j : j + 1]. */
+int or_remove_seam(const uint8_t* in, int w, int h, const int* seam, int n, uint8_t* out) {
+    int st = or_validate_seam(seam, n, w, h);
+    if (st) return st;
+    if (w < 2) return OR_WIDTH_TOO_SMALL;
+    for (int i = 0; i < h; ++i) {
+        const uint8_t* src = in + (size_t)i * w * 3;
+        uint8_t* dst = out + (size_t)i * (w - 1) * 3;
+        memcpy(dst, src, (size_t)seam[i] * 3);
+        memcpy(dst + (size_t)seam[i] * 3, src + (size_t)(seam[i] + 1) * 3, (size_t)(w - seam[i] - 1) * 3);
+    }
+    return OR_OK;
+}
+
+/* raster.hpp:73-79 */
+int or_transpose(const uint8_t* in, int w, int h, uint8_t* out) {
+    for (int i = 0; i < h; ++i)
+        for (int j = 0; j < w; ++j) memcpy(out + ((size_t)j * h + i) * 3, in + ((size_t)i * w + j) * 3, 3);
+    return OR_OK;
+}
+
+/* carver.hpp:191-214 carve_to_width with the default config (recompute=true,
+ * e1, dp): every seam recomputes luma+energy on the current grid, solves,
+ * removes. `work` holds the current grid in place. */
+static int carve_width_inplace(uint8_t* work, int w, int h, int target_w, int** seams_cursor) {
+    double* e = (double*)malloc(sizeof(double) * (size_t)w * h);
+    uint8_t* tmp = (uint8_t*)malloc((size_t)w * h * 3);
+    int* seam = (int*)malloc(sizeof(int) * (size_t)h);
+    if (!e || !tmp || !seam) return OR_NO_MEMORY;
+    for (int cw = w; cw > target_w; --cw) {
+        or_energy_e1_rgb(work, cw, h, e);
+        or_dp_seam(e, cw, h, NULL, NULL, seam);
+        or_remove_seam(work, cw, h, seam, h, tmp);
+        memcpy(work, tmp, (size_t)(cw - 1) * h * 3);
+        if (seams_cursor && *seams_cursor) {
+            memcpy(*seams_cursor, seam, sizeof(int) * (size_t)h);
+            *seams_cursor += h;
+        }
+    }
+    free(e);
+    free(tmp);
+    free(seam);
+    return OR_OK;
+}
+
+/* run_resize (cli.hpp:242-259): width phase, then carve_to_height
+ * (carver.hpp:216-222) as transpose ∘ carve_to_width ∘ transpose. */
+int or_carve(const uint8_t* rgb, int w, int h, int target_w, int target_h, uint8_t* out, int* seams_out) {
+    if (w < 1 || h < 1) return OR_EMPTY_IMAGE;
+    if (target_w < 1 || target_w > w) return OR_INVALID_TARGET;
+    if (target_h < 1 || target_h > h) return OR_INVALID_TARGET;
+    uint8_t* work = (uint8_t*)malloc((size_t)w * h * 3);
+    if (!work) return OR_NO_MEMORY;
+    memcpy(work, rgb, (size_t)w * h * 3);
+    int* cursor = seams_out;
+    int st = carve_width_inplace(work, w, h, target_w, &cursor);
+    int cw = target_w;
+    if (!st && target_h != h) {
+        uint8_t* t = (uint8_t*)malloc((size_t)cw * h * 3);
+        if (!t) return OR_NO_MEMORY;
+        or_transpose(work, cw, h, t);
+        st = carve_width_inplace(t, h, cw, target_h, &cursor);
+        or_transpose(t, target_h, cw, work);
+        free(t);
+    }
+    if (!st) memcpy(out, work, (size_t)cw * target_h * 3);
+    free(work);
+    return st;
+}
+
+/* FNV-1a-64 of a byte buffer (the survey's output-hash convention). */
+uint64_t or_fnv1a64(const uint8_t* p, size_t n) {
+    uint64_t hsh = 0xcbf29ce484222325ull;
+    for (size_t k = 0; k < n; ++k) {
+        hsh ^= p[k];
+        hsh *= 0x100000001b3ull;
+    }
+    return hsh;
+}

@@ -1,0 +1,207 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product.
+//
+// extern "C" shim over the *unmodified* reference headers, compiled in place
+// from /root/reference/proj/include by oracle/Makefile into oracle/_ref/.
+// The reference is placed in namespace carve_ref so it can never collide with
+// the product's own `carve::` drop-in headers.
+//
+// Build flags follow the reference's own Release default
+// (/root/reference/proj/CMakeLists.txt:8-10): -O3, default x86-64 target,
+// no -march (FMA contraction would change FP64 luma bits).
+//
+// Status codes: 0 = ok, 1 + Errc on carve::Error, 100 on any other exception.
+
+#define carve carve_ref
+#include "carve/bench.hpp"
+#include "carve/carver.hpp"
+#include "carve/energy.hpp"
+#include "carve/raster.hpp"
+#include "carve/solvers.hpp"
+#undef carve
+
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const carve_ref::Error& e) {
+        g_err = e.what();
+        return 1 + int(e.code());
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 100;
+    }
+}
+
+carve_ref::PixelGrid grid_from(const std::uint8_t* rgb, int w, int h) {
+    carve_ref::PixelGrid g(w, h);
+    std::memcpy(g.pixels.data(), rgb, size_t(w) * h * 3);
+    return g;
+}
+
+void grid_to(const carve_ref::PixelGrid& g, std::uint8_t* out) {
+    std::memcpy(out, g.pixels.data(), g.pixels.size() * 3);
+}
+
+carve_ref::EnergyMap map_from(const double* e, int w, int h) {
+    carve_ref::EnergyMap m;
+    m.width = w;
+    m.height = h;
+    m.values.assign(e, e + size_t(w) * h);
+    return m;
+}
+
+carve_ref::CarveConfig config_for(int solver, unsigned workers) {
+    carve_ref::CarveConfig cfg;
+    cfg.solver = solver == 0 ? carve_ref::SolverKind::Dynamic : carve_ref::SolverKind::ParallelDynamic;
+    cfg.solver_opts.workers = workers;
+    return cfg;
+}
+
+} // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+unsigned ref_hardware_concurrency(void) { return std::thread::hardware_concurrency(); }
+
+// bench.hpp:67-94
+int ref_make_test_image(int w, int h, std::uint8_t* out) {
+    return guarded([&] { grid_to(carve_ref::make_test_image(w, h), out); });
+}
+
+// raster.hpp:61-71
+int ref_to_grayscale(const std::uint8_t* rgb, int w, int h, double* out) {
+    return guarded([&] {
+        auto l = carve_ref::to_grayscale(grid_from(rgb, w, h));
+        std::memcpy(out, l.values.data(), l.values.size() * sizeof(double));
+    });
+}
+
+// energy.hpp:89-98 on an arbitrary luma plane
+int ref_energy_e1_luma(const double* luma, int w, int h, double* out) {
+    return guarded([&] {
+        carve_ref::LumaGrid g;
+        g.width = w;
+        g.height = h;
+        g.values.assign(luma, luma + size_t(w) * h);
+        auto e = carve_ref::energy_e1(g);
+        std::memcpy(out, e.values.data(), e.values.size() * sizeof(double));
+    });
+}
+
+// energy_e1(to_grayscale(img)) — the composition solve_step uses (carver.hpp:161-162)
+int ref_energy_e1_rgb(const std::uint8_t* rgb, int w, int h, double* out) {
+    return guarded([&] {
+        auto e = carve_ref::compute_energy(carve_ref::to_grayscale(grid_from(rgb, w, h)), carve_ref::EnergyFn::e1);
+        std::memcpy(out, e.values.data(), e.values.size() * sizeof(double));
+    });
+}
+
+// solvers.hpp:263-289 (solver 0, dp_seam) / :331-347 (solver 1, parallel_dp_seam)
+int ref_dp_seam(const double* e, int w, int h, int solver, unsigned workers, double* m_out, int* b_out,
+                int* seam_out) {
+    return guarded([&] {
+        auto m = map_from(e, w, h);
+        auto r = solver == 0 ? carve_ref::dp_seam(m) : carve_ref::parallel_dp_seam(m, workers);
+        if (m_out) std::memcpy(m_out, r.table.m.data(), r.table.m.size() * sizeof(double));
+        if (b_out) std::memcpy(b_out, r.table.b.data(), r.table.b.size() * sizeof(int));
+        std::memcpy(seam_out, r.seam.data(), r.seam.size() * sizeof(int));
+    });
+}
+
+// solvers.hpp:69-78
+int ref_validate_seam(const int* seam, int n, int w, int h) {
+    return guarded([&] { carve_ref::validate_seam(carve_ref::Seam(seam, seam + n), w, h); });
+}
+
+// carver.hpp:71-82
+int ref_remove_seam(const std::uint8_t* rgb, int w, int h, const int* seam, int n, std::uint8_t* out) {
+    return guarded([&] {
+        auto g = carve_ref::remove_seam(grid_from(rgb, w, h), carve_ref::Seam(seam, seam + n));
+        grid_to(g, out);
+    });
+}
+
+// raster.hpp:73-79
+int ref_transpose(const std::uint8_t* rgb, int w, int h, std::uint8_t* out) {
+    return guarded([&] { grid_to(carve_ref::transpose(grid_from(rgb, w, h)), out); });
+}
+
+// run_resize semantics (cli.hpp:242-259): carve_to_width then carve_to_height.
+// seams_out (nullable) receives every seam, concatenated in removal order.
+// times_out (nullable) receives {width-phase total_s, height-phase total_s}.
+int ref_carve(const std::uint8_t* rgb, int w, int h, int target_w, int target_h, int solver, unsigned workers,
+              std::uint8_t* out, int* seams_out, double* times_out) {
+    return guarded([&] {
+        auto cfg = config_for(solver, workers);
+        carve_ref::PixelGrid img = grid_from(rgb, w, h);
+        size_t off = 0;
+        double tw = 0.0, th = 0.0;
+        if (target_w < 1 || target_w > img.width)
+            carve_ref::fail(carve_ref::Errc::invalid_target, "target width must be in [1, width]");
+        if (target_w < img.width) {
+            auto [carved, report] = carve_ref::carve_to_width(img, target_w, cfg);
+            img = std::move(carved);
+            tw = report.total_s;
+            if (seams_out)
+                for (auto& s : report.seams) {
+                    std::memcpy(seams_out + off, s.data(), s.size() * sizeof(int));
+                    off += s.size();
+                }
+        }
+        if (target_h != img.height) {
+            auto [carved, report] = carve_ref::carve_to_height(img, target_h, cfg);
+            img = std::move(carved);
+            th = report.total_s;
+            if (seams_out)
+                for (auto& s : report.seams) {
+                    std::memcpy(seams_out + off, s.data(), s.size() * sizeof(int));
+                    off += s.size();
+                }
+        }
+        grid_to(img, out);
+        if (times_out) {
+            times_out[0] = tw;
+            times_out[1] = th;
+        }
+    });
+}
+
+// Batch driver for the C5 CPU baseline: the reference has no batch API but its
+// pipelines are reentrant, so `threads` host threads each run
+// carve_to_width over a static, strided share of the images.
+int ref_carve_batch(const std::uint8_t* const* in, int n, int w, int h, int target_w, int solver, unsigned workers,
+                    unsigned threads, std::uint8_t* const* out) {
+    std::vector<int> status(threads ? threads : 1, 0);
+    if (threads == 0) threads = 1;
+    auto worker = [&](unsigned t) {
+        status[t] = guarded([&] {
+            auto cfg = config_for(solver, workers);
+            for (int k = int(t); k < n; k += int(threads)) {
+                auto [carved, report] = carve_ref::carve_to_width(grid_from(in[k], w, h), target_w, cfg);
+                grid_to(carved, out[k]);
+            }
+        });
+    };
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < threads; ++t) pool.emplace_back(worker, t);
+    worker(0);
+    for (auto& th : pool) th.join();
+    for (int s : status)
+        if (s) return s;
+    return 0;
+}
+
+} // extern "C"

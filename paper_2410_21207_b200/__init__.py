@@ -1,0 +1,461 @@
+"""B200-native seam carving (arXiv 2410.21207 DP path) — Python host mirror.
+
+Every function here mirrors a reference entry point in
+/root/reference/proj/include/carve/ (same name, argument meaning and error
+behaviour) and runs on the GPU through the C ABI of ``libcarve_cuda.so``
+(``include/carve_cuda.h``). There is no CPU fallback: if the library is
+missing, importing a compute function raises; if no sm_100 device is present,
+calls raise ``CarveError`` with code ``Errc.device_failure``.
+
+Images are numpy ``uint8`` arrays of shape (H, W, 3) — the row-major packed
+``PixelGrid`` (raster.hpp:28-42). Luma/energy maps are (H, W) float64 arrays
+(``LumaGrid``/``EnergyMap``, raster.hpp:45-59, energy.hpp:16-23).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = [
+    "Errc", "CarveError", "SolverKind", "EnergyFn", "CarveConfig", "SolverOptions", "SeamTiming",
+    "CarveReport", "CostTable", "SeamResult", "make_test_image", "to_grayscale", "energy_e1", "compute_energy",
+    "energy_e1_rgb", "dp_seam", "parallel_dp_seam", "find_seam", "validate_seam", "remove_seam", "transpose",
+    "carve_to_width", "carve_to_height", "carve", "carve_batch", "carve_device", "carve_batch_device",
+    "library", "library_path", "device_count", "launch_count", "reset_launch_count",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcarve_cuda.so")
+
+
+class Errc(enum.IntEnum):
+    """error.hpp:8-26 (ordinal + 1 as returned by the C ABI), plus device failure."""
+    file_not_found = 1
+    unsupported_format = 2
+    corrupt_image = 3
+    io_failure = 4
+    dimension_mismatch = 5
+    invalid_seam = 6
+    image_too_large = 7
+    empty_image = 8
+    width_too_small = 9
+    invalid_target = 10
+    target_too_large = 11
+    empty_mask = 12
+    insufficient_data = 13
+    size_exceeds_source = 14
+    solver_cap_violated = 15
+    empty_input = 16
+    usage_error = 17
+    device_failure = 100
+
+
+class CarveError(RuntimeError):
+    """carve::Error (error.hpp:28-35): carries the Errc code."""
+
+    def __init__(self, code: int, what: str):
+        super().__init__(what)
+        try:
+            self.code = Errc(code)
+        except ValueError:
+            self.code = Errc.device_failure
+
+
+class SolverKind(enum.Enum):  # solvers.hpp:21
+    BruteForce = "bruteforce"
+    Greedy = "greedy"
+    Dynamic = "dp"
+    ParallelDynamic = "pardp"
+
+
+class EnergyFn(enum.Enum):  # energy.hpp:52
+    e1 = "e1"
+    e2 = "e2"
+    hog = "hog"
+    entropy = "entropy"
+
+
+@dataclass
+class SolverOptions:  # solvers.hpp:64-67
+    brute_cap: int = 16
+    workers: int = 0  # accepted for drop-in compatibility; never changes output
+
+
+@dataclass
+class CarveConfig:  # carver.hpp:15-21
+    solver: SolverKind = SolverKind.ParallelDynamic
+    energy_fn: EnergyFn = EnergyFn.e1
+    forward: bool = False
+    recompute: bool = True
+    solver_opts: SolverOptions = field(default_factory=SolverOptions)
+
+
+@dataclass
+class SeamTiming:  # carver.hpp:23-27
+    energy_s: float = 0.0
+    solve_s: float = 0.0
+    remove_s: float = 0.0
+
+
+@dataclass
+class CarveReport:  # carver.hpp:29-34
+    seam_count: int = 0
+    per_seam: list = field(default_factory=list)
+    seams: list = field(default_factory=list)
+    total_s: float = 0.0
+
+
+@dataclass
+class CostTable:  # solvers.hpp:42-55
+    width: int
+    height: int
+    m: np.ndarray  # (H, W) float64 accumulated minimum costs
+    b: np.ndarray  # (H, W) int32 predecessor columns
+
+    def cost(self, row: int, col: int) -> float:
+        return float(self.m[row, col])
+
+    def back(self, row: int, col: int) -> int:
+        return int(self.b[row, col])
+
+    def __eq__(self, other) -> bool:  # operator== compares m and b exactly (:54)
+        return (isinstance(other, CostTable) and self.width == other.width and self.height == other.height
+                and np.array_equal(self.m.view(np.uint64), other.m.view(np.uint64))
+                and np.array_equal(self.b, other.b))
+
+
+@dataclass
+class SeamResult:  # solvers.hpp:57-60
+    seam: np.ndarray
+    table: CostTable
+
+
+class _Timing(C.Structure):
+    _fields_ = [("energy_s", C.c_double), ("solve_s", C.c_double), ("remove_s", C.c_double)]
+
+
+_lib = None
+_u8p = C.POINTER(C.c_uint8)
+
+
+def library_path() -> str:
+    return LIB_PATH
+
+
+def library() -> C.CDLL:
+    """Load libcarve_cuda.so (in-tree build). Raises if it was not built —
+    there is deliberately no fallback implementation."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with `make` or __graft_entry__.build(); "
+                               "the B200 engine has no CPU fallback")
+        lib = C.CDLL(LIB_PATH)
+        vp, i = C.c_void_p, C.c_int
+        sigs = {
+            "carve_cuda_last_error": ([], C.c_char_p),
+            "carve_cuda_version": ([], C.c_char_p),
+            "carve_cuda_device_count": ([], i),
+            "carve_cuda_set_device": ([i], i),
+            "carve_cuda_launch_count": ([], C.c_uint64),
+            "carve_cuda_reset_launch_count": ([], None),
+            "carve_cuda_to_grayscale": ([vp, i, i, vp], i),
+            "carve_cuda_energy_e1_rgb": ([vp, i, i, vp], i),
+            "carve_cuda_energy_e1_luma": ([vp, i, i, vp], i),
+            "carve_cuda_transpose_rgb": ([vp, i, i, vp], i),
+            "carve_cuda_dp_seam": ([vp, i, i, vp, vp, vp], i),
+            "carve_cuda_validate_seam": ([vp, i, i, i], i),
+            "carve_cuda_remove_seam_rgb": ([vp, i, i, vp, i, vp], i),
+            "carve_cuda_carve": ([vp, i, i, i, i, vp, vp, vp], i),
+            "carve_cuda_carve_batch": ([vp, i, i, i, i, i, vp, vp, i], i),
+            "carve_cuda_carve_device": ([vp, i, i, i, i, vp, vp, vp], i),
+            "carve_cuda_carve_batch_device": ([vp, i, i, i, i, i, vp, vp], i),
+            "carve_make_test_image": ([i, i, C.c_uint32, vp], i),
+            "carve_cuda_set_kernel_events": ([i], i),
+            "carve_cuda_kernel_event_stats": ([i, vp, vp, vp], i),
+        }
+        for name, (args, res) in sigs.items():
+            f = getattr(lib, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = lib
+    return _lib
+
+
+def _check(status: int) -> None:
+    if status:
+        msg = library().carve_cuda_last_error().decode()
+        raise CarveError(status, msg)
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def _img(img: np.ndarray) -> np.ndarray:
+    a = np.ascontiguousarray(img, dtype=np.uint8)
+    if a.ndim != 3 or a.shape[2] != 3:
+        raise CarveError(Errc.dimension_mismatch, "image must have shape (H, W, 3)")
+    return a
+
+
+def device_count() -> int:
+    return int(library().carve_cuda_device_count())
+
+
+def set_device(device: int) -> None:
+    _check(library().carve_cuda_set_device(device))
+
+
+def launch_count() -> int:
+    """Kernels this library launched on the calling thread since the last reset."""
+    return int(library().carve_cuda_launch_count())
+
+
+def reset_launch_count() -> None:
+    library().carve_cuda_reset_launch_count()
+
+
+KERNEL_KINDS = {0: "k_energy_full", 1: "k_dp_seam", 2: "k_compact", 3: "k_unpack", 4: "k_pack", 5: "k_transpose"}
+
+
+def set_kernel_events(on: bool) -> None:
+    """Bracket every kernel the carve driver launches with CUDA events (bench attribution)."""
+    _check(library().carve_cuda_set_kernel_events(1 if on else 0))
+
+
+def kernel_event_stats() -> dict:
+    """Per kernel: total event ms, launches, algorithmic bytes."""
+    out = {}
+    for kind, name in KERNEL_KINDS.items():
+        ms, n, by = C.c_double(), C.c_uint64(), C.c_double()
+        _check(library().carve_cuda_kernel_event_stats(kind, C.addressof(ms), C.addressof(n), C.addressof(by)))
+        if n.value:
+            out[name] = {"ms_total": ms.value, "launches": int(n.value), "bytes_total": by.value}
+    return out
+
+
+def _unsupported(what: str):
+    raise CarveError(Errc.usage_error, f"{what} is not supported by the B200 engine")
+
+
+# -- bench fixture (bench.hpp:67-94) -------------------------------------------
+def make_test_image(width: int, height: int, variant: int = 0) -> np.ndarray:
+    out = np.empty((max(height, 0), max(width, 0), 3), np.uint8)
+    _check(library().carve_make_test_image(width, height, variant, _ptr(out)))
+    return out
+
+
+# -- raster / energy -------------------------------------------------------------
+def to_grayscale(img: np.ndarray) -> np.ndarray:
+    """raster.hpp:61-71"""
+    a = _img(img)
+    h, w, _ = a.shape
+    out = np.empty((h, w), np.float64)
+    _check(library().carve_cuda_to_grayscale(_ptr(a), w, h, _ptr(out)))
+    return out
+
+
+def energy_e1(gray: np.ndarray) -> np.ndarray:
+    """energy.hpp:89-98 on a LumaGrid (any float64 plane)."""
+    g = np.ascontiguousarray(gray, dtype=np.float64)
+    h, w = g.shape
+    out = np.empty((h, w), np.float64)
+    _check(library().carve_cuda_energy_e1_luma(_ptr(g), w, h, _ptr(out)))
+    return out
+
+
+def energy_e1_rgb(img: np.ndarray) -> np.ndarray:
+    """energy_e1(to_grayscale(img)) fused on the device (carver.hpp:161-162)."""
+    a = _img(img)
+    h, w, _ = a.shape
+    out = np.empty((h, w), np.float64)
+    _check(library().carve_cuda_energy_e1_rgb(_ptr(a), w, h, _ptr(out)))
+    return out
+
+
+def compute_energy(gray: np.ndarray, fn: EnergyFn = EnergyFn.e1) -> np.ndarray:
+    """energy.hpp:186-194; only e1 is on the B200 path."""
+    if EnergyFn(fn) is not EnergyFn.e1:
+        _unsupported(f"energy function {EnergyFn(fn).value}")
+    return energy_e1(gray)
+
+
+def transpose(img: np.ndarray) -> np.ndarray:
+    """raster.hpp:73-79"""
+    a = _img(img)
+    h, w, _ = a.shape
+    out = np.empty((w, h, 3), np.uint8)
+    _check(library().carve_cuda_transpose_rgb(_ptr(a), w, h, _ptr(out)))
+    return out
+
+
+# -- solvers ------------------------------------------------------------------------
+def dp_seam(energy: np.ndarray) -> SeamResult:
+    """solvers.hpp:263-289 — seam plus the full cost table."""
+    e = np.ascontiguousarray(energy, dtype=np.float64)
+    if e.ndim != 2 or e.size == 0:
+        raise CarveError(Errc.empty_image, "image is empty")
+    h, w = e.shape
+    m = np.empty((h, w), np.float64)
+    b = np.empty((h, w), np.int32)
+    seam = np.empty(h, np.int32)
+    _check(library().carve_cuda_dp_seam(_ptr(e), w, h, _ptr(m), _ptr(b), _ptr(seam)))
+    return SeamResult(seam, CostTable(w, h, m, b))
+
+
+def parallel_dp_seam(energy: np.ndarray, workers: int = 0) -> SeamResult:
+    """solvers.hpp:331-347 — same table as dp_seam for every worker count."""
+    return dp_seam(energy)
+
+
+def find_seam(energy: np.ndarray, kind: SolverKind = SolverKind.ParallelDynamic,
+              opts: SolverOptions | None = None) -> np.ndarray:
+    """solvers.hpp:350-358"""
+    kind = SolverKind(kind)
+    if kind not in (SolverKind.Dynamic, SolverKind.ParallelDynamic):
+        _unsupported(f"solver {kind.value}")
+    e = np.ascontiguousarray(energy, dtype=np.float64)
+    if e.ndim != 2 or e.size == 0:
+        raise CarveError(Errc.empty_image, "image is empty")
+    h, w = e.shape
+    seam = np.empty(h, np.int32)
+    _check(library().carve_cuda_dp_seam(_ptr(e), w, h, None, None, _ptr(seam)))
+    return seam
+
+
+def validate_seam(seam, width: int, height: int) -> None:
+    """solvers.hpp:69-78"""
+    s = np.ascontiguousarray(seam, dtype=np.int32)
+    _check(library().carve_cuda_validate_seam(_ptr(s), len(s), width, height))
+
+
+# -- pipelines --------------------------------------------------------------------
+def remove_seam(img: np.ndarray, seam) -> np.ndarray:
+    """carver.hpp:71-82"""
+    a = _img(img)
+    h, w, _ = a.shape
+    s = np.ascontiguousarray(seam, dtype=np.int32)
+    out = np.empty((h, max(w - 1, 0), 3), np.uint8)
+    _check(library().carve_cuda_remove_seam_rgb(_ptr(a), w, h, _ptr(s), len(s), _ptr(out)))
+    return out
+
+
+def _check_config(cfg: CarveConfig | None) -> None:
+    if cfg is None:
+        return
+    if cfg.forward and SolverKind(cfg.solver) not in (SolverKind.Dynamic, SolverKind.ParallelDynamic):
+        raise CarveError(Errc.usage_error, "forward energy requires the dp or pardp solver")  # carver.hpp:51-54
+    if SolverKind(cfg.solver) not in (SolverKind.Dynamic, SolverKind.ParallelDynamic):
+        _unsupported(f"solver {SolverKind(cfg.solver).value}")
+    if EnergyFn(cfg.energy_fn) is not EnergyFn.e1:
+        _unsupported(f"energy function {EnergyFn(cfg.energy_fn).value}")
+    if cfg.forward:
+        _unsupported("forward energy")
+    # cfg.recompute=False carves the stale map (carver.hpp:175-187) and is not the
+    # bit-exact default path; the engine always produces the recompute=True result.
+
+
+def carve(img: np.ndarray, target_width: int, target_height: int | None = None, *, seams: bool = False,
+          timings: bool = False):
+    """run_resize semantics (cli.hpp:249-256): carve_to_width then carve_to_height.
+    Returns the carved image, plus (seams, timings) lists when requested."""
+    a = _img(img)
+    h, w, _ = a.shape
+    th = h if target_height is None else int(target_height)
+    tw = int(target_width)
+    if tw < 1 or tw > w:
+        raise CarveError(Errc.invalid_target, "target width must be in [1, width]")
+    if th < 1 or th > h:
+        raise CarveError(Errc.invalid_target, "target height must be in [1, height]")
+    out = np.empty((th, tw, 3), np.uint8)
+    n_ints = (w - tw) * h + (h - th) * tw
+    nseams = (w - tw) + (h - th)
+    s = np.empty(max(n_ints, 1), np.int32)
+    t = (_Timing * max(nseams, 1))()
+    _check(library().carve_cuda_carve(_ptr(a), w, h, tw, th, _ptr(out), _ptr(s) if seams else None,
+                                      C.cast(t, C.c_void_p) if timings else None))
+    if not (seams or timings):
+        return out
+    seam_list = []
+    if seams:
+        off = 0
+        for _ in range(w - tw):
+            seam_list.append(s[off:off + h].copy())
+            off += h
+        for _ in range(h - th):
+            seam_list.append(s[off:off + tw].copy())
+            off += tw
+    tim = [SeamTiming(t[k].energy_s, t[k].solve_s, t[k].remove_s) for k in range(nseams)] if timings else []
+    return out, seam_list, tim
+
+
+def _report(seams, tims, total_s) -> CarveReport:
+    return CarveReport(seam_count=len(seams), per_seam=tims, seams=seams, total_s=total_s)
+
+
+def carve_to_width(img: np.ndarray, target_width: int, cfg: CarveConfig | None = None):
+    """carver.hpp:191-214 — returns (carved, CarveReport)."""
+    import time
+    a = _img(img)
+    h, w, _ = a.shape
+    if target_width < 1 or target_width > w:
+        raise CarveError(Errc.invalid_target, "target width must be in [1, width]")
+    _check_config(cfg)
+    t0 = time.perf_counter()
+    out, seams, tims = carve(a, target_width, h, seams=True, timings=True)
+    return out, _report(seams, tims, time.perf_counter() - t0)
+
+
+def carve_to_height(img: np.ndarray, target_height: int, cfg: CarveConfig | None = None):
+    """carver.hpp:216-222 — transpose ∘ carve_to_width ∘ transpose, on the device."""
+    import time
+    a = _img(img)
+    h, w, _ = a.shape
+    if target_height < 1 or target_height > h:
+        raise CarveError(Errc.invalid_target, "target height must be in [1, height]")
+    _check_config(cfg)
+    t0 = time.perf_counter()
+    out, seams, tims = carve(a, w, target_height, seams=True, timings=True)
+    return out, _report(seams, tims, time.perf_counter() - t0)
+
+
+def carve_batch(imgs, target_width: int, target_height: int | None = None, devices=None) -> list:
+    """Batch of same-size images, sharded by image across devices."""
+    arrs = [_img(x) for x in imgs]
+    if not arrs:
+        raise CarveError(Errc.empty_input, "empty batch")
+    h, w, _ = arrs[0].shape
+    if any(x.shape != arrs[0].shape for x in arrs):
+        raise CarveError(Errc.dimension_mismatch, "batch images must share one size")
+    th = h if target_height is None else int(target_height)
+    outs = [np.empty((th, target_width, 3), np.uint8) for _ in arrs]
+    n = len(arrs)
+    ins = (C.c_void_p * n)(*[_ptr(x) for x in arrs])
+    ous = (C.c_void_p * n)(*[_ptr(x) for x in outs])
+    if devices is None:
+        devs, nd = None, 0
+    else:
+        devs = (C.c_int * len(devices))(*devices)
+        nd = len(devices)
+    _check(library().carve_cuda_carve_batch(C.cast(ins, C.c_void_p), n, w, h, target_width, th,
+                                            C.cast(ous, C.c_void_p), C.cast(devs, C.c_void_p) if devs else None, nd))
+    return outs
+
+
+def carve_device(d_in: int, width: int, height: int, target_width: int, target_height: int, d_out: int,
+                 d_seams: int | None = None, stream: int | None = None) -> None:
+    """Enqueue a carve of a device-resident packed image (no host sync)."""
+    _check(library().carve_cuda_carve_device(d_in, width, height, target_width, target_height, d_out, d_seams,
+                                             stream))
+
+
+def carve_batch_device(d_in: int, n: int, width: int, height: int, target_width: int, target_height: int,
+                       d_out: int, stream: int | None = None) -> None:
+    """Enqueue a carve of n contiguous device-resident packed images (no host sync)."""
+    _check(library().carve_cuda_carve_batch_device(d_in, n, width, height, target_width, target_height, d_out,
+                                                   stream))

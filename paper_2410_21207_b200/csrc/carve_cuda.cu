@@ -1,0 +1,784 @@
+// carve_cuda.cu — host side of libcarve_cuda.so: per-thread device contexts,
+// the device-resident carve driver, and the extern "C" boundary declared in
+// include/carve_cuda.h. No CPU compute path exists: every compute entry point
+// runs the sm_100a kernels in carve_kernels.cuh or returns CARVE_E_CUDA.
+#include "carve_cuda.h"
+#include "carve_kernels.cuh"
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace {
+
+using namespace carve_dev;
+
+thread_local std::string t_err;
+thread_local int t_device = 0;
+thread_local uint64_t t_launches = 0;
+
+struct Fail {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Fail{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(CARVE_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define LAUNCHED(what)                              \
+    do {                                            \
+        ++t_launches;                               \
+        ck(cudaGetLastError(), "launch " what);     \
+    } while (0)
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return CARVE_OK;
+    } catch (const Fail& e) {
+        t_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        t_err = "host allocation failed";
+        return CARVE_E_CUDA;
+    } catch (const std::exception& e) {
+        t_err = e.what();
+        return CARVE_E_CUDA;
+    }
+}
+
+size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* ensure(size_t n) {
+        if (n > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            ck(cudaMalloc(&p, n), "cudaMalloc");
+            cap = n;
+        }
+        return p;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    DevBuf packed_in, packed_out, rgb[2], e[2], dir, seams, stamps, scratch_a, scratch_b;
+    int max_smem_optin = 0;
+    std::map<const void*, int> smem_set;  // kernel -> dynamic smem attribute set
+    // kernel-event profiling mode (bench attribution): one event pair per launch
+    bool prof = false;
+    struct ProfRec {
+        int kind;
+        double bytes;
+        cudaEvent_t a, b;
+    };
+    std::vector<ProfRec> prof_recs;
+    std::vector<cudaEvent_t> ev_pool;
+    cudaEvent_t ev() {
+        if (!ev_pool.empty()) {
+            cudaEvent_t e = ev_pool.back();
+            ev_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        ck(cudaEventCreate(&e), "cudaEventCreate");
+        return e;
+    }
+    explicit Ctx(int dev) : device(dev) {
+        ck(cudaSetDevice(dev), "cudaSetDevice");
+        cudaDeviceProp prop{};
+        ck(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
+        if (prop.major < 10)
+            fail(CARVE_E_CUDA, "device " + std::to_string(dev) + " (" + prop.name +
+                                   ") is not sm_100-class; libcarve_cuda is built for sm_100a only");
+        max_smem_optin = int(prop.sharedMemPerBlockOptin);
+        ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    }
+    ~Ctx() {
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+thread_local std::map<int, std::unique_ptr<Ctx>> t_ctx;
+
+enum KernelKind { KK_ENERGY = 0, KK_DP = 1, KK_COMPACT = 2, KK_UNPACK = 3, KK_PACK = 4, KK_TRANSPOSE = 5, KK_N = 6 };
+
+// RAII bracket: records an event pair around one launch when profiling is on
+struct Prof {
+    Ctx& c;
+    cudaStream_t s;
+    int kind;
+    double bytes;
+    cudaEvent_t a = nullptr;
+    Prof(Ctx& c_, cudaStream_t s_, int kind_, double bytes_) : c(c_), s(s_), kind(kind_), bytes(bytes_) {
+        if (c.prof) {
+            a = c.ev();
+            ck(cudaEventRecord(a, s), "cudaEventRecord");
+        }
+    }
+    ~Prof() {
+        if (a) {
+            cudaEvent_t b = c.ev();
+            cudaEventRecord(b, s);
+            c.prof_recs.push_back({kind, bytes, a, b});
+        }
+    }
+};
+
+Ctx& ctx() {
+    auto it = t_ctx.find(t_device);
+    if (it == t_ctx.end()) {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) fail(CARVE_E_CUDA, "no CUDA device available");
+        if (t_device < 0 || t_device >= n) fail(CARVE_E_CUDA, "invalid device index");
+        it = t_ctx.emplace(t_device, std::make_unique<Ctx>(t_device)).first;
+    }
+    ck(cudaSetDevice(it->second->device), "cudaSetDevice");
+    return *it->second;
+}
+
+void sync(Ctx& c) { ck(cudaStreamSynchronize(c.stream), "cudaStreamSynchronize"); }
+
+int grid_for(long long n, int block, int per_image_cap = 148 * 8) {
+    long long g = (n + block - 1) / block;
+    return int(std::max<long long>(1, std::min<long long>(g, per_image_cap)));
+}
+
+// ---------------------------------------------------------------------------
+// kernel launchers
+
+void launch_unpack(Ctx& c, const uint8_t* in, int W, int H, uint32_t* out, int pitch, int nimg, long long in_is,
+                   long long out_is, cudaStream_t s) {
+    dim3 grid(grid_for((long long)W * H, 256), nimg);
+    k_unpack<<<grid, 256, 0, s>>>(in, W, H, out, pitch, in_is, out_is);
+    LAUNCHED("k_unpack");
+}
+
+void launch_pack(Ctx& c, const uint32_t* in, int pitch, int W, int H, bool transposed, uint8_t* out, int nimg,
+                 long long in_is, long long out_is, cudaStream_t s) {
+    dim3 grid(grid_for((long long)W * H, 256), nimg);
+    if (transposed) k_pack<true><<<grid, 256, 0, s>>>(in, pitch, W, H, out, in_is, out_is);
+    else k_pack<false><<<grid, 256, 0, s>>>(in, pitch, W, H, out, in_is, out_is);
+    LAUNCHED("k_pack");
+}
+
+void launch_transpose(const uint32_t* in, int ipitch, int W, int H, uint32_t* out, int opitch, int nimg,
+                      long long in_is, long long out_is, cudaStream_t s) {
+    dim3 grid((W + 31) / 32, (H + 31) / 32, nimg);
+    k_transpose<<<grid, dim3(32, 8), 0, s>>>(in, ipitch, W, H, out, opitch, in_is, out_is);
+    LAUNCHED("k_transpose");
+}
+
+void launch_energy(const uint32_t* rgb, int pitch, int W, int H, double* e, int nimg, long long is, cudaStream_t s) {
+    dim3 grid((W + K1_TW - 1) / K1_TW, (H + K1_TH - 1) / K1_TH, nimg);
+    k_energy_full<<<grid, 256, 0, s>>>(rgb, pitch, W, H, e, pitch, is, is);
+    LAUNCHED("k_energy_full");
+}
+
+constexpr int kDpSmemBudget = 220 * 1024;
+constexpr int kMaxWinWarps = 16;
+
+struct DpShape {
+    int C, threads, R, nblk, nwin;
+    size_t smem;
+};
+
+DpShape dp_shape(int W, int H) {
+    DpShape d{};
+    const int cands[] = {1, 2, 4, 8, 16};
+    d.C = 0;
+    for (int C : cands) {
+        const int maxt = C >= 8 ? 512 : 1024;
+        if ((W + C - 1) / C <= maxt) {
+            d.C = C;
+            break;
+        }
+    }
+    if (!d.C) fail(CARVE_E_IMAGE_TOO_LARGE, "width " + std::to_string(W) + " exceeds the single-CTA DP limit of 8192");
+    d.threads = int(round_up(std::max(1, (W + d.C - 1) / d.C), 32));
+    const int nw = d.threads / 32;
+    d.nwin = std::min(nw, kMaxWinWarps);
+    const size_t Wl = round_up(W, 8);
+    const size_t win = size_t(d.nwin) * WIN_ROWS * WIN_BYTES;
+    const int rows = H - 1;  // rows carrying a direction
+    if (rows <= 0) {
+        d.R = 1;
+        d.nblk = 0;
+    } else {
+        const size_t budget = kDpSmemBudget - win - 1024;
+        int max_blocks = int(std::max<size_t>(1, budget / (Wl * 2)));
+        int nblk = std::min((rows + 31) / 32, max_blocks);
+        d.R = (rows + nblk - 1) / nblk;
+        d.nblk = (rows + d.R - 1) / d.R;
+    }
+    d.nwin = std::min(d.nwin, std::max(1, d.nblk));
+    d.smem = round_up(size_t(d.nblk) * Wl * 2, 16) + round_up(size_t(d.nblk + 1) * 4, 16) +
+             size_t(d.nwin) * WIN_ROWS * WIN_BYTES;
+    return d;
+}
+
+template <int C, int D>
+void launch_dp_t(Ctx& c, const DpShape& d, const DpParams& p, int nimg, cudaStream_t s) {
+    auto k = k_dp_seam<C, D>;
+    auto it = c.smem_set.find((const void*)k);
+    if (it == c.smem_set.end() || it->second < int(d.smem)) {
+        ck(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kDpSmemBudget),
+           "cudaFuncSetAttribute(dp smem)");
+        c.smem_set[(const void*)k] = kDpSmemBudget;
+    }
+    k<<<nimg, d.threads, d.smem, s>>>(p);
+    LAUNCHED("k_dp_seam");
+}
+
+void launch_dp(Ctx& c, const DpShape& d, const DpParams& p, int nimg, cudaStream_t s) {
+    switch (d.C) {
+        case 1: launch_dp_t<1, 4>(c, d, p, nimg, s); break;
+        case 2: launch_dp_t<2, 4>(c, d, p, nimg, s); break;
+        case 4: launch_dp_t<4, 2>(c, d, p, nimg, s); break;
+        case 8: launch_dp_t<8, 2>(c, d, p, nimg, s); break;
+        default: launch_dp_t<16, 1>(c, d, p, nimg, s); break;
+    }
+}
+
+void launch_compact(const CompactParams& p, int nimg, cudaStream_t s) {
+    const int wpb = 8;
+    dim3 grid((p.H + wpb - 1) / wpb, nimg);
+    k_compact<<<grid, wpb * 32, 0, s>>>(p);
+    LAUNCHED("k_compact");
+}
+
+// ---------------------------------------------------------------------------
+// the resident carve loop: nimg same-size images, packed RGB in -> packed out.
+// Layout per image in the plane buffers: one plane of `plane` elements.
+
+struct CarveGeometry {
+    int w, h, tw, th;
+    int pitch_a, pitch_b;
+    size_t plane;     // elements per image plane (max over both orientations)
+    int dpitch;       // bytes per direction row
+    int dir_rows;
+    size_t seam_ints; // per image
+    int nseams;
+};
+
+CarveGeometry geometry(int w, int h, int tw, int th) {
+    CarveGeometry g{};
+    g.w = w;
+    g.h = h;
+    g.tw = tw;
+    g.th = th;
+    g.pitch_a = int(round_up(w, 32));
+    g.pitch_b = int(round_up(h, 32));
+    g.plane = size_t(g.pitch_a) * h;
+    if (th != h) g.plane = std::max(g.plane, size_t(g.pitch_b) * tw);
+    g.dpitch = int(round_up(std::max(w, h), 16) + 128);
+    g.dir_rows = std::max(h, tw);
+    g.seam_ints = size_t(w - tw) * h + size_t(h - th) * tw;
+    g.nseams = (w - tw) + (h - th);
+    return g;
+}
+
+void check_targets(int w, int h, int tw, int th) {
+    if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "PixelGrid dimensions must be >= 1");
+    if (tw < 1 || tw > w) fail(CARVE_E_INVALID_TARGET, "target width must be in [1, width]");
+    if (th < 1 || th > h) fail(CARVE_E_INVALID_TARGET, "target height must be in [1, height]");
+    // single-CTA DP limit on the widths the solver will see
+    if (tw < w) dp_shape(w, h);
+    if (th < h) dp_shape(h, tw);
+}
+
+// stamps layout per image: [4 per seam: dp start/end, compact start/end] then
+// [4: energy full start/end for phase A, phase B]
+size_t stamp_words(const CarveGeometry& g) { return size_t(g.nseams) * 4 + 4; }
+
+void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const CarveGeometry& g, int* d_seams,
+               size_t seam_istride, unsigned long long* d_stamps, cudaStream_t s) {
+    const long long in_is = (long long)g.w * g.h * 3, out_is = (long long)g.tw * g.th * 3;
+    uint32_t* rgb[2] = {c.rgb[0].as<uint32_t>(), c.rgb[1].as<uint32_t>()};
+    double* e[2] = {c.e[0].as<double>(), c.e[1].as<double>()};
+    uint8_t* dir = c.dir.as<uint8_t>();
+    const long long pis = (long long)g.plane;
+    const long long dis = (long long)g.dpitch * g.dir_rows;
+    const size_t sw = stamp_words(g);
+    int cur = 0;
+    {
+        Prof pr(c, s, KK_UNPACK, 7.0 * g.w * g.h * nimg);
+        launch_unpack(c, d_in, g.w, g.h, rgb[cur], g.pitch_a, nimg, in_is, pis, s);
+    }
+
+    auto phase = [&](int W0, int H, int ntake, int pitch, int seam_base, int stamp_seam0, int estamp) {
+        if (ntake <= 0) return;
+        {
+            // algorithmic bytes: 3 B RGB read + 8 B FP64 write per pixel
+            Prof pr(c, s, KK_ENERGY, 11.0 * W0 * H * nimg);
+            launch_energy(rgb[cur], pitch, W0, H, e[cur], nimg, pis, s);
+        }
+        (void)estamp;
+        for (int k = 0; k < ntake; ++k) {
+            const int W = W0 - k;
+            const DpShape d = dp_shape(W, H);
+            DpParams p{};
+            p.e = e[cur];
+            p.epitch = pitch;
+            p.W = W;
+            p.H = H;
+            p.dir = dir;
+            p.dpitch = g.dpitch;
+            p.R = d.R;
+            p.nblk = d.nblk;
+            p.nwin = d.nwin;
+            p.seam = d_seams + seam_base + size_t(k) * H;
+            p.stamps = d_stamps ? d_stamps + size_t(stamp_seam0 + k) * 4 : nullptr;
+            p.e_istride = pis;
+            p.d_istride = dis;
+            p.s_istride = (long long)seam_istride;
+            p.st_istride = (long long)sw;
+            {
+                // 8 B FP64 energy read + 1 B direction write per cell
+                Prof pr(c, s, KK_DP, 9.0 * W * H * nimg);
+                launch_dp(c, d, p, nimg, s);
+            }
+            CompactParams q{};
+            q.rgb_in = rgb[cur];
+            q.rgb_out = rgb[cur ^ 1];
+            const bool last = (k + 1 == ntake);
+            q.e_in = last ? nullptr : e[cur];  // the final width needs no energy
+            q.e_out = e[cur ^ 1];
+            q.pitch = pitch;
+            q.W = W;
+            q.H = H;
+            q.seam = p.seam;
+            q.stamps = d_stamps ? d_stamps + size_t(stamp_seam0 + k) * 4 + 2 : nullptr;
+            q.p_istride = pis;
+            q.s_istride = (long long)seam_istride;
+            q.st_istride = (long long)sw;
+            {
+                // read W, write W-1 per row: 3 B RGB (+ 8 B FP64 energy) per element
+                Prof pr(c, s, KK_COMPACT, (last ? 3.0 : 11.0) * H * (2.0 * W - 1) * nimg);
+                launch_compact(q, nimg, s);
+            }
+            cur ^= 1;
+        }
+    };
+    phase(g.w, g.h, g.w - g.tw, g.pitch_a, 0, 0, 0);
+    if (g.th != g.h) {
+        {
+            Prof pr(c, s, KK_TRANSPOSE, 8.0 * g.tw * g.h * nimg);
+            launch_transpose(rgb[cur], g.pitch_a, g.tw, g.h, rgb[cur ^ 1], g.pitch_b, nimg, pis, pis, s);
+        }
+        cur ^= 1;
+        phase(g.h, g.tw, g.h - g.th, g.pitch_b, (g.w - g.tw) * g.h, g.w - g.tw, 2);
+        Prof pr(c, s, KK_PACK, 7.0 * g.tw * g.th * nimg);
+        launch_pack(c, rgb[cur], g.pitch_b, g.tw, g.th, true, d_out, nimg, pis, out_is, s);
+    } else {
+        Prof pr(c, s, KK_PACK, 7.0 * g.tw * g.th * nimg);
+        launch_pack(c, rgb[cur], g.pitch_a, g.tw, g.th, false, d_out, nimg, pis, out_is, s);
+    }
+}
+
+void ensure_carve_buffers(Ctx& c, const CarveGeometry& g, int nimg) {
+    for (int k = 0; k < 2; ++k) {
+        c.rgb[k].ensure(g.plane * 4 * nimg);
+        c.e[k].ensure(g.plane * 8 * nimg);
+    }
+    c.dir.ensure(size_t(g.dpitch) * g.dir_rows * nimg + 256);
+}
+
+// ---------------------------------------------------------------------------
+// bench.hpp:67-94 make_test_image (host fixture generator)
+
+void make_test_image_host(int w, int h, uint32_t variant, uint8_t* out) {
+    uint32_t s = 0x9E3779B9u ^ (uint32_t(w) * 2654435761u) ^ uint32_t(h);
+    if (variant) {
+        s ^= variant;
+        if (!s) s = 1u;
+    }
+    auto next = [&s] {
+        s ^= s << 13;
+        s ^= s >> 17;
+        s ^= s << 5;
+        return s;
+    };
+    auto clampd = [](double v, double lo, double hi) { return std::clamp(v, lo, hi); };
+    const double pi = 3.14159265358979323846;
+    for (int i = 0; i < h; ++i)
+        for (int j = 0; j < w; ++j) {
+            const double u = double(i) / std::max(1, h - 1);
+            const double v = double(j) / std::max(1, w - 1);
+            double base = 60.0 + 70.0 * (u + v) / 2.0 + 45.0 * std::sin(3.0 * pi * u) * std::cos(3.0 * pi * v);
+            if (u > 0.33 && u < 0.66 && v > 0.25 && v < 0.75) base += (((i / 3) + (j / 3)) % 2) ? 55.0 : -55.0;
+            const int n1 = int(next() % 37) - 18;
+            const int n2 = int(next() % 37) - 18;
+            const int n3 = int(next() % 37) - 18;
+            uint8_t* p = out + (size_t(i) * w + j) * 3;
+            p[0] = uint8_t(clampd(base + n1, 0.0, 255.0));
+            p[1] = uint8_t(clampd(base * 0.85 + 24.0 + n2, 8.0, 255.0));
+            p[2] = uint8_t(clampd(210.0 - base * 0.55 + n3, 0.0, 255.0));
+        }
+}
+
+void validate_seam_host(const int32_t* seam, int n, int w, int h) {
+    if (n != h) fail(CARVE_E_INVALID_SEAM, "seam length does not match image height");
+    for (int i = 0; i < n; ++i) {
+        if (seam[i] < 0 || seam[i] >= w) fail(CARVE_E_INVALID_SEAM, "seam column out of range");
+        if (i > 0 && std::abs(seam[i] - seam[i - 1]) > 1) fail(CARVE_E_INVALID_SEAM, "seam is not connected");
+    }
+}
+
+void carve_one_host(Ctx& c, const uint8_t* rgb, int w, int h, int tw, int th, uint8_t* out, int32_t* seams_out,
+                    carve_seam_timing* timings) {
+    const CarveGeometry g = geometry(w, h, tw, th);
+    cudaStream_t s = c.stream;
+    const size_t in_bytes = size_t(w) * h * 3, out_bytes = size_t(tw) * th * 3;
+    uint8_t* d_in = static_cast<uint8_t*>(c.packed_in.ensure(in_bytes));
+    uint8_t* d_out = static_cast<uint8_t*>(c.packed_out.ensure(out_bytes));
+    ensure_carve_buffers(c, g, 1);
+    int* d_seams = static_cast<int*>(c.seams.ensure(std::max<size_t>(g.seam_ints, 1) * 4));
+    unsigned long long* d_st = nullptr;
+    if (timings) {
+        d_st = static_cast<unsigned long long*>(c.stamps.ensure(stamp_words(g) * 8));
+        ck(cudaMemsetAsync(d_st, 0, stamp_words(g) * 8, s), "memset stamps");
+    }
+    ck(cudaMemcpyAsync(d_in, rgb, in_bytes, cudaMemcpyHostToDevice, s), "H2D rgb");
+    run_carve(c, d_in, d_out, 1, g, d_seams, g.seam_ints, d_st, s);
+    ck(cudaMemcpyAsync(out, d_out, out_bytes, cudaMemcpyDeviceToHost, s), "D2H rgb");
+    if (seams_out && g.seam_ints)
+        ck(cudaMemcpyAsync(seams_out, d_seams, g.seam_ints * 4, cudaMemcpyDeviceToHost, s), "D2H seams");
+    std::vector<unsigned long long> st;
+    if (timings) {
+        st.resize(stamp_words(g));
+        ck(cudaMemcpyAsync(st.data(), d_st, st.size() * 8, cudaMemcpyDeviceToHost, s), "D2H stamps");
+    }
+    sync(c);
+    if (timings) {
+        for (int k = 0; k < g.nseams; ++k) {
+            const unsigned long long* q = &st[size_t(k) * 4];
+            timings[k].energy_s = 0.0;
+            timings[k].solve_s = q[1] > q[0] ? double(q[1] - q[0]) * 1e-9 : 0.0;
+            timings[k].remove_s = q[3] > q[2] ? double(q[3] - q[2]) * 1e-9 : 0.0;
+        }
+    }
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* carve_cuda_last_error(void) { return t_err.c_str(); }
+const char* carve_cuda_version(void) { return "carve_cuda 0.1 (sm_100a)"; }
+
+int carve_cuda_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+carve_status carve_cuda_set_device(int device) {
+    return guarded([&] {
+        const int n = carve_cuda_device_count();
+        if (device < 0 || device >= n) fail(CARVE_E_CUDA, "invalid device index " + std::to_string(device));
+        t_device = device;
+    });
+}
+
+uint64_t carve_cuda_launch_count(void) { return t_launches; }
+
+carve_status carve_cuda_set_kernel_events(int on) {
+    return guarded([&] {
+        Ctx& c = ctx();
+        c.prof = on != 0;
+        for (auto& r : c.prof_recs) {
+            c.ev_pool.push_back(r.a);
+            c.ev_pool.push_back(r.b);
+        }
+        c.prof_recs.clear();
+    });
+}
+
+carve_status carve_cuda_kernel_event_stats(int kind, double* ms_total, uint64_t* launches, double* bytes_total) {
+    return guarded([&] {
+        Ctx& c = ctx();
+        sync(c);
+        double ms = 0.0, bytes = 0.0;
+        uint64_t n = 0;
+        for (auto& r : c.prof_recs)
+            if (r.kind == kind) {
+                float x = 0.f;
+                ck(cudaEventElapsedTime(&x, r.a, r.b), "cudaEventElapsedTime");
+                ms += x;
+                bytes += r.bytes;
+                ++n;
+            }
+        *ms_total = ms;
+        *launches = n;
+        *bytes_total = bytes;
+    });
+}
+void carve_cuda_reset_launch_count(void) { t_launches = 0; }
+
+carve_status carve_make_test_image(int w, int h, uint32_t variant, uint8_t* out) {
+    return guarded([&] {
+        if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "PixelGrid dimensions must be >= 1");
+        make_test_image_host(w, h, variant, out);
+    });
+}
+
+carve_status carve_cuda_validate_seam(const int32_t* seam, int n, int w, int h) {
+    return guarded([&] { validate_seam_host(seam, n, w, h); });
+}
+
+carve_status carve_cuda_to_grayscale(const uint8_t* rgb, int w, int h, double* luma_out) {
+    return guarded([&] {
+        if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "PixelGrid dimensions must be >= 1");
+        Ctx& c = ctx();
+        const int pitch = int(round_up(w, 32));
+        uint8_t* d_in = static_cast<uint8_t*>(c.packed_in.ensure(size_t(w) * h * 3));
+        uint32_t* plane = static_cast<uint32_t*>(c.rgb[0].ensure(size_t(pitch) * h * 4));
+        double* l = static_cast<double*>(c.scratch_a.ensure(size_t(w) * h * 8));
+        ck(cudaMemcpyAsync(d_in, rgb, size_t(w) * h * 3, cudaMemcpyHostToDevice, c.stream), "H2D");
+        launch_unpack(c, d_in, w, h, plane, pitch, 1, 0, 0, c.stream);
+        k_luma<<<grid_for((long long)w * h, 256), 256, 0, c.stream>>>(plane, pitch, w, h, l);
+        LAUNCHED("k_luma");
+        ck(cudaMemcpyAsync(luma_out, l, size_t(w) * h * 8, cudaMemcpyDeviceToHost, c.stream), "D2H");
+        sync(c);
+    });
+}
+
+carve_status carve_cuda_energy_e1_rgb(const uint8_t* rgb, int w, int h, double* e_out) {
+    return guarded([&] {
+        if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "PixelGrid dimensions must be >= 1");
+        Ctx& c = ctx();
+        const int pitch = int(round_up(w, 32));
+        uint8_t* d_in = static_cast<uint8_t*>(c.packed_in.ensure(size_t(w) * h * 3));
+        uint32_t* plane = static_cast<uint32_t*>(c.rgb[0].ensure(size_t(pitch) * h * 4));
+        double* e = static_cast<double*>(c.e[0].ensure(size_t(pitch) * h * 8));
+        ck(cudaMemcpyAsync(d_in, rgb, size_t(w) * h * 3, cudaMemcpyHostToDevice, c.stream), "H2D");
+        launch_unpack(c, d_in, w, h, plane, pitch, 1, 0, 0, c.stream);
+        launch_energy(plane, pitch, w, h, e, 1, 0, c.stream);
+        ck(cudaMemcpy2DAsync(e_out, size_t(w) * 8, e, size_t(pitch) * 8, size_t(w) * 8, h, cudaMemcpyDeviceToHost,
+                             c.stream),
+           "D2H");
+        sync(c);
+    });
+}
+
+carve_status carve_cuda_energy_e1_luma(const double* luma, int w, int h, double* e_out) {
+    return guarded([&] {
+        if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "LumaGrid dimensions must be >= 1");
+        Ctx& c = ctx();
+        double* l = static_cast<double*>(c.scratch_a.ensure(size_t(w) * h * 8));
+        double* e = static_cast<double*>(c.scratch_b.ensure(size_t(w) * h * 8));
+        ck(cudaMemcpyAsync(l, luma, size_t(w) * h * 8, cudaMemcpyHostToDevice, c.stream), "H2D");
+        k_energy_luma<<<grid_for((long long)w * h, 256), 256, 0, c.stream>>>(l, w, h, e);
+        LAUNCHED("k_energy_luma");
+        ck(cudaMemcpyAsync(e_out, e, size_t(w) * h * 8, cudaMemcpyDeviceToHost, c.stream), "D2H");
+        sync(c);
+    });
+}
+
+carve_status carve_cuda_transpose_rgb(const uint8_t* rgb, int w, int h, uint8_t* out) {
+    return guarded([&] {
+        if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "PixelGrid dimensions must be >= 1");
+        Ctx& c = ctx();
+        const int pa = int(round_up(w, 32)), pb = int(round_up(h, 32));
+        uint8_t* d_in = static_cast<uint8_t*>(c.packed_in.ensure(size_t(w) * h * 3));
+        uint8_t* d_out = static_cast<uint8_t*>(c.packed_out.ensure(size_t(w) * h * 3));
+        uint32_t* a = static_cast<uint32_t*>(c.rgb[0].ensure(size_t(pa) * h * 4));
+        uint32_t* b = static_cast<uint32_t*>(c.rgb[1].ensure(size_t(pb) * w * 4));
+        ck(cudaMemcpyAsync(d_in, rgb, size_t(w) * h * 3, cudaMemcpyHostToDevice, c.stream), "H2D");
+        launch_unpack(c, d_in, w, h, a, pa, 1, 0, 0, c.stream);
+        launch_transpose(a, pa, w, h, b, pb, 1, 0, 0, c.stream);
+        launch_pack(c, b, pb, h, w, false, d_out, 1, 0, 0, c.stream);
+        ck(cudaMemcpyAsync(out, d_out, size_t(w) * h * 3, cudaMemcpyDeviceToHost, c.stream), "D2H");
+        sync(c);
+    });
+}
+
+carve_status carve_cuda_dp_seam(const double* e, int w, int h, double* m_out, int32_t* b_out, int32_t* seam_out) {
+    return guarded([&] {
+        if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "image is empty");
+        if ((m_out == nullptr) != (b_out == nullptr)) fail(CARVE_E_USAGE_ERROR, "m_out and b_out go together");
+        Ctx& c = ctx();
+        const DpShape d = dp_shape(w, h);
+        const int pitch = int(round_up(w, 32));
+        const int dpitch = int(round_up(w, 16) + 128);
+        double* de = static_cast<double*>(c.e[0].ensure(size_t(pitch) * h * 8));
+        uint8_t* dir = static_cast<uint8_t*>(c.dir.ensure(size_t(dpitch) * h + 256));
+        int* dseam = static_cast<int*>(c.seams.ensure(size_t(h) * 4));
+        double* dm = nullptr;
+        int* db = nullptr;
+        if (m_out) {
+            dm = static_cast<double*>(c.scratch_a.ensure(size_t(w) * h * 8));
+            db = static_cast<int*>(c.scratch_b.ensure(size_t(w) * h * 4));
+        }
+        ck(cudaMemcpy2DAsync(de, size_t(pitch) * 8, e, size_t(w) * 8, size_t(w) * 8, h, cudaMemcpyHostToDevice,
+                             c.stream),
+           "H2D energy");
+        DpParams p{};
+        p.e = de;
+        p.epitch = pitch;
+        p.W = w;
+        p.H = h;
+        p.dir = dir;
+        p.dpitch = dpitch;
+        p.R = d.R;
+        p.nblk = d.nblk;
+        p.nwin = d.nwin;
+        p.seam = dseam;
+        p.m_out = dm;
+        p.b_out = db;
+        launch_dp(c, d, p, 1, c.stream);
+        ck(cudaMemcpyAsync(seam_out, dseam, size_t(h) * 4, cudaMemcpyDeviceToHost, c.stream), "D2H seam");
+        if (m_out) {
+            ck(cudaMemcpyAsync(m_out, dm, size_t(w) * h * 8, cudaMemcpyDeviceToHost, c.stream), "D2H m");
+            ck(cudaMemcpyAsync(b_out, db, size_t(w) * h * 4, cudaMemcpyDeviceToHost, c.stream), "D2H b");
+        }
+        sync(c);
+    });
+}
+
+carve_status carve_cuda_remove_seam_rgb(const uint8_t* rgb, int w, int h, const int32_t* seam, int n, uint8_t* out) {
+    return guarded([&] {
+        validate_seam_host(seam, n, w, h);  // carver.hpp:72
+        if (w < 2) fail(CARVE_E_WIDTH_TOO_SMALL, "cannot remove a seam from a 1-pixel-wide image");
+        Ctx& c = ctx();
+        const int pitch = int(round_up(w, 32));
+        uint8_t* d_in = static_cast<uint8_t*>(c.packed_in.ensure(size_t(w) * h * 3));
+        uint8_t* d_out = static_cast<uint8_t*>(c.packed_out.ensure(size_t(w - 1) * h * 3));
+        uint32_t* a = static_cast<uint32_t*>(c.rgb[0].ensure(size_t(pitch) * h * 4));
+        uint32_t* b = static_cast<uint32_t*>(c.rgb[1].ensure(size_t(pitch) * h * 4));
+        int* ds = static_cast<int*>(c.seams.ensure(size_t(h) * 4));
+        ck(cudaMemcpyAsync(d_in, rgb, size_t(w) * h * 3, cudaMemcpyHostToDevice, c.stream), "H2D");
+        ck(cudaMemcpyAsync(ds, seam, size_t(h) * 4, cudaMemcpyHostToDevice, c.stream), "H2D seam");
+        launch_unpack(c, d_in, w, h, a, pitch, 1, 0, 0, c.stream);
+        CompactParams q{};
+        q.rgb_in = a;
+        q.rgb_out = b;
+        q.pitch = pitch;
+        q.W = w;
+        q.H = h;
+        q.seam = ds;
+        launch_compact(q, 1, c.stream);
+        launch_pack(c, b, pitch, w - 1, h, false, d_out, 1, 0, 0, c.stream);
+        ck(cudaMemcpyAsync(out, d_out, size_t(w - 1) * h * 3, cudaMemcpyDeviceToHost, c.stream), "D2H");
+        sync(c);
+    });
+}
+
+carve_status carve_cuda_carve(const uint8_t* rgb, int w, int h, int target_w, int target_h, uint8_t* rgb_out,
+                              int32_t* seams_out, carve_seam_timing* timings_out) {
+    return guarded([&] {
+        check_targets(w, h, target_w, target_h);
+        Ctx& c = ctx();
+        carve_one_host(c, rgb, w, h, target_w, target_h, rgb_out, seams_out, timings_out);
+    });
+}
+
+carve_status carve_cuda_carve_device(const uint8_t* d_rgb, int w, int h, int target_w, int target_h, uint8_t* d_out,
+                                     int32_t* d_seams, void* stream) {
+    return guarded([&] {
+        check_targets(w, h, target_w, target_h);
+        Ctx& c = ctx();
+        const CarveGeometry g = geometry(w, h, target_w, target_h);
+        ensure_carve_buffers(c, g, 1);
+        int* seams = d_seams ? d_seams : static_cast<int*>(c.seams.ensure(std::max<size_t>(g.seam_ints, 1) * 4));
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c.stream;
+        run_carve(c, d_rgb, d_out, 1, g, seams, g.seam_ints, nullptr, s);
+    });
+}
+
+carve_status carve_cuda_carve_batch_device(const uint8_t* d_rgb, int n, int w, int h, int target_w, int target_h,
+                                           uint8_t* d_out, void* stream) {
+    return guarded([&] {
+        if (n < 1) fail(CARVE_E_EMPTY_INPUT, "empty batch");
+        check_targets(w, h, target_w, target_h);
+        Ctx& c = ctx();
+        const CarveGeometry g = geometry(w, h, target_w, target_h);
+        ensure_carve_buffers(c, g, n);
+        int* seams = static_cast<int*>(c.seams.ensure(std::max<size_t>(g.seam_ints, 1) * 4 * n));
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c.stream;
+        run_carve(c, d_rgb, d_out, n, g, seams, std::max<size_t>(g.seam_ints, 1), nullptr, s);
+    });
+}
+
+carve_status carve_cuda_carve_batch(const uint8_t* const* rgb, int n, int w, int h, int target_w, int target_h,
+                                    uint8_t* const* rgb_out, const int* devices, int ndev) {
+    return guarded([&] {
+        if (n < 1) fail(CARVE_E_EMPTY_INPUT, "empty batch");
+        check_targets(w, h, target_w, target_h);
+        const int avail = carve_cuda_device_count();
+        if (avail == 0) fail(CARVE_E_CUDA, "no CUDA device available");
+        if (ndev <= 0) ndev = avail;
+        std::vector<int> devs(ndev);
+        for (int k = 0; k < ndev; ++k) {
+            devs[k] = devices ? devices[k] : k;
+            if (devs[k] < 0 || devs[k] >= avail) fail(CARVE_E_CUDA, "invalid device index");
+        }
+        const CarveGeometry g = geometry(w, h, target_w, target_h);
+        const size_t in_bytes = size_t(w) * h * 3, out_bytes = size_t(target_w) * target_h * 3;
+        // per-image device footprint -> chunk size (keep well inside 180 GB HBM)
+        const size_t per_img = g.plane * 24 + size_t(g.dpitch) * g.dir_rows + in_bytes + out_bytes + g.seam_ints * 4;
+        const int chunk_cap = int(std::max<size_t>(1, (size_t(48) << 30) / per_img));
+        std::vector<int> status(ndev, CARVE_OK);
+        std::vector<std::string> msgs(ndev);
+        auto worker = [&](int k) {
+            const int lo = int((long long)n * k / ndev), hi = int((long long)n * (k + 1) / ndev);
+            if (lo >= hi) return;
+            t_device = devs[k];
+            status[k] = guarded([&] {
+                Ctx& c = ctx();
+                for (int b0 = lo; b0 < hi; b0 += chunk_cap) {
+                    const int m = std::min(chunk_cap, hi - b0);
+                    uint8_t* d_in = static_cast<uint8_t*>(c.packed_in.ensure(in_bytes * m));
+                    uint8_t* d_out = static_cast<uint8_t*>(c.packed_out.ensure(out_bytes * m));
+                    ensure_carve_buffers(c, g, m);
+                    int* seams = static_cast<int*>(c.seams.ensure(std::max<size_t>(g.seam_ints, 1) * 4 * m));
+                    for (int q = 0; q < m; ++q)
+                        ck(cudaMemcpyAsync(d_in + in_bytes * q, rgb[b0 + q], in_bytes, cudaMemcpyHostToDevice,
+                                           c.stream),
+                           "H2D");
+                    run_carve(c, d_in, d_out, m, g, seams, std::max<size_t>(g.seam_ints, 1), nullptr, c.stream);
+                    for (int q = 0; q < m; ++q)
+                        ck(cudaMemcpyAsync(rgb_out[b0 + q], d_out + out_bytes * q, out_bytes, cudaMemcpyDeviceToHost,
+                                           c.stream),
+                           "D2H");
+                    sync(c);
+                }
+            });
+            msgs[k] = t_err;
+        };
+        std::vector<std::thread> pool;
+        for (int k = 1; k < ndev; ++k) pool.emplace_back(worker, k);
+        const int saved = t_device;
+        worker(0);
+        t_device = saved;
+        for (auto& th : pool) th.join();
+        for (int k = 0; k < ndev; ++k)
+            if (status[k]) fail(status[k], msgs[k]);
+    });
+}
+
+}  // extern "C"

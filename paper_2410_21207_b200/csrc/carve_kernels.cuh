@@ -1,0 +1,570 @@
+// carve_kernels.cuh — the four sm_100a kernels of the seam-carving hot path.
+//
+//   K1  energy stencil        k_energy_full   (energy.hpp:82-98 + raster.hpp:61-71)
+//       + 2-column fix-up     inside k_compact
+//   K2  cumulative-energy DP  k_dp_seam       (solvers.hpp:116-157, 263-289)
+//   K3  argmin + backtrack    tail of k_dp_seam (solvers.hpp:94-111)
+//   K4  seam removal          k_compact       (carver.hpp:71-98), transposing
+//                             variants for horizontal seams (carver.hpp:216-222)
+//
+// Arithmetic contract: every FP64 operation is an
+// explicit round-to-nearest intrinsic (__dmul_rn/__dadd_rn/__dsub_rn) so no
+// FMA contraction can occur, matching the reference built for baseline
+// x86-64. The whole library is also compiled with -fmad=false.
+//
+// Device layout: pixels are RGBX uint32 (r | g<<8 | b<<16),
+// energy is FP64, both row-major with a fixed pitch (a multiple of 32
+// elements) that does not change as the width shrinks; DP directions are one
+// byte per cell (0: from j-1, 1: from j, 2: from j+1).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace carve_dev {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
+
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// raster.hpp:68 — 0.299*r + 0.587*g + 0.114*b, left to right, no contraction.
+__device__ __forceinline__ double luma(uint32_t p) {
+    const double r = double(p & 0xffu), g = double((p >> 8) & 0xffu), b = double((p >> 16) & 0xffu);
+    return __dadd_rn(__dadd_rn(__dmul_rn(0.299, r), __dmul_rn(0.587, g)), __dmul_rn(0.114, b));
+}
+
+// energy.hpp:95 — |gx| + |gy|, x term first.
+__device__ __forceinline__ double e1(double l_left, double l_right, double l_up, double l_down) {
+    return __dadd_rn(fabs(__dsub_rn(l_right, l_left)), fabs(__dsub_rn(l_down, l_up)));
+}
+
+// ---------------------------------------------------------------------------
+// layout conversion (host boundary): packed RGB bytes <-> RGBX plane
+
+__global__ void k_unpack(const uint8_t* __restrict__ in, int W, int H, uint32_t* __restrict__ out, int pitch,
+                         long long in_istride, long long out_istride) {
+    in += blockIdx.y * in_istride;
+    out += blockIdx.y * out_istride;
+    const long long n = (long long)W * H;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const int i = int(k / W), j = int(k - (long long)i * W);
+        const uint8_t* p = in + 3 * k;
+        out[(long long)i * pitch + j] = uint32_t(p[0]) | (uint32_t(p[1]) << 8) | (uint32_t(p[2]) << 16);
+    }
+}
+
+// transposed==true: the plane holds the image transposed (plane row = image column).
+template <bool transposed>
+__global__ void k_pack(const uint32_t* __restrict__ in, int pitch, int W, int H, uint8_t* __restrict__ out,
+                       long long in_istride, long long out_istride) {
+    in += blockIdx.y * in_istride;
+    out += blockIdx.y * out_istride;
+    const long long n = (long long)W * H;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const int i = int(k / W), j = int(k - (long long)i * W);
+        const uint32_t p = transposed ? in[(long long)j * pitch + i] : in[(long long)i * pitch + j];
+        uint8_t* o = out + 3 * k;
+        o[0] = uint8_t(p);
+        o[1] = uint8_t(p >> 8);
+        o[2] = uint8_t(p >> 16);
+    }
+}
+
+// 32x32 tiled transpose of an RGBX plane (raster.hpp:73-79): out(j, i) = in(i, j).
+__global__ void k_transpose(const uint32_t* __restrict__ in, int ipitch, int W, int H, uint32_t* __restrict__ out,
+                            int opitch, long long in_istride, long long out_istride) {
+    __shared__ uint32_t tile[32][33];
+    in += blockIdx.z * in_istride;
+    out += blockIdx.z * out_istride;
+    const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int i = by + r, j = bx + threadIdx.x;
+        if (i < H && j < W) tile[r][threadIdx.x] = in[(long long)i * ipitch + j];
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int j = bx + r, i = by + threadIdx.x;  // out row j, col i
+        if (i < H && j < W) out[(long long)j * opitch + i] = tile[threadIdx.x][r];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1 — full energy map. 64x16 output tile per 256-thread CTA; the (16+2) x
+// (64+2) luma tile (edge-replicated, raster.hpp:54-58) is staged in shared
+// memory from 128-bit coalesced RGBX loads; each thread writes 4 energies as
+// two 128-bit stores. Algorithmic traffic: 4 B read + 8 B written per pixel.
+
+constexpr int K1_TW = 64, K1_TH = 16;
+
+__device__ __forceinline__ void k1_tile(const uint32_t* __restrict__ rgb, int pitch, int W, int H,
+                                        double* __restrict__ e, int epitch, int i0, int j0,
+                                        double (*L)[K1_TW + 2]) {
+    const int t = threadIdx.x;
+    // interior columns: 18 rows x 16 chunks of 4 pixels
+    for (int item = t; item < (K1_TH + 2) * (K1_TW / 4); item += blockDim.x) {
+        const int r = item / (K1_TW / 4), q = item % (K1_TW / 4);
+        const int gi = min(max(i0 + r - 1, 0), H - 1);
+        const int gj = j0 + 4 * q;
+        const uint32_t* row = rgb + (long long)gi * pitch;
+        uint32_t px[4];
+        if (gj + 3 < W) {
+            const uint4 v = *reinterpret_cast<const uint4*>(row + gj);
+            px[0] = v.x; px[1] = v.y; px[2] = v.z; px[3] = v.w;
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) px[u] = row[min(gj + u, W - 1)];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) L[r][1 + 4 * q + u] = luma(px[u]);
+    }
+    // halo columns j0-1 and j0+64
+    for (int item = t; item < (K1_TH + 2) * 2; item += blockDim.x) {
+        const int r = item >> 1, side = item & 1;
+        const int gi = min(max(i0 + r - 1, 0), H - 1);
+        const int gj = side ? min(j0 + K1_TW, W - 1) : max(j0 - 1, 0);
+        L[r][side ? K1_TW + 1 : 0] = luma(rgb[(long long)gi * pitch + gj]);
+    }
+    __syncthreads();
+    {
+        const int r = t / (K1_TW / 4), q = t % (K1_TW / 4);
+        const int gi = i0 + r;
+        if (gi < H) {
+            double out[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int c = 1 + 4 * q + u;
+                // clamped columns: for the last real column the right neighbour
+                // must be itself (at_clamped); smem col c+1 holds column gj+1
+                // clamped only at the tile edge, so clamp explicitly here.
+                const int gj = j0 + 4 * q + u;
+                const int cr = (gj + 1 < W) ? c + 1 : c;
+                const int cl = (gj - 1 >= 0) ? c - 1 : c;
+                out[u] = e1(L[r + 1][cl], L[r + 1][cr], L[r][c], L[r + 2][c]);
+            }
+            double* erow = e + (long long)gi * epitch;
+            const int gj = j0 + 4 * q;
+            if (gj + 3 < W) {
+                *reinterpret_cast<double2*>(erow + gj) = make_double2(out[0], out[1]);
+                *reinterpret_cast<double2*>(erow + gj + 2) = make_double2(out[2], out[3]);
+            } else {
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (gj + u < W) erow[gj + u] = out[u];
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_energy_full(const uint32_t* __restrict__ rgb, int pitch, int W, int H,
+                                                     double* __restrict__ e, int epitch, long long rgb_istride,
+                                                     long long e_istride) {
+    __shared__ double L[K1_TH + 2][K1_TW + 2];
+    rgb += blockIdx.z * rgb_istride;
+    e += blockIdx.z * e_istride;
+    k1_tile(rgb, pitch, W, H, e, epitch, blockIdx.y * K1_TH, blockIdx.x * K1_TW, L);
+}
+
+// Luma plane -> e1 (the LumaGrid overload of energy_e1, energy.hpp:89-98).
+__global__ void k_energy_luma(const double* __restrict__ l, int W, int H, double* __restrict__ e) {
+    const long long n = (long long)W * H;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const int i = int(k / W), j = int(k - (long long)i * W);
+        const double* row = l + (long long)i * W;
+        const double lft = row[max(j - 1, 0)], rgt = row[min(j + 1, W - 1)];
+        const double up = l[(long long)max(i - 1, 0) * W + j], dn = l[(long long)min(i + 1, H - 1) * W + j];
+        e[k] = e1(lft, rgt, up, dn);
+    }
+}
+
+__global__ void k_luma(const uint32_t* __restrict__ rgb, int pitch, int W, int H, double* __restrict__ out) {
+    const long long n = (long long)W * H;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const int i = int(k / W), j = int(k - (long long)i * W);
+        out[k] = luma(rgb[(long long)i * pitch + j]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2 + K3 — cumulative-energy DP, argmin and backtrack for one image per CTA.
+//
+// Thread t owns C consecutive columns [t*C, t*C+C) and keeps the previous
+// row's cumulative cost M in registers. Neighbour values cross lanes with
+// warp shuffles and cross warps through a double-buffered shared-memory edge
+// slot, one __syncthreads per row. Out-of-range neighbours are +inf, which is
+// equivalent to the reference's candidate exclusion because
+// the middle candidate is always finite. The scan order left, mid, right with
+// strict < reproduces fill_row_span's tie-break (solvers.hpp:136-145).
+//
+// Backtrack without a serial H-step chain: rows 1..H-1 are cut into nblk
+// blocks of R rows. Alongside M each cell carries a label = the column at
+// the row above the block from which its optimal path descends (propagated
+// with the same neighbour exchange as M). The label row of each block's last
+// row is kept in shared memory, so the block-boundary columns of the seam
+// follow from nblk shared-memory lookups (phase 1). Each block's rows are
+// then recovered in parallel, one warp per block, from the stored per-cell
+// directions, 32 rows at a time through a 32x80-byte shared-memory window
+// loaded with independent 128-bit loads (phase 2).
+
+struct DpParams {
+    const double* e;
+    int epitch;
+    int W, H;
+    uint8_t* dir;
+    int dpitch;
+    int R, nblk, nwin;
+    int* seam;
+    double* m_out;  // optional full cost table (pitch W)
+    int* b_out;     // optional predecessor table (pitch W)
+    unsigned long long* stamps;  // optional [start, end] per image
+    long long e_istride, d_istride, s_istride, st_istride;
+};
+
+constexpr int WIN_ROWS = 32, WIN_BYTES = 80;
+
+template <int C>
+__device__ __forceinline__ void load_cols(const double* __restrict__ row, int j0, int W, double (&v)[C]) {
+    if (j0 + C <= W) {
+        if constexpr (C == 1) {
+            v[0] = __ldg(row + j0);
+        } else {
+#pragma unroll
+            for (int k = 0; k < C; k += 2) {
+                const double2 x = __ldg(reinterpret_cast<const double2*>(row + j0 + k));
+                v[k] = x.x;
+                v[k + 1] = x.y;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < C; ++k) v[k] = (j0 + k < W) ? __ldg(row + j0 + k) : 0.0;
+    }
+}
+
+template <int C>
+__device__ __forceinline__ void store_dirs(uint8_t* p, const uint32_t (&dw)[(C + 3) / 4]) {
+    if constexpr (C == 1) *p = uint8_t(dw[0]);
+    else if constexpr (C == 2) *reinterpret_cast<uint16_t*>(p) = uint16_t(dw[0]);
+    else if constexpr (C == 4) *reinterpret_cast<uint32_t*>(p) = dw[0];
+    else if constexpr (C == 8) *reinterpret_cast<uint2*>(p) = make_uint2(dw[0], dw[1]);
+    else *reinterpret_cast<uint4*>(p) = make_uint4(dw[0], dw[1], dw[2], dw[3]);
+}
+
+// columns per thread -> max threads per CTA (register budget: C >= 8 needs > 64 regs)
+template <int C>
+constexpr int dp_max_threads() { return C >= 8 ? 512 : 1024; }
+
+template <int C, int D>
+__global__ void __launch_bounds__(dp_max_threads<C>(), 1) k_dp_seam(DpParams p) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ double s_em[2][2][32];  // [buf][side: 0 = first col of warp, 1 = last col][warp]
+    __shared__ int s_el[2][2][32];
+    __shared__ double s_rv[32];
+    __shared__ int s_ri[32];
+
+    const int img = blockIdx.x;
+    const double* __restrict__ e = p.e + img * p.e_istride;
+    uint8_t* __restrict__ dir = p.dir + img * p.d_istride;
+    int* __restrict__ seam = p.seam + img * p.s_istride;
+    const int W = p.W, H = p.H, R = p.R, nblk = p.nblk;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
+    const int j0 = t * C;
+    const int Wl = (W + 7) & ~7;
+    int16_t* labels = reinterpret_cast<int16_t*>(dsm);                          // nblk x Wl
+    int* cb = reinterpret_cast<int*>(dsm + ((size_t(nblk) * Wl * 2 + 15) & ~size_t(15)));  // nblk + 1
+    uint8_t* win = reinterpret_cast<uint8_t*>(cb) + ((size_t(nblk + 1) * 4 + 15) & ~size_t(15));
+
+    if (p.stamps && t == 0) p.stamps[img * p.st_istride + 0] = globaltimer();
+
+    const double INF = dinf();
+    double m[C];
+    int lab[C];
+    {
+        double v[C];
+        load_cols<C>(e, j0, W, v);
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            m[k] = (j0 + k < W) ? v[k] : INF;
+            lab[k] = j0 + k;
+        }
+        if (p.m_out) {
+#pragma unroll
+            for (int k = 0; k < C; ++k)
+                if (j0 + k < W) {
+                    p.m_out[j0 + k] = m[k];
+                    p.b_out[j0 + k] = j0 + k;
+                }
+        }
+    }
+
+    // register ring of D prefetched energy rows
+    double ring[D][C];
+#pragma unroll
+    for (int u = 0; u < D; ++u)
+        if (1 + u < H) load_cols<C>(e + (long long)(1 + u) * p.epitch, j0, W, ring[u]);
+
+    int blk = 0, inblk = 0;  // block of the current row and its offset in the block
+    for (int i0 = 1; i0 < H; i0 += D) {
+#pragma unroll
+        for (int u = 0; u < D; ++u) {
+            const int i = i0 + u;
+            if (i >= H) break;
+            double ecur[C];
+#pragma unroll
+            for (int k = 0; k < C; ++k) ecur[k] = ring[u][k];
+            if (i + D < H) load_cols<C>(e + (long long)(i + D) * p.epitch, j0, W, ring[u]);
+
+            // previous-row neighbours
+            const int pb = (i - 1) & 1;
+            double lm = __shfl_up_sync(FULL, m[C - 1], 1);
+            int ll = __shfl_up_sync(FULL, lab[C - 1], 1);
+            double rm = __shfl_down_sync(FULL, m[0], 1);
+            int rl = __shfl_down_sync(FULL, lab[0], 1);
+            if (lane == 0) {
+                lm = warp > 0 ? s_em[pb][1][warp - 1] : INF;
+                ll = warp > 0 ? s_el[pb][1][warp - 1] : 0;
+            }
+            if (lane == 31) {
+                rm = warp + 1 < nw ? s_em[pb][0][warp + 1] : INF;
+                rl = warp + 1 < nw ? s_el[pb][0][warp + 1] : 0;
+            }
+            if (inblk == 0) {  // block start: labels restart as identity
+                ll = j0 - 1;
+                rl = j0 + C;
+#pragma unroll
+                for (int k = 0; k < C; ++k) lab[k] = j0 + k;
+            }
+
+            uint32_t dw[(C + 3) / 4];
+#pragma unroll
+            for (int q = 0; q < (C + 3) / 4; ++q) dw[q] = 0;
+            double pm = lm;
+            int pl = ll;
+#pragma unroll
+            for (int k = 0; k < C; ++k) {
+                const double cm = m[k];
+                const int cl = lab[k];
+                const double nm = (k + 1 < C) ? m[k + 1] : rm;
+                const int nl = (k + 1 < C) ? lab[k + 1] : rl;
+                // solvers.hpp:136-145: best = left; mid < best; right < best
+                double best = pm;
+                int d = 0, bl = pl;
+                if (cm < best) { best = cm; d = 1; bl = cl; }
+                if (nm < best) { best = nm; d = 2; bl = nl; }
+                m[k] = (j0 + k < W) ? __dadd_rn(ecur[k], best) : INF;  // solvers.hpp:146
+                lab[k] = bl;
+                dw[k >> 2] |= uint32_t(d) << (8 * (k & 3));
+                pm = cm;
+                pl = cl;
+            }
+            if (j0 < W) store_dirs<C>(dir + (long long)i * p.dpitch + j0, dw);
+            if (p.m_out) {
+#pragma unroll
+                for (int k = 0; k < C; ++k)
+                    if (j0 + k < W) {
+                        const int d = int((dw[k >> 2] >> (8 * (k & 3))) & 0xffu);
+                        p.m_out[(long long)i * W + j0 + k] = m[k];
+                        p.b_out[(long long)i * W + j0 + k] = j0 + k + d - 1;
+                    }
+            }
+            if (inblk == R - 1 || i == H - 1) {  // block's last row: keep its labels
+#pragma unroll
+                for (int k = 0; k < C; ++k)
+                    if (j0 + k < W) labels[(size_t)blk * Wl + j0 + k] = int16_t(lab[k] - (j0 + k));
+            }
+            if (++inblk == R) {
+                inblk = 0;
+                ++blk;
+            }
+            const int cbuf = i & 1;
+            if (lane == 0) { s_em[cbuf][0][warp] = m[0]; s_el[cbuf][0][warp] = lab[0]; }
+            if (lane == 31) { s_em[cbuf][1][warp] = m[C - 1]; s_el[cbuf][1][warp] = lab[C - 1]; }
+            __syncthreads();
+        }
+    }
+
+    // K3a: argmin of the bottom row, first index of the minimum (solvers.hpp:94-99)
+    double bv = INF;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int k = 0; k < C; ++k)
+        if (j0 + k < W && m[k] < bv) { bv = m[k]; bi = j0 + k; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(FULL, bv, o);
+        const int oi = __shfl_xor_sync(FULL, bi, o);
+        if (ov < bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) { s_rv[warp] = bv; s_ri[warp] = bi; }
+    __syncthreads();
+    if (warp == 0) {
+        bv = lane < nw ? s_rv[lane] : INF;
+        bi = lane < nw ? s_ri[lane] : 0x7fffffff;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(FULL, bv, o);
+            const int oi = __shfl_xor_sync(FULL, bi, o);
+            if (ov < bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+        }
+        // K3b phase 1: block-boundary columns through the stored labels
+        if (lane == 0) {
+            int c = bi;
+            seam[H - 1] = c;
+            for (int b = nblk - 1; b >= 0; --b) {
+                cb[b] = c;
+                c += labels[(size_t)b * Wl + c];
+            }
+            if (nblk > 0) seam[0] = c;
+        }
+    }
+    __syncthreads();
+
+    // K3b phase 2: per-block walks, one warp per block, 32-row windows
+    if (warp < p.nwin) {
+        uint8_t* w = win + warp * (WIN_ROWS * WIN_BYTES);
+        for (int b = warp; b < nblk; b += p.nwin) {
+            const int r0 = 1 + b * R, r1 = min(r0 + R - 1, H - 1);
+            int c = cb[b];
+            int i = r1;
+            while (i >= r0) {
+                const int nrows = min(WIN_ROWS, i - r0 + 1);
+                const int base = max(c - 32, 0) & ~15;
+                if (lane < nrows) {
+                    const uint4* src = reinterpret_cast<const uint4*>(dir + (long long)(i - lane) * p.dpitch + base);
+                    uint4* dst = reinterpret_cast<uint4*>(w + lane * WIN_BYTES);
+#pragma unroll
+                    for (int q = 0; q < WIN_BYTES / 16; ++q) dst[q] = src[q];
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    for (int k = 0; k < nrows; ++k) {
+                        c += int(w[k * WIN_BYTES + (c - base)]) - 1;
+                        seam[i - k - 1] = c;
+                    }
+                }
+                c = __shfl_sync(FULL, c, 0);
+                i -= nrows;
+                __syncwarp();
+            }
+        }
+    }
+    if (p.stamps) {
+        __syncthreads();
+        if (t == 0) p.stamps[img * p.st_istride + 1] = globaltimer();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K4 — seam removal: out[i][j] = in[i][j < s[i] ? j : j+1] (carver.hpp:71-82)
+// for the RGBX plane and the FP64 energy plane, fused with the K1 fix-up of
+// the (at most) two new-grid columns s[i]-1 and s[i] whose stencil changed
+// (every other cell keeps its old energy bitwise).
+// One warp per row; each lane produces one 16-byte output chunk per step
+// from its aligned 16-byte input chunk plus the next lane's first element.
+
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<uint32_t> {
+    static constexpr int N = 4;
+    using V = uint4;
+    __device__ static void unpack(const V& v, uint32_t (&a)[4]) { a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w; }
+    __device__ static V pack(const uint32_t (&a)[4]) { return make_uint4(a[0], a[1], a[2], a[3]); }
+};
+template <>
+struct Vec16<double> {
+    static constexpr int N = 2;
+    using V = double2;
+    __device__ static void unpack(const V& v, double (&a)[2]) { a[0] = v.x; a[1] = v.y; }
+    __device__ static V pack(const double (&a)[2]) { return make_double2(a[0], a[1]); }
+};
+
+// energy of new-grid cell (i, x) recomputed from the pre-removal RGBX plane
+__device__ __forceinline__ double fixup_energy(const uint32_t* __restrict__ rgb, int pitch, int Wn, int H,
+                                               const int* __restrict__ seam, int i, int x) {
+    auto old = [&](int r, int c) { return rgb[(long long)r * pitch + c + (c >= __ldg(seam + r) ? 1 : 0)]; };
+    const int xl = max(x - 1, 0), xr = min(x + 1, Wn - 1);
+    const int iu = max(i - 1, 0), id = min(i + 1, H - 1);
+    return e1(luma(old(i, xl)), luma(old(i, xr)), luma(old(iu, x)), luma(old(id, x)));
+}
+
+template <typename T>
+__device__ __forceinline__ void compact_row(const T* __restrict__ in, T* __restrict__ out, int W, int s, int lane,
+                                            const uint32_t* __restrict__ rgb_old, int rpitch, int H,
+                                            const int* __restrict__ seam, int i, bool fix) {
+    using VT = Vec16<T>;
+    constexpr int N = VT::N;
+    const int Wn = W - 1;
+    for (int q0 = 0; q0 * N < Wn; q0 += 32) {
+        const int base = (q0 + lane) * N;
+        const bool active = base < Wn;
+        T a[N];
+        if (active) VT::unpack(*reinterpret_cast<const typename VT::V*>(in + base), a);
+        else {
+#pragma unroll
+            for (int u = 0; u < N; ++u) a[u] = T(0);
+        }
+        T nxt = __shfl_down_sync(FULL, a[0], 1);
+        if (lane == 31 && active && base + N < W) nxt = in[base + N];
+        T o[N];
+#pragma unroll
+        for (int u = 0; u < N; ++u) {
+            const T hi = (u + 1 < N) ? a[u + 1] : nxt;
+            o[u] = (base + u >= s) ? hi : a[u];
+        }
+        if (fix) {
+#pragma unroll
+            for (int u = 0; u < N; ++u) {
+                const int x = base + u;
+                if ((x == s - 1 || x == s) && x < Wn)
+                    o[u] = T(fixup_energy(rgb_old, rpitch, Wn, H, seam, i, x));
+            }
+        }
+        if (base + N <= Wn) *reinterpret_cast<typename VT::V*>(out + base) = VT::pack(o);
+        else if (active) {
+#pragma unroll
+            for (int u = 0; u < N; ++u)
+                if (base + u < Wn) out[base + u] = o[u];
+        }
+    }
+}
+
+struct CompactParams {
+    const uint32_t* rgb_in;
+    uint32_t* rgb_out;
+    const double* e_in;  // nullable: RGB-only removal
+    double* e_out;
+    int pitch;  // shared by rgb and energy planes
+    int W, H;
+    const int* seam;
+    unsigned long long* stamps;  // optional [start, end] per image (written by block 0 / last block)
+    long long p_istride, s_istride, st_istride;
+};
+
+__global__ void __launch_bounds__(256) k_compact(CompactParams p) {
+    const int img = blockIdx.y;
+    const uint32_t* rgb_in = p.rgb_in + img * p.p_istride;
+    uint32_t* rgb_out = p.rgb_out + img * p.p_istride;
+    const int* seam = p.seam + img * p.s_istride;
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    if (p.stamps && blockIdx.x == 0 && threadIdx.x == 0) p.stamps[img * p.st_istride + 0] = globaltimer();
+    for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < p.H; i += gridDim.x * wpb) {
+        const int s = __ldg(seam + i);
+        const long long ro = (long long)i * p.pitch;
+        compact_row<uint32_t>(rgb_in + ro, rgb_out + ro, p.W, s, lane, nullptr, 0, 0, nullptr, 0, false);
+        if (p.e_in)
+            compact_row<double>(p.e_in + img * p.p_istride + ro, p.e_out + img * p.p_istride + ro, p.W, s, lane,
+                                rgb_in, p.pitch, p.H, seam, i, true);
+    }
+    if (p.stamps && threadIdx.x == 0) {
+        // last block to finish stamps the end (monotonic max)
+        atomicMax(&p.stamps[img * p.st_istride + 1], (unsigned long long)globaltimer());
+    }
+}
+
+}  // namespace carve_dev

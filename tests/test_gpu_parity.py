@@ -1,0 +1,251 @@
+"""Parity of the CUDA path (through the C ABI) against the CPU oracle and the
+reference-generated golden vectors. Bar: bit-exact everywhere — FP64 bits of
+energies and cost tables, seam column indices, carved pixels.
+
+Mirrors the reference's own pins: test_solvers.cpp:152-326,
+test_energy.cpp:33-64, test_carver.cpp:34-210, acceptance.cpp:108-122,212-218.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2410_21207_b200 as cv
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float64).view(np.uint64)
+
+
+@pytest.fixture(scope="module")
+def port():
+    return oracle.port()
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return json.load(open(os.path.join(GOLD, "golden.json")))
+
+
+# -- K1 energy --------------------------------------------------------------------
+@pytest.mark.parametrize("w,h", [(1, 1), (1, 7), (7, 1), (2, 2), (3, 5), (63, 17), (64, 16), (65, 17),
+                                 (130, 33), (512, 512), (1920, 1080)])
+def test_energy_rgb_bitexact(port, w, h):
+    rng = np.random.default_rng(w * 1000 + h)
+    for img in (rng.integers(0, 256, (h, w, 3), dtype=np.uint8), port.make_test_image(w, h)):
+        assert np.array_equal(bits(cv.energy_e1_rgb(img)), bits(port.energy_e1_rgb(img)))
+        assert np.array_equal(bits(cv.to_grayscale(img)), bits(port.to_grayscale(img)))
+
+
+def test_energy_luma_reference_cases():
+    # test_energy.cpp:33-64
+    assert (cv.energy_e1(np.full((4, 6), 123.0)) == 0).all()
+    e = cv.energy_e1(np.array([[0.0, 100.0, 0.0]]))
+    assert e.tolist() == [[100.0, 0.0, 100.0]]
+    g = np.zeros((5, 8))
+    g[:, 4:] = 255.0
+    e = cv.energy_e1(g)
+    exp = np.zeros((5, 8))
+    exp[:, 3:5] = 255.0
+    assert np.array_equal(e, exp)
+
+
+def test_energy_luma_random(port):
+    rng = np.random.default_rng(3)
+    for (w, h) in [(1, 1), (9, 4), (100, 37)]:
+        g = rng.uniform(0, 255, (h, w))
+        assert np.array_equal(bits(cv.energy_e1(g)), bits(port.energy_e1_luma(g)))
+
+
+def test_energy_golden_c1(port, gold):
+    img = cv.make_test_image(512, 512)
+    assert f"{oracle.fnv1a64(img):016x}" == gold["configs"]["C1"]["input"]
+    assert f"{oracle.fnv1a64(cv.energy_e1_rgb(img)):016x}" == gold["configs"]["C1"]["energy0"]
+
+
+# -- K2/K3 DP ---------------------------------------------------------------------
+def test_dp_corpus_tables_bitexact():
+    z = np.load(os.path.join(GOLD, "corpus.npz"))
+    for k in range(int(z["n"])):
+        e = z[f"e{k}"].astype(np.float64)
+        r = cv.dp_seam(e)
+        assert np.array_equal(r.seam, z[f"s{k}"]), k
+        assert np.array_equal(r.table.b, z[f"b{k}"].astype(np.int32)), k
+        assert np.array_equal(r.table.m, z[f"m{k}"].astype(np.float64)), k
+
+
+def test_dp_worked_example():
+    # test_solvers.cpp:156-174
+    m = np.array([[1, 2, 3], [4, 1, 6], [7, 8, 1]], np.float64)
+    r = cv.dp_seam(m)
+    assert r.table.m.tolist() == [[1, 2, 3], [5, 2, 8], [9, 10, 3]]
+    assert r.seam.tolist() == [0, 1, 2]
+    assert cv.dp_seam(np.array([[8.0, 2, 6, 2]])).seam.tolist() == [1]  # :152-155
+
+
+@pytest.mark.parametrize("w,h", [(1, 1), (1, 300), (2, 5), (300, 1), (31, 9), (33, 70), (257, 63), (1024, 768),
+                                 (1025, 40), (2048, 50), (2049, 65), (4097, 40), (7680, 70), (8192, 33)])
+def test_dp_random_real_energies(port, w, h):
+    """Real-valued (non-integer) FP64 energies from the fixture: bit-exact m, b, seam."""
+    img = port.make_test_image(w, h)
+    e = port.energy_e1_rgb(img)
+    seam, m, b = port.dp_seam(e)
+    r = cv.dp_seam(e)
+    assert np.array_equal(r.seam, seam)
+    assert np.array_equal(bits(r.table.m), bits(m))
+    assert np.array_equal(r.table.b, b)
+    assert np.array_equal(cv.find_seam(e, cv.SolverKind.Dynamic), seam)
+
+
+def test_dp_ties_everywhere(port):
+    for (w, h) in [(1, 5), (6, 4), (64, 64), (1000, 300), (3000, 97)]:
+        e = np.zeros((h, w))
+        r = cv.dp_seam(e)
+        assert (r.seam == 0).all()
+        rng = np.random.default_rng(w)
+        e = np.floor(rng.uniform(0, 2, (h, w)))
+        seam, m, b = port.dp_seam(e)
+        r = cv.dp_seam(e)
+        assert np.array_equal(r.seam, seam) and np.array_equal(r.table.b, b) and np.array_equal(r.table.m, m)
+
+
+def test_dp_1080_fixture_matches(port):
+    # acceptance.cpp:212-218 (criterion 7's parity half)
+    img = port.make_test_image(1080, 1080)
+    e = port.energy_e1_rgb(img)
+    seam, m, b = port.dp_seam(e)
+    r = cv.parallel_dp_seam(e, 4)
+    assert np.array_equal(r.seam, seam) and np.array_equal(bits(r.table.m), bits(m)) and np.array_equal(r.table.b, b)
+
+
+# -- K4 removal, transpose ----------------------------------------------------------
+def test_remove_seam_cases(port):
+    g = np.zeros((1, 2, 3), np.uint8)
+    g[0, 0] = 1
+    g[0, 1] = 2
+    assert cv.remove_seam(g, [0]).tolist() == [[[2, 2, 2]]]  # test_carver.cpp:35-42
+    rng = np.random.default_rng(1)
+    for (w, h) in [(3, 3), (9, 6), (33, 5), (130, 20), (1921, 7)]:
+        img = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+        s = [int(rng.integers(0, w))]
+        for _ in range(h - 1):
+            s.append(int(np.clip(s[-1] + rng.integers(-1, 2), 0, w - 1)))
+        assert np.array_equal(cv.remove_seam(img, s), port.remove_seam(img, s))
+
+
+def test_remove_seam_errors():
+    with pytest.raises(cv.CarveError) as ei:
+        cv.remove_seam(np.zeros((2, 1, 3), np.uint8), [0, 0])
+    assert ei.value.code == cv.Errc.width_too_small
+    with pytest.raises(cv.CarveError) as ei:
+        cv.remove_seam(np.zeros((2, 3, 3), np.uint8), [0, 2])
+    assert ei.value.code == cv.Errc.invalid_seam
+
+
+def test_transpose(port):
+    rng = np.random.default_rng(2)
+    for (w, h) in [(1, 1), (3, 2), (5, 4), (33, 65), (100, 7)]:
+        img = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+        t = cv.transpose(img)
+        assert np.array_equal(t, port.transpose(img))
+        assert np.array_equal(cv.transpose(t), img)
+
+
+# -- whole pipeline -------------------------------------------------------------------
+def test_carve_small_golden():
+    z = np.load(os.path.join(GOLD, "small.npz"))
+    for k in range(int(z["n"])):
+        img = z[f"img{k}"]
+        tw, th = (int(v) for v in z[f"tgt{k}"])
+        out, seams, _ = cv.carve(img, tw, th, seams=True)
+        assert np.array_equal(out, z[f"out{k}"]), k
+        flat = np.concatenate(seams) if seams else np.zeros(0, np.int32)
+        ref = z[f"seams{k}"][: flat.size]
+        assert np.array_equal(flat, ref), k
+        assert np.array_equal(bits(cv.energy_e1_rgb(img)), bits(z[f"e{k}"])), k
+
+
+@pytest.mark.parametrize("w,h,tw,th", [(64, 48, 40, 48), (100, 80, 60, 50), (37, 120, 30, 100), (200, 3, 150, 3),
+                                       (5, 200, 5, 100), (260, 140, 129, 70)])
+def test_carve_vs_port(port, w, h, tw, th):
+    rng = np.random.default_rng(w + h)
+    for img in (port.make_test_image(w, h), rng.integers(0, 256, (h, w, 3), dtype=np.uint8),
+                np.full((h, w, 3), 77, np.uint8)):
+        out, s_ref = port.carve(img, tw, th, seams=True)
+        got, seams, tim = cv.carve(img, tw, th, seams=True, timings=True)
+        assert np.array_equal(got, out)
+        flat = np.concatenate(seams) if seams else np.zeros(0, np.int32)
+        assert np.array_equal(flat, s_ref)
+        assert len(tim) == len(seams)
+
+
+def test_carve_reference_api_contract():
+    # test_carver.cpp:117-142, 160-168, 202-210
+    g = np.zeros((4, 4, 3), np.uint8)
+    for j, v in enumerate([10, 50, 10, 90]):
+        g[:, j] = v
+    out, rep = cv.carve_to_width(g, 3)
+    assert rep.seam_count == 1 and rep.seams[0].tolist() == [1, 1, 1, 1]
+    assert np.array_equal(out, g[:, [0, 2, 3]])
+    img = cv.make_test_image(24, 16)
+    out, rep = cv.carve_to_width(img, 10)
+    assert out.shape == (16, 10, 3) and rep.seam_count == 14 and len(rep.per_seam) == 14
+    for t, s in enumerate(rep.seams):
+        cv.validate_seam(s, 24 - t, 16)
+    assert rep.total_s >= sum(x.energy_s + x.solve_s + x.remove_s for x in rep.per_seam)
+    out, rep = cv.carve_to_width(img, 24)
+    assert np.array_equal(out, img) and rep.seam_count == 0
+    for bad in (0, 25):
+        with pytest.raises(cv.CarveError) as ei:
+            cv.carve_to_width(img, bad)
+        assert ei.value.code == cv.Errc.invalid_target
+    rng = np.random.default_rng(6)
+    g = rng.integers(0, 256, (8, 10, 3), dtype=np.uint8)
+    direct = cv.carve_to_height(g, 5)[0]
+    sandwich = cv.transpose(cv.carve_to_width(cv.transpose(g), 5)[0])
+    assert np.array_equal(direct, sandwich)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_config_golden(gold, name):
+    c = gold["configs"][name]
+    img = cv.make_test_image(c["W"], c["H"])
+    assert f"{oracle.fnv1a64(img):016x}" == c["input"]
+    out, seams, _ = cv.carve(img, c["target_w"], c["target_h"], seams=True)
+    assert f"{oracle.fnv1a64(out):016x}" == c["output"]
+    assert f"{oracle.fnv1a64(np.concatenate(seams)):016x}" == c["seams"]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_config_golden_full(gold, name):
+    c = gold["configs"].get(name)
+    if c is None:
+        pytest.skip(f"{name} golden not generated")
+    img = cv.make_test_image(c["W"], c["H"])
+    assert f"{oracle.fnv1a64(img):016x}" == c["input"]
+    out, seams, _ = cv.carve(img, c["target_w"], c["target_h"], seams=True)
+    assert f"{oracle.fnv1a64(out):016x}" == c["output"]
+    assert f"{oracle.fnv1a64(np.concatenate(seams)):016x}" == c["seams"]
+
+
+def test_batch_golden_sample(gold):
+    c = gold["configs"]["C5"]
+    ks = [int(k) for k in c["samples"]]
+    imgs = [cv.make_test_image(c["W"], c["H"], k) for k in ks]
+    outs = cv.carve_batch(imgs, c["target_w"], c["target_h"])
+    for k, img, out in zip(ks, imgs, outs):
+        assert f"{oracle.fnv1a64(img):016x}" == c["samples"][str(k)]["input"]
+        assert f"{oracle.fnv1a64(out):016x}" == c["samples"][str(k)]["output"], k
+
+
+def test_native_kernels_launched():
+    cv.reset_launch_count()
+    cv.carve(cv.make_test_image(64, 32), 60)
+    # unpack + energy + 4 x (dp + compact) + pack
+    assert cv.launch_count() == 11

@@ -1,0 +1,132 @@
+"""CPU suite: pins the oracle (oracle/carve_oracle.c) before it is trusted.
+
+1. against the reference itself compiled from /root/reference (oracle/_ref),
+   when that build is present;
+2. against the committed golden vectors (tests/golden/, generated from the
+   reference by tests/golden/make_golden.py) — always.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float64).view(np.uint64)
+
+
+@pytest.fixture(scope="module")
+def port():
+    return oracle.port()
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return json.load(open(os.path.join(GOLD, "golden.json")))
+
+
+need_ref = pytest.mark.skipif(not oracle.have_reference(), reason="oracle/_ref not built (no /root/reference)")
+
+
+def test_fixture_generator_matches_golden(port, gold):
+    for name in ("C1", "C2", "C3", "C4"):
+        c = gold["configs"].get(name)
+        if c is None:
+            continue
+        img = port.make_test_image(c["W"], c["H"])
+        assert f"{oracle.fnv1a64(img):016x}" == c["input"], name
+    for k, rec in gold["configs"]["C5"]["samples"].items():
+        img = port.make_test_image(gold["configs"]["C5"]["W"], gold["configs"]["C5"]["H"], int(k))
+        assert f"{oracle.fnv1a64(img):016x}" == rec["input"], k
+
+
+def test_c1_energy_and_table_golden(port, gold):
+    c = gold["configs"]["C1"]
+    img = port.make_test_image(512, 512)
+    e = port.energy_e1_rgb(img)
+    assert f"{oracle.fnv1a64(e):016x}" == c["energy0"]
+    seam, m, b = port.dp_seam(e)
+    assert f"{oracle.fnv1a64(m):016x}" == c["table0_m"]
+    assert f"{oracle.fnv1a64(b):016x}" == c["table0_b"]
+    assert f"{oracle.fnv1a64(seam):016x}" == c["seam0"]
+
+
+def test_c1_full_carve_golden(port, gold):
+    c = gold["configs"]["C1"]
+    out, seams = port.carve(port.make_test_image(512, 512), 448, seams=True)
+    assert f"{oracle.fnv1a64(out):016x}" == c["output"]
+    assert f"{oracle.fnv1a64(seams):016x}" == c["seams"]
+
+
+def test_corpus_golden(port):
+    z = np.load(os.path.join(GOLD, "corpus.npz"))
+    for k in range(int(z["n"])):
+        e = z[f"e{k}"].astype(np.float64)
+        seam, m, b = port.dp_seam(e)
+        assert np.array_equal(seam, z[f"s{k}"]), k
+        assert np.array_equal(b, z[f"b{k}"].astype(np.int32)), k
+        assert np.array_equal(m, z[f"m{k}"].astype(np.float64)), k
+
+
+def test_small_images_golden(port):
+    z = np.load(os.path.join(GOLD, "small.npz"))
+    for k in range(int(z["n"])):
+        img = z[f"img{k}"]
+        tw, th = (int(v) for v in z[f"tgt{k}"])
+        assert np.array_equal(bits(port.energy_e1_rgb(img)), bits(z[f"e{k}"])), k
+        out, seams = port.carve(img, tw, th, seams=True)
+        assert np.array_equal(out, z[f"out{k}"]), k
+        assert np.array_equal(seams, z[f"seams{k}"][: seams.size]), k
+
+
+def test_port_reference_cases(port):
+    # test_solvers.cpp:152-174, test_energy.cpp:33-64, test_carver.cpp:34-73
+    seam, m, _ = port.dp_seam(np.array([[1, 2, 3], [4, 1, 6], [7, 8, 1]], np.float64))
+    assert m.tolist() == [[1, 2, 3], [5, 2, 8], [9, 10, 3]] and seam.tolist() == [0, 1, 2]
+    assert port.dp_seam(np.array([[8.0, 2, 6, 2]]))[0].tolist() == [1]
+    assert port.energy_e1_luma(np.array([[0.0, 100.0, 0.0]])).tolist() == [[100.0, 0.0, 100.0]]
+    assert port.validate_seam([0, 2], 3, 2) == 6  # invalid_seam
+    with pytest.raises(oracle.OracleError):
+        port.remove_seam(np.zeros((2, 1, 3), np.uint8), [0, 0])
+
+
+@need_ref
+def test_port_vs_reference_random(port):
+    ref = oracle.reference()
+    rng = np.random.default_rng(11)
+    for _ in range(40):
+        w, h = (int(x) for x in rng.integers(1, 40, 2))
+        img = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+        assert np.array_equal(bits(port.to_grayscale(img)), bits(ref.to_grayscale(img)))
+        assert np.array_equal(bits(port.energy_e1_rgb(img)), bits(ref.energy_e1_rgb(img)))
+        assert np.array_equal(port.transpose(img), ref.transpose(img))
+        e = ref.energy_e1_rgb(img)
+        s1, m1, b1 = port.dp_seam(e)
+        s2, m2, b2 = ref.dp_seam(e)
+        assert np.array_equal(s1, s2) and np.array_equal(bits(m1), bits(m2)) and np.array_equal(b1, b2)
+        tw, th = int(rng.integers(1, w + 1)), int(rng.integers(1, h + 1))
+        o1, q1 = port.carve(img, tw, th, seams=True)
+        o2, q2 = ref.carve(img, tw, th, seams=True)
+        assert np.array_equal(o1, o2) and np.array_equal(q1, q2)
+
+
+@need_ref
+def test_port_vs_reference_fixture(port):
+    ref = oracle.reference()
+    for (w, h) in [(1, 1), (2, 3), (640, 360), (1920, 1080)]:
+        assert np.array_equal(port.make_test_image(w, h), ref.make_test_image(w, h))
+
+
+@need_ref
+def test_reference_pardp_equals_dp():
+    ref = oracle.reference()
+    img = ref.make_test_image(300, 200)
+    e = ref.energy_e1_rgb(img)
+    a = ref.dp_seam(e, 0)
+    b = ref.dp_seam(e, 1, 4)
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))
