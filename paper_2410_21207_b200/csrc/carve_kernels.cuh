@@ -301,6 +301,11 @@ __global__ void __launch_bounds__(dp_max_threads<C>(), 1) k_dp_seam(DpParams p) 
         }
     }
 
+    // publish row 0's warp-edge values for row 1 (buffer (1-1)&1 = 0)
+    if (lane == 0) { s_em[0][0][warp] = m[0]; s_el[0][0][warp] = lab[0]; }
+    if (lane == 31) { s_em[0][1][warp] = m[C - 1]; s_el[0][1][warp] = lab[C - 1]; }
+    __syncthreads();
+
     // register ring of D prefetched energy rows
     double ring[D][C];
 #pragma unroll
