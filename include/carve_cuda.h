@@ -128,7 +128,7 @@ carve_status carve_cuda_carve_batch(const uint8_t* const* rgb, int n, int w, int
 
 /* ---- device-resident entry points (inputs already in HBM) --------------
  * d_rgb / d_out are device pointers to packed RGB on the current device;
- * `stream` is a cudaStream_t (NULL = the thread context's stream). These
+ * `stream` is a cudaStream_t (NULL = the legacy default stream). These
  * enqueue work and return without synchronizing (the bench times them with
  * CUDA events on `stream`). d_seams (nullable) receives seams as above. */
 carve_status carve_cuda_carve_device(const uint8_t* d_rgb, int w, int h, int target_w, int target_h,

@@ -705,7 +705,7 @@ carve_status carve_cuda_carve_device(const uint8_t* d_rgb, int w, int h, int tar
         const CarveGeometry g = geometry(w, h, target_w, target_h);
         ensure_carve_buffers(c, g, 1);
         int* seams = d_seams ? d_seams : static_cast<int*>(c.seams.ensure(std::max<size_t>(g.seam_ints, 1) * 4));
-        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c.stream;
+        cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL = the legacy default stream
         run_carve(c, d_rgb, d_out, 1, g, seams, g.seam_ints, nullptr, s);
     });
 }
@@ -719,7 +719,7 @@ carve_status carve_cuda_carve_batch_device(const uint8_t* d_rgb, int n, int w, i
         const CarveGeometry g = geometry(w, h, target_w, target_h);
         ensure_carve_buffers(c, g, n);
         int* seams = static_cast<int*>(c.seams.ensure(std::max<size_t>(g.seam_ints, 1) * 4 * n));
-        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c.stream;
+        cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL = the legacy default stream
         run_carve(c, d_rgb, d_out, n, g, seams, std::max<size_t>(g.seam_ints, 1), nullptr, s);
     });
 }

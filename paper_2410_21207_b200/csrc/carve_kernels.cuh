@@ -508,7 +508,10 @@ __device__ __forceinline__ void compact_row(const T* __restrict__ in, T* __restr
         const int base = (q0 + lane) * N;
         const bool active = base < Wn;
         T a[N];
-        if (active) VT::unpack(*reinterpret_cast<const typename VT::V*>(in + base), a);
+        // load whenever the chunk holds an input element: the previous lane's
+        // last output may need this chunk's first element even when no output
+        // position of this chunk survives
+        if (base < W) VT::unpack(*reinterpret_cast<const typename VT::V*>(in + base), a);
         else {
 #pragma unroll
             for (int u = 0; u < N; ++u) a[u] = T(0);
