@@ -4,11 +4,13 @@
 // runs the sm_100a kernels in carve_kernels.cuh or returns CARVE_E_CUDA.
 #include "carve_cuda.h"
 #include "carve_kernels.cuh"
+#include "dp_cluster.cuh"
 
 #include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -84,7 +86,7 @@ struct DevBuf {
 struct Ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
-    DevBuf packed_in, packed_out, rgb[2], e[2], dir, seams, stamps, scratch_a, scratch_b;
+    DevBuf packed_in, packed_out, rgb[2], e[2], dir, seams, stamps, scratch_a, scratch_b, mbound;
     int max_smem_optin = 0;
     std::map<const void*, int> smem_set;  // kernel -> dynamic smem attribute set
     // kernel-event profiling mode (bench attribution): one event pair per launch
@@ -262,6 +264,91 @@ void launch_dp(Ctx& c, const DpShape& d, const DpParams& p, int nimg, cudaStream
     }
 }
 
+// ---- K2+K3 v2: cluster trapezoid DP (dp_cluster.cuh) ------------------------
+struct Dp2Variant {
+    int C, K, NW, D;
+    const void* fn;
+    size_t (*smem)(int nblk);
+    int S() const { return 32 * C - 2 * K; }
+    int cols() const { return NW * S(); }
+};
+
+template <int C, int K, int NW, int D>
+constexpr Dp2Variant dp2_variant() {
+    return Dp2Variant{C, K, NW, D, (const void*)k_dp2<C, K, NW, D>, &Dp2Smem<C, K, NW>::total};
+}
+
+// preference order: the first variant whose cluster fits (<= 8 CTAs, then <= 16) wins
+const Dp2Variant kDp2Variants[] = {
+    dp2_variant<4, 16, 4, 8>(),   // 0: S=96,  384 cols/CTA
+    dp2_variant<8, 16, 4, 4>(),   // 1: S=224, 896 cols/CTA
+    dp2_variant<8, 16, 8, 4>(),   // 2: S=224, 1792 cols/CTA
+    dp2_variant<4, 8, 4, 8>(),    // 3: S=112, 448 cols/CTA
+    dp2_variant<8, 32, 4, 4>(),   // 4: S=192, 768 cols/CTA
+    dp2_variant<4, 16, 8, 8>(),   // 5: S=96,  768 cols/CTA
+    dp2_variant<2, 8, 8, 8>(),    // 6: S=48,  384 cols/CTA
+    dp2_variant<8, 16, 16, 4>(),  // 7: S=224, 3584 cols/CTA
+};
+constexpr int kNumDp2Variants = int(sizeof(kDp2Variants) / sizeof(kDp2Variants[0]));
+
+struct Dp2Plan {
+    const Dp2Variant* v;
+    int ncl, nblk;
+    size_t smem;
+};
+
+int env_int(const char* name, int dflt) {
+    const char* s = std::getenv(name);
+    return s && *s ? std::atoi(s) : dflt;
+}
+
+Dp2Plan dp2_plan(int W, int H) {
+    const int nblk = H > 1 ? (H - 1 + LBLK - 1) / LBLK : 0;
+    const int forced = env_int("CARVE_DP_VARIANT", -1);
+    const int max_ncl = env_int("CARVE_DP_MAX_NCL", 8);
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int k = 0; k < kNumDp2Variants; ++k) {
+            if (forced >= 0 && k != forced) continue;
+            const Dp2Variant& v = kDp2Variants[k];
+            const int ncl = (W + v.cols() - 1) / v.cols();
+            const size_t smem = v.smem(nblk);
+            if (ncl > (pass == 0 ? max_ncl : 16) || smem > size_t(kDpSmemBudget)) continue;
+            return Dp2Plan{&v, ncl, nblk, smem};
+        }
+    }
+    fail(CARVE_E_IMAGE_TOO_LARGE, "no DP cluster configuration fits width " + std::to_string(W) + " x height " +
+                                      std::to_string(H));
+}
+
+void launch_dp2(Ctx& c, const Dp2Plan& pl, Dp2Params p, int nimg, cudaStream_t s) {
+    const Dp2Variant& v = *pl.v;
+    p.G = pl.ncl * v.NW;
+    p.nblk = pl.nblk;
+    auto it = c.smem_set.find(v.fn);
+    if (it == c.smem_set.end()) {
+        ck(cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kDpSmemBudget),
+           "cudaFuncSetAttribute(dp2 smem)");
+        ck(cudaFuncSetAttribute(v.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+           "cudaFuncSetAttribute(dp2 cluster)");
+        c.smem_set[v.fn] = kDpSmemBudget;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(nimg * pl.ncl));
+    cfg.blockDim = dim3(unsigned(v.NW * 32));
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(pl.ncl);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    void* args[] = {&p};
+    ck(cudaLaunchKernelExC(&cfg, v.fn, args), "launch k_dp2");
+    LAUNCHED("k_dp2");
+}
+
 void launch_compact(const CompactParams& p, int nimg, cudaStream_t s) {
     const int wpb = 8;
     dim3 grid((p.H + wpb - 1) / wpb, nimg);
@@ -281,6 +368,8 @@ struct CarveGeometry {
     int dir_rows;
     size_t seam_ints; // per image
     int nseams;
+    int mpitch;       // M-boundary row pitch (doubles)
+    long long mb_istride;
 };
 
 CarveGeometry geometry(int w, int h, int tw, int th) {
@@ -297,6 +386,8 @@ CarveGeometry geometry(int w, int h, int tw, int th) {
     g.dir_rows = std::max(h, tw);
     g.seam_ints = size_t(w - tw) * h + size_t(h - th) * tw;
     g.nseams = (w - tw) + (h - th);
+    g.mpitch = std::max(g.pitch_a, g.pitch_b);
+    g.mb_istride = (long long)((g.dir_rows + LBLK - 1) / LBLK + 1) * g.mpitch;
     return g;
 }
 
@@ -304,9 +395,9 @@ void check_targets(int w, int h, int tw, int th) {
     if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "PixelGrid dimensions must be >= 1");
     if (tw < 1 || tw > w) fail(CARVE_E_INVALID_TARGET, "target width must be in [1, width]");
     if (th < 1 || th > h) fail(CARVE_E_INVALID_TARGET, "target height must be in [1, height]");
-    // single-CTA DP limit on the widths the solver will see
-    if (tw < w) dp_shape(w, h);
-    if (th < h) dp_shape(h, tw);
+    // DP configuration must exist for the widths the solver will see
+    if (tw < w) dp2_plan(w, h);
+    if (th < h) dp2_plan(h, tw);
 }
 
 // stamps layout per image: [4 per seam: dp start/end, compact start/end] then
@@ -322,6 +413,7 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
     const long long pis = (long long)g.plane;
     const long long dis = (long long)g.dpitch * g.dir_rows;
     const size_t sw = stamp_words(g);
+    const bool dp_v1 = env_int("CARVE_DP", 2) == 1;
     int cur = 0;
     {
         Prof pr(c, s, KK_UNPACK, 7.0 * g.w * g.h * nimg);
@@ -338,27 +430,45 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
         (void)estamp;
         for (int k = 0; k < ntake; ++k) {
             const int W = W0 - k;
-            const DpShape d = dp_shape(W, H);
             DpParams p{};
-            p.e = e[cur];
-            p.epitch = pitch;
-            p.W = W;
-            p.H = H;
-            p.dir = dir;
-            p.dpitch = g.dpitch;
-            p.R = d.R;
-            p.nblk = d.nblk;
-            p.nwin = d.nwin;
             p.seam = d_seams + seam_base + size_t(k) * H;
             p.stamps = d_stamps ? d_stamps + size_t(stamp_seam0 + k) * 4 : nullptr;
-            p.e_istride = pis;
-            p.d_istride = dis;
-            p.s_istride = (long long)seam_istride;
-            p.st_istride = (long long)sw;
-            {
+            if (dp_v1) {
+                const DpShape d = dp_shape(W, H);
+                p.e = e[cur];
+                p.epitch = pitch;
+                p.W = W;
+                p.H = H;
+                p.dir = dir;
+                p.dpitch = g.dpitch;
+                p.R = d.R;
+                p.nblk = d.nblk;
+                p.nwin = d.nwin;
+                p.e_istride = pis;
+                p.d_istride = dis;
+                p.s_istride = (long long)seam_istride;
+                p.st_istride = (long long)sw;
                 // 8 B FP64 energy read + 1 B direction write per cell
                 Prof pr(c, s, KK_DP, 9.0 * W * H * nimg);
                 launch_dp(c, d, p, nimg, s);
+            } else {
+                const Dp2Plan pl = dp2_plan(W, H);
+                Dp2Params q{};
+                q.e = e[cur];
+                q.epitch = pitch;
+                q.W = W;
+                q.H = H;
+                q.mbound = c.mbound.as<double>();
+                q.mpitch = g.mpitch;
+                q.seam = p.seam;
+                q.stamps = p.stamps;
+                q.e_istride = pis;
+                q.mb_istride = g.mb_istride;
+                q.s_istride = (long long)seam_istride;
+                q.st_istride = (long long)sw;
+                // algorithmic: 8 B FP64 energy read per cell (no direction plane)
+                Prof pr(c, s, KK_DP, 8.0 * W * H * nimg);
+                launch_dp2(c, pl, q, nimg, s);
             }
             CompactParams q{};
             q.rgb_in = rgb[cur];
@@ -404,6 +514,7 @@ void ensure_carve_buffers(Ctx& c, const CarveGeometry& g, int nimg) {
         c.e[k].ensure(g.plane * 8 * nimg);
     }
     c.dir.ensure(size_t(g.dpitch) * g.dir_rows * nimg + 256);
+    c.mbound.ensure(size_t(g.mb_istride) * 8 * nimg);
 }
 
 // ---------------------------------------------------------------------------
@@ -622,11 +733,10 @@ carve_status carve_cuda_dp_seam(const double* e, int w, int h, double* m_out, in
         if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "image is empty");
         if ((m_out == nullptr) != (b_out == nullptr)) fail(CARVE_E_USAGE_ERROR, "m_out and b_out go together");
         Ctx& c = ctx();
-        const DpShape d = dp_shape(w, h);
+        const Dp2Plan pl = dp2_plan(w, h);
         const int pitch = int(round_up(w, 32));
-        const int dpitch = int(round_up(w, 16) + 128);
         double* de = static_cast<double*>(c.e[0].ensure(size_t(pitch) * h * 8));
-        uint8_t* dir = static_cast<uint8_t*>(c.dir.ensure(size_t(dpitch) * h + 256));
+        double* mb = static_cast<double*>(c.mbound.ensure(size_t(pl.nblk + 1) * pitch * 8));
         int* dseam = static_cast<int*>(c.seams.ensure(size_t(h) * 4));
         double* dm = nullptr;
         int* db = nullptr;
@@ -637,20 +747,17 @@ carve_status carve_cuda_dp_seam(const double* e, int w, int h, double* m_out, in
         ck(cudaMemcpy2DAsync(de, size_t(pitch) * 8, e, size_t(w) * 8, size_t(w) * 8, h, cudaMemcpyHostToDevice,
                              c.stream),
            "H2D energy");
-        DpParams p{};
+        Dp2Params p{};
         p.e = de;
         p.epitch = pitch;
         p.W = w;
         p.H = h;
-        p.dir = dir;
-        p.dpitch = dpitch;
-        p.R = d.R;
-        p.nblk = d.nblk;
-        p.nwin = d.nwin;
+        p.mbound = mb;
+        p.mpitch = pitch;
         p.seam = dseam;
         p.m_out = dm;
         p.b_out = db;
-        launch_dp(c, d, p, 1, c.stream);
+        launch_dp2(c, pl, p, 1, c.stream);
         ck(cudaMemcpyAsync(seam_out, dseam, size_t(h) * 4, cudaMemcpyDeviceToHost, c.stream), "D2H seam");
         if (m_out) {
             ck(cudaMemcpyAsync(m_out, dm, size_t(w) * h * 8, cudaMemcpyDeviceToHost, c.stream), "D2H m");

@@ -1,0 +1,373 @@
+// dp_cluster.cuh — K2+K3 v2: cluster-spread trapezoid DP, argmin, backtrack.
+//
+// Recurrence (solvers.hpp:116-157, 263-289): M[0][j] = e[0][j];
+//   M[i][j] = e[i][j] + min(M[i-1][j-1], M[i-1][j], M[i-1][j+1]) scanned
+//   left, mid, right with strict < (smallest column wins ties); out-of-range
+//   neighbours excluded. Out-of-image columns hold +inf here (e := +inf), which
+//   is equivalent because the middle candidate is always finite.
+//
+// Work decomposition. The row is cut into warp segments of
+// S = 32*C - 2*K useful columns. Warp g holds 32*C consecutive columns
+// [g*S - K, g*S - K + 32*C) in registers (C per lane): its S useful columns
+// plus a K-column halo on each side that overlaps its neighbours. It then
+// computes K rows with lane shuffles only; the valid region shrinks by one
+// column per row on each side, so after K rows exactly its S useful columns
+// are exact. Only then do neighbouring warps swap K halo values through a
+// shared-memory mailbox — in the neighbour CTA's shared memory (DSMEM) when
+// the neighbour lives in another CTA of the thread-block cluster — followed
+// by one barrier. One barrier per K rows instead of one per row; the price is
+// 2K/(32C) redundant halo cells.
+//
+// Backtrack (solvers.hpp:94-111) without an H-step serial chain:
+//  * labels: every cell also carries the column, at the row above its
+//    32-row block, that its optimal path descends from (selected with the same
+//    predicates as M). Each block's last-row labels stay in shared memory as
+//    int8 offsets; phase 1 hops block to block (one lookup per 32 rows).
+//  * M-boundary rows: M of every 32nd row goes to global memory. Phase 2
+//    recomputes each block's 32 rows bit-identically inside a 128-column
+//    window around the block's known bottom column (one warp per block, all
+//    blocks in parallel), records directions in shared memory and walks them.
+// No per-cell direction plane is written in the hot loop.
+#pragma once
+#include <cooperative_groups.h>
+#include <cstdint>
+
+namespace carve_dev {
+
+namespace cg = cooperative_groups;
+
+constexpr int LBLK = 32;      // label / M-boundary block height (rows)
+constexpr int P2_COLS = 128;  // phase-2 window: 32 lanes x 4 columns
+
+struct Dp2Params {
+    const double* e;   // energy plane (pitch epitch), image stride e_istride
+    int epitch;
+    int W, H;
+    int G;             // warps in the cluster (= ncl * NWARP)
+    int nblk;          // label blocks: ceil((H-1)/LBLK)
+    double* mbound;    // [nblk][mpitch] M rows 0, 32, 64, ... (global scratch), image stride mb_istride
+    int mpitch;
+    int* seam;         // H ints, image stride s_istride
+    double* m_out;     // optional full cost table (pitch W)
+    int* b_out;        // optional predecessor table (pitch W)
+    unsigned long long* stamps;  // optional [start, end]
+    long long e_istride, mb_istride, s_istride, st_istride;
+};
+
+// smem layout (dynamic): labels int8 [nblk][NWARP*S] | mailbox | cb | phase-2 dirs | reduce
+template <int C, int K, int NWARP>
+struct Dp2Smem {
+    static constexpr int S = 32 * C - 2 * K;
+    static constexpr int COLS = NWARP * S;  // useful columns per CTA
+    __host__ __device__ static size_t labels_bytes(int nblk) { return (size_t(nblk) * COLS + 15) & ~size_t(15); }
+    static constexpr size_t mail_bytes = size_t(2) * NWARP * 2 * K * (8 + 4);
+    __host__ __device__ static size_t cb_bytes(int nblk) { return (size_t(nblk + 1) * 4 + 15) & ~size_t(15); }
+    static constexpr size_t p2_bytes = size_t(NWARP) * LBLK * P2_COLS;
+    static constexpr size_t red_bytes = 64 * 16;
+    __host__ __device__ static size_t total(int nblk) { return labels_bytes(nblk) + mail_bytes + cb_bytes(nblk) + p2_bytes + red_bytes; }
+};
+
+// the 9-instruction cell update shared by the forward pass and phase 2
+// (DSETP, 2xFSEL, DSETP, 2xFSEL, DADD + the selects that carry the label)
+__device__ __forceinline__ void dp_cell(double L, double M, double R, int lL, int lM, int lR, double e, double& out,
+                                        int& lab, int& d) {
+    double best = L;
+    int bl = lL;
+    d = 0;
+    if (M < best) { best = M; bl = lM; d = 1; }
+    if (R < best) { best = R; bl = lR; d = 2; }
+    out = __dadd_rn(e, best);
+    lab = bl;
+}
+
+template <int C>
+__device__ __forceinline__ void load_row(const double* __restrict__ row, int col0, int W, double (&v)[C]) {
+    // C consecutive columns starting at col0 (even); +inf outside the image
+    if (col0 >= 0 && col0 + C <= W) {
+#pragma unroll
+        for (int k = 0; k < C; k += 2) {
+            const double2 x = __ldg(reinterpret_cast<const double2*>(row + col0 + k));
+            v[k] = x.x;
+            v[k + 1] = x.y;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            const int j = col0 + k;
+            v[k] = (j >= 0 && j < W) ? __ldg(row + j) : dinf();
+        }
+    }
+}
+
+__device__ __forceinline__ void argmin_combine(double& v, int& i, double ov, int oi) {
+    if (ov < v || (ov == v && oi < i)) { v = ov; i = oi; }
+}
+
+template <int C, int K, int NWARP, int D>
+__global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
+    static_assert(K % C == 0 && (32 * C) > 2 * K, "halo must be whole lanes and leave useful columns");
+    using SM = Dp2Smem<C, K, NWARP>;
+    constexpr int S = SM::S;
+    constexpr int KL = K / C;  // lanes per halo
+    extern __shared__ __align__(16) unsigned char dsm[];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int ncl = int(cluster.num_blocks());
+    const int cta = int(cluster.block_rank());
+    const int img = blockIdx.x / ncl;
+
+    const double* __restrict__ e = p.e + img * p.e_istride;
+    double* __restrict__ mbound = p.mbound + img * p.mb_istride;
+    int* __restrict__ seam = p.seam + img * p.s_istride;
+    const int W = p.W, H = p.H, G = p.G, nblk = p.nblk;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = cta * NWARP + warp;
+    const int ucol0 = g * S;                   // first useful column of this warp
+    const int col0 = ucol0 - K + lane * C;     // first column held by this lane
+    const int cta_col0 = cta * SM::COLS;
+
+    int8_t* labels = reinterpret_cast<int8_t*>(dsm);
+    double* mail_m = reinterpret_cast<double*>(dsm + SM::labels_bytes(nblk));  // [2][NWARP][2][K]
+    int* mail_l = reinterpret_cast<int*>(mail_m + 2 * NWARP * 2 * K);
+    int* cb = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(mail_l + 2 * NWARP * 2 * K));
+    uint8_t* p2 = reinterpret_cast<uint8_t*>(cb) + SM::cb_bytes(nblk);
+    double* red_v = reinterpret_cast<double*>(p2 + SM::p2_bytes);
+    int* red_i = reinterpret_cast<int*>(red_v + 32);
+
+    if (p.stamps && cta == 0 && threadIdx.x == 0) p.stamps[img * p.st_istride + 0] = globaltimer();
+
+    // which of my C columns are useful (inside my segment and the image)
+    uint32_t useful = 0;
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+        const int j = col0 + k;
+        if (j >= ucol0 && j < ucol0 + S && j < W) useful |= 1u << k;
+    }
+
+    double m[C];
+    int lab[C];
+    load_row<C>(e, col0, W, m);
+#pragma unroll
+    for (int k = 0; k < C; ++k) lab[k] = col0 + k;
+    // M-boundary row 0 (block 0 starts from it)
+#pragma unroll
+    for (int k = 0; k < C; ++k)
+        if (useful >> k & 1) mbound[col0 + k] = m[k];
+    if (p.m_out) {
+#pragma unroll
+        for (int k = 0; k < C; ++k)
+            if (useful >> k & 1) { p.m_out[col0 + k] = m[k]; p.b_out[col0 + k] = col0 + k; }
+    }
+
+    // mailbox pointers of my neighbours (possibly in other CTAs of the cluster)
+    const int gl = g - 1, gr = g + 1;
+    double* nb_left_m = nullptr;  // left neighbour's right-halo slot (side 1)
+    int* nb_left_l = nullptr;
+    double* nb_right_m = nullptr; // right neighbour's left-halo slot (side 0)
+    int* nb_right_l = nullptr;
+    if (gl >= 0) {
+        nb_left_m = cluster.map_shared_rank(mail_m, gl / NWARP) + ((gl % NWARP) * 2 + 1) * K;
+        nb_left_l = cluster.map_shared_rank(mail_l, gl / NWARP) + ((gl % NWARP) * 2 + 1) * K;
+    }
+    if (gr < G) {
+        nb_right_m = cluster.map_shared_rank(mail_m, gr / NWARP) + ((gr % NWARP) * 2 + 0) * K;
+        nb_right_l = cluster.map_shared_rank(mail_l, gr / NWARP) + ((gr % NWARP) * 2 + 0) * K;
+    }
+    const double* my_m = mail_m + (warp * 2) * K;  // + side*K, + parity*(NWARP*2*K)
+    const int* my_l = mail_l + (warp * 2) * K;
+    constexpr int PSTRIDE = NWARP * 2 * K;
+
+    // register ring: energy rows i+1 .. i+D are in flight while row i computes
+    double ring[D][C];
+#pragma unroll
+    for (int u = 0; u < D; ++u)
+        if (1 + u < H) load_row<C>(e + (long long)(1 + u) * p.epitch, col0, W, ring[u]);
+
+    int kt = 0, lt = 0, blk = 0, par = 0;
+    for (int i0 = 1; i0 < H; i0 += D) {
+#pragma unroll
+      for (int u = 0; u < D; ++u) {
+        const int i = i0 + u;
+        if (i >= H) break;
+        double ecur[C];
+#pragma unroll
+        for (int k = 0; k < C; ++k) ecur[k] = ring[u][k];
+        if (i + D < H) load_row<C>(e + (long long)(i + D) * p.epitch, col0, W, ring[u]);
+        if (lt == 0) {
+#pragma unroll
+            for (int k = 0; k < C; ++k) lab[k] = col0 + k;
+        }
+        const double lm = __shfl_up_sync(FULL, m[C - 1], 1);
+        const int ll = __shfl_up_sync(FULL, lab[C - 1], 1);
+        const double rm = __shfl_down_sync(FULL, m[0], 1);
+        const int rl = __shfl_down_sync(FULL, lab[0], 1);
+        double pm = lm;
+        int pl = ll;
+        uint32_t dbits = 0;
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            const double cm = m[k];
+            const int cl = lab[k];
+            const double nm = (k + 1 < C) ? m[k + 1] : rm;
+            const int nl = (k + 1 < C) ? lab[k + 1] : rl;
+            int d;
+            dp_cell(pm, cm, nm, pl, cl, nl, ecur[k], m[k], lab[k], d);
+            dbits |= uint32_t(d) << (2 * k);
+            pm = cm;
+            pl = cl;
+        }
+        if (p.m_out) {  // parity API only: full cost / predecessor tables
+#pragma unroll
+            for (int k = 0; k < C; ++k)
+                if (useful >> k & 1) {
+                    p.m_out[(long long)i * W + col0 + k] = m[k];
+                    p.b_out[(long long)i * W + col0 + k] = col0 + k + int(dbits >> (2 * k) & 3) - 1;
+                }
+        }
+        if (lt == LBLK - 1 || i == H - 1) {  // block's last row: labels to smem, M to the boundary plane
+#pragma unroll
+            for (int k = 0; k < C; ++k)
+                if (useful >> k & 1) labels[blk * SM::COLS + (col0 + k - cta_col0)] = int8_t(lab[k] - (col0 + k));
+            if (i != H - 1) {
+#pragma unroll
+                for (int k = 0; k < C; ++k)
+                    if (useful >> k & 1) mbound[(long long)(blk + 1) * p.mpitch + col0 + k] = m[k];
+            }
+        }
+        if (++lt == LBLK) { lt = 0; ++blk; }
+        if (++kt == K && i + 1 < H) {
+            kt = 0;
+            // send my K leftmost / rightmost useful columns to the neighbours' halos
+#pragma unroll
+            for (int k = 0; k < C; ++k) {
+                const int wi = lane * C + k;
+                if (wi >= K && wi < 2 * K && nb_left_m) {
+                    nb_left_m[par * PSTRIDE + wi - K] = m[k];
+                    nb_left_l[par * PSTRIDE + wi - K] = lab[k];
+                }
+                if (wi >= 32 * C - 2 * K && wi < 32 * C - K && nb_right_m) {
+                    nb_right_m[par * PSTRIDE + wi - (32 * C - 2 * K)] = m[k];
+                    nb_right_l[par * PSTRIDE + wi - (32 * C - 2 * K)] = lab[k];
+                }
+            }
+            if (ncl > 1) cluster.sync();
+            else __syncthreads();
+            if (lane < KL) {
+#pragma unroll
+                for (int k = 0; k < C; ++k) {
+                    const int wi = lane * C + k;
+                    m[k] = gl >= 0 ? my_m[par * PSTRIDE + wi] : dinf();
+                    lab[k] = gl >= 0 ? my_l[par * PSTRIDE + wi] : 0;
+                }
+            }
+            if (lane >= 32 - KL) {
+#pragma unroll
+                for (int k = 0; k < C; ++k) {
+                    const int wi = lane * C + k - (32 * C - K);
+                    m[k] = gr < G ? my_m[par * PSTRIDE + K + wi] : dinf();
+                    lab[k] = gr < G ? my_l[par * PSTRIDE + K + wi] : 0;
+                }
+            }
+            par ^= 1;
+        }
+      }
+    }
+
+    // ---- K3a: argmin of the bottom row over useful columns (solvers.hpp:94-99)
+    double bv = dinf();
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int k = 0; k < C; ++k)
+        if ((useful >> k & 1) && m[k] < bv) { bv = m[k]; bi = col0 + k; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) argmin_combine(bv, bi, __shfl_xor_sync(FULL, bv, o), __shfl_xor_sync(FULL, bi, o));
+    if (lane == 0) { red_v[warp] = bv; red_i[warp] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < NWARP; ++w) argmin_combine(bv, bi, red_v[w], red_i[w]);
+        red_v[NWARP] = bv;  // this CTA's result
+        red_i[NWARP] = bi;
+    }
+    __threadfence();
+    if (ncl > 1) cluster.sync();
+    else __syncthreads();
+
+    // ---- K3b phase 1 (CTA 0, one thread): block-boundary columns through the labels
+    if (cta == 0 && threadIdx.x == 0) {
+        for (int r = 1; r < ncl; ++r) {
+            const double* rv = cluster.map_shared_rank(red_v, r);
+            const int* ri = cluster.map_shared_rank(red_i, r);
+            argmin_combine(bv, bi, rv[NWARP], ri[NWARP]);
+        }
+        int c = bi;
+        seam[H - 1] = c;
+        for (int b = nblk - 1; b >= 0; --b) {
+            cb[b] = c;
+            const int owner = (c / S) / NWARP;
+            const int8_t* lb = cluster.map_shared_rank(labels, owner);
+            c += lb[b * SM::COLS + (c - owner * SM::COLS)];
+            if (b > 0) seam[LBLK * b] = c;  // row 32b = last row of block b-1
+        }
+        if (nblk > 0) seam[0] = c;
+    }
+    if (ncl > 1) cluster.sync();
+    else __syncthreads();
+
+    // ---- K3b phase 2: every warp recomputes blocks g, g+G, ... in a 128-column window
+    {
+        const int* cb0 = cluster.map_shared_rank(cb, 0);
+        uint8_t* dirs = p2 + size_t(warp) * LBLK * P2_COLS;
+        for (int b = g; b < nblk; b += G) {
+            const int c1 = cb0[b];
+            const int r0 = 1 + LBLK * b, r1 = min(LBLK * (b + 1), H - 1);
+            const int wc0 = c1 - P2_COLS / 2 + lane * 4;
+            double mm[4];
+            int ll4[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int j = wc0 + k;
+                mm[k] = (j >= 0 && j < W) ? mbound[(long long)b * p.mpitch + j] : dinf();
+                ll4[k] = 0;
+            }
+            double en[4];
+            load_row<4>(e + (long long)r0 * p.epitch, wc0, W, en);
+            for (int r = r0; r <= r1; ++r) {
+                double ec[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) ec[k] = en[k];
+                if (r + 1 <= r1) load_row<4>(e + (long long)(r + 1) * p.epitch, wc0, W, en);
+                const double lm = __shfl_up_sync(FULL, mm[3], 1);
+                const double rm = __shfl_down_sync(FULL, mm[0], 1);
+                double pm = lane == 0 ? dinf() : lm;
+                const double rr = lane == 31 ? dinf() : rm;
+                uint32_t db = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const double cm = mm[k];
+                    const double nm = (k + 1 < 4) ? mm[k + 1] : rr;
+                    int d, dummy;
+                    dp_cell(pm, cm, nm, 0, 0, 0, ec[k], mm[k], dummy, d);
+                    db |= uint32_t(d) << (8 * k);
+                    pm = cm;
+                }
+                reinterpret_cast<uint32_t*>(dirs + (r - r0) * P2_COLS)[lane] = db;
+                (void)ll4;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                int c = c1;
+                for (int r = r1; r >= r0; --r) {
+                    c += int(dirs[(r - r0) * P2_COLS + (c - (c1 - P2_COLS / 2))]) - 1;
+                    if (r - 1 != LBLK * b || b == 0) seam[r - 1] = c;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    if (p.stamps) {
+        if (ncl > 1) cluster.sync();
+        else __syncthreads();
+        if (cta == 0 && threadIdx.x == 0) p.stamps[img * p.st_istride + 1] = globaltimer();
+    }
+}
+
+}  // namespace carve_dev
