@@ -29,7 +29,7 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcarve_cuda.so")
+LIB_PATH = os.environ.get("CARVE_LIB") or os.path.join(HERE, "libcarve_cuda.so")
 
 
 class Errc(enum.IntEnum):

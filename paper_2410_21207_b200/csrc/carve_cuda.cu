@@ -324,6 +324,7 @@ void launch_dp2(Ctx& c, const Dp2Plan& pl, Dp2Params p, int nimg, cudaStream_t s
     const Dp2Variant& v = *pl.v;
     p.G = pl.ncl * v.NW;
     p.nblk = pl.nblk;
+    p.dbg = env_int("CARVE_DP_DBG", 0);
     auto it = c.smem_set.find(v.fn);
     if (it == c.smem_set.end()) {
         ck(cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kDpSmemBudget),

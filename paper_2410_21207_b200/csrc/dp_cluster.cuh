@@ -31,10 +31,23 @@
 #pragma once
 #include <cooperative_groups.h>
 #include <cstdint>
+#include <cstdio>
 
 namespace carve_dev {
 
 namespace cg = cooperative_groups;
+
+#ifdef CARVE_DEBUG
+#define DP2_ALIGN(ptr, n, tag)                                                                                  \
+    do {                                                                                                       \
+        if ((reinterpret_cast<uintptr_t>(ptr) % (n)) != 0)                                                    \
+            printf("misaligned %s: %p blk %d thr %d\n", tag, (const void*)(ptr), int(blockIdx.x), int(threadIdx.x)); \
+    } while (0)
+#else
+#define DP2_ALIGN(ptr, n, tag) \
+    do {                       \
+    } while (0)
+#endif
 
 constexpr int LBLK = 32;      // label / M-boundary block height (rows)
 constexpr int P2_COLS = 128;  // phase-2 window: 32 lanes x 4 columns
@@ -52,6 +65,7 @@ struct Dp2Params {
     int* b_out;        // optional predecessor table (pitch W)
     unsigned long long* stamps;  // optional [start, end]
     long long e_istride, mb_istride, s_istride, st_istride;
+    int dbg;           // debugging: bit0 skips phase 2, bit1 skips phase 1, bit2 skips the walk
 };
 
 // smem layout (dynamic): labels int8 [nblk][NWARP*S] | mailbox | cb | phase-2 dirs | reduce
@@ -86,6 +100,7 @@ __device__ __forceinline__ void load_row(const double* __restrict__ row, int col
     if (col0 >= 0 && col0 + C <= W) {
 #pragma unroll
         for (int k = 0; k < C; k += 2) {
+            DP2_ALIGN(row + col0 + k, 16, "load_row");
             const double2 x = __ldg(reinterpret_cast<const double2*>(row + col0 + k));
             v[k] = x.x;
             v[k + 1] = x.y;
@@ -134,6 +149,9 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     int* red_i = reinterpret_cast<int*>(red_v + 32);
 
     if (p.stamps && cta == 0 && threadIdx.x == 0) p.stamps[img * p.st_istride + 0] = globaltimer();
+    DP2_ALIGN(mail_m, 16, "mail_m");
+    DP2_ALIGN(red_v, 16, "red_v");
+    DP2_ALIGN(mbound, 16, "mbound");
 
     // which of my C columns are useful (inside my segment and the image)
     uint32_t useful = 0;
@@ -241,10 +259,12 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
             for (int k = 0; k < C; ++k) {
                 const int wi = lane * C + k;
                 if (wi >= K && wi < 2 * K && nb_left_m) {
+                    DP2_ALIGN(&nb_left_m[par * PSTRIDE + wi - K], 8, "mail_left");
                     nb_left_m[par * PSTRIDE + wi - K] = m[k];
                     nb_left_l[par * PSTRIDE + wi - K] = lab[k];
                 }
                 if (wi >= 32 * C - 2 * K && wi < 32 * C - K && nb_right_m) {
+                    DP2_ALIGN(&nb_right_m[par * PSTRIDE + wi - (32 * C - 2 * K)], 8, "mail_right");
                     nb_right_m[par * PSTRIDE + wi - (32 * C - 2 * K)] = m[k];
                     nb_right_l[par * PSTRIDE + wi - (32 * C - 2 * K)] = lab[k];
                 }
@@ -292,7 +312,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     else __syncthreads();
 
     // ---- K3b phase 1 (CTA 0, one thread): block-boundary columns through the labels
-    if (cta == 0 && threadIdx.x == 0) {
+    if (cta == 0 && threadIdx.x == 0 && !(p.dbg & 2)) {
         for (int r = 1; r < ncl; ++r) {
             const double* rv = cluster.map_shared_rank(red_v, r);
             const int* ri = cluster.map_shared_rank(red_i, r);
@@ -316,10 +336,11 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     {
         const int* cb0 = cluster.map_shared_rank(cb, 0);
         uint8_t* dirs = p2 + size_t(warp) * LBLK * P2_COLS;
-        for (int b = g; b < nblk; b += G) {
+        for (int b = g; b < nblk && !(p.dbg & 1); b += G) {
             const int c1 = cb0[b];
             const int r0 = 1 + LBLK * b, r1 = min(LBLK * (b + 1), H - 1);
-            const int wc0 = c1 - P2_COLS / 2 + lane * 4;
+            const int wbase = (c1 - P2_COLS / 2) & ~1;  // even: 16-byte aligned double2 loads
+            const int wc0 = wbase + lane * 4;
             double mm[4];
             int ll4[4];
 #pragma unroll
@@ -349,14 +370,15 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
                     db |= uint32_t(d) << (8 * k);
                     pm = cm;
                 }
+                DP2_ALIGN(dirs + (r - r0) * P2_COLS + 4 * lane, 4, "dirs");
                 reinterpret_cast<uint32_t*>(dirs + (r - r0) * P2_COLS)[lane] = db;
                 (void)ll4;
             }
             __syncwarp();
-            if (lane == 0) {
+            if (lane == 0 && !(p.dbg & 4)) {
                 int c = c1;
                 for (int r = r1; r >= r0; --r) {
-                    c += int(dirs[(r - r0) * P2_COLS + (c - (c1 - P2_COLS / 2))]) - 1;
+                    c += int(dirs[(r - r0) * P2_COLS + (c - wbase)]) - 1;
                     if (r - 1 != LBLK * b || b == 0) seam[r - 1] = c;
                 }
             }
