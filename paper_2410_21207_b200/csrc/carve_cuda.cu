@@ -38,10 +38,22 @@ void ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess) fail(CARVE_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-#define LAUNCHED(what)                              \
-    do {                                            \
-        ++t_launches;                               \
-        ck(cudaGetLastError(), "launch " what);     \
+bool sync_debug() {
+    static const bool on = [] {
+        const char* e = std::getenv("CARVE_SYNC_DEBUG");
+        return e && *e == '1';
+    }();
+    return on;
+}
+
+thread_local long long t_dbg_tag = 0;  // caller-set context for CARVE_SYNC_DEBUG reports
+
+#define LAUNCHED(what)                                                                            \
+    do {                                                                                          \
+        ++t_launches;                                                                             \
+        ck(cudaGetLastError(), "launch " what);                                                   \
+        if (sync_debug())                                                                         \
+            ck(cudaDeviceSynchronize(), (std::string("after " what " tag ") + std::to_string(t_dbg_tag)).c_str()); \
     } while (0)
 
 template <class F>
@@ -125,6 +137,8 @@ struct Ctx {
 
 thread_local std::map<int, std::unique_ptr<Ctx>> t_ctx;
 
+void init_kernel_attributes(Ctx& c);  // defined after the kernel tables
+
 enum KernelKind { KK_ENERGY = 0, KK_DP = 1, KK_COMPACT = 2, KK_UNPACK = 3, KK_PACK = 4, KK_TRANSPOSE = 5, KK_N = 6 };
 
 // RAII bracket: records an event pair around one launch when profiling is on
@@ -156,6 +170,8 @@ Ctx& ctx() {
         if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) fail(CARVE_E_CUDA, "no CUDA device available");
         if (t_device < 0 || t_device >= n) fail(CARVE_E_CUDA, "invalid device index");
         it = t_ctx.emplace(t_device, std::make_unique<Ctx>(t_device)).first;
+        // kernel attributes are set once, before any launch on this context
+        init_kernel_attributes(*it->second);
     }
     ck(cudaSetDevice(it->second->device), "cudaSetDevice");
     return *it->second;
@@ -193,11 +209,20 @@ void launch_transpose(const uint32_t* in, int ipitch, int W, int H, uint32_t* ou
     LAUNCHED("k_transpose");
 }
 
-void launch_energy(const uint32_t* rgb, int pitch, int W, int H, double* e, int nimg, long long is, cudaStream_t s) {
+void launch_energy(const uint32_t* rgb, int pitch, int W, int H, double* e, int epitch, int nimg, long long rgb_is,
+                   long long e_is, cudaStream_t s) {
     dim3 grid((W + K1_TW - 1) / K1_TW, (H + K1_TH - 1) / K1_TH, nimg);
-    k_energy_full<<<grid, 256, 0, s>>>(rgb, pitch, W, H, e, pitch, is, is);
+    k_energy_full<<<grid, 256, 0, s>>>(rgb, pitch, W, H, e, epitch, rgb_is, e_is);
     LAUNCHED("k_energy_full");
 }
+
+void launch_fill_pads(double* e, int epitch, int W, int H, int nimg, long long e_is, cudaStream_t s) {
+    dim3 grid(grid_for((long long)H * (EPAD_L + EPAD_R), 256), nimg);
+    k_fill_pads<<<grid, 256, 0, s>>>(e, epitch, W, H, e_is);
+    LAUNCHED("k_fill_pads");
+}
+
+int padded_epitch(int w) { return int(round_up(size_t(EPAD_L) + w + EPAD_R, 32)); }
 
 constexpr int kDpSmemBudget = 220 * 1024;
 constexpr int kMaxWinWarps = 16;
@@ -244,12 +269,6 @@ DpShape dp_shape(int W, int H) {
 template <int C, int D>
 void launch_dp_t(Ctx& c, const DpShape& d, const DpParams& p, int nimg, cudaStream_t s) {
     auto k = k_dp_seam<C, D>;
-    auto it = c.smem_set.find((const void*)k);
-    if (it == c.smem_set.end() || it->second < int(d.smem)) {
-        ck(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kDpSmemBudget),
-           "cudaFuncSetAttribute(dp smem)");
-        c.smem_set[(const void*)k] = kDpSmemBudget;
-    }
     k<<<nimg, d.threads, d.smem, s>>>(p);
     LAUNCHED("k_dp_seam");
 }
@@ -267,7 +286,8 @@ void launch_dp(Ctx& c, const DpShape& d, const DpParams& p, int nimg, cudaStream
 // ---- K2+K3 v2: cluster trapezoid DP (dp_cluster.cuh) ------------------------
 struct Dp2Variant {
     int C, K, NW, D;
-    const void* fn;
+    const void* fn;        // hot kernel (no tables)
+    const void* fn_tables; // parity-API kernel (writes the full cost / predecessor tables)
     size_t (*smem)(int nblk);
     int S() const { return 32 * C - 2 * K; }
     int cols() const { return NW * S(); }
@@ -275,7 +295,8 @@ struct Dp2Variant {
 
 template <int C, int K, int NW, int D>
 constexpr Dp2Variant dp2_variant() {
-    return Dp2Variant{C, K, NW, D, (const void*)k_dp2<C, K, NW, D>, &Dp2Smem<C, K, NW>::total};
+    return Dp2Variant{C, K, NW, D, (const void*)k_dp2<C, K, NW, D, false>, (const void*)k_dp2<C, K, NW, D, true>,
+                      &Dp2Smem<C, K, NW>::total};
 }
 
 // preference order: the first variant whose cluster fits (<= 8 CTAs, then <= 16) wins
@@ -287,9 +308,28 @@ const Dp2Variant kDp2Variants[] = {
     dp2_variant<8, 32, 4, 4>(),   // 4: S=192, 768 cols/CTA
     dp2_variant<4, 16, 8, 8>(),   // 5: S=96,  768 cols/CTA
     dp2_variant<2, 8, 8, 8>(),    // 6: S=48,  384 cols/CTA
-    dp2_variant<8, 16, 16, 4>(),  // 7: S=224, 3584 cols/CTA
+    dp2_variant<2, 8, 16, 8>(),   // 7: S=48,  768 cols/CTA
+    dp2_variant<2, 16, 8, 8>(),   // 8: S=32,  256 cols/CTA
+    dp2_variant<4, 32, 4, 8>(),   // 9: S=64,  256 cols/CTA
 };
 constexpr int kNumDp2Variants = int(sizeof(kDp2Variants) / sizeof(kDp2Variants[0]));
+
+void init_kernel_attributes(Ctx& c) {
+    for (const Dp2Variant& v : kDp2Variants)
+        for (const void* fn : {v.fn, v.fn_tables}) {
+            ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kDpSmemBudget),
+               "cudaFuncSetAttribute(dp2 smem)");
+            ck(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+               "cudaFuncSetAttribute(dp2 cluster)");
+            c.smem_set[fn] = kDpSmemBudget;
+        }
+    for (const void* fn : {(const void*)k_dp_seam<1, 4>, (const void*)k_dp_seam<2, 4>, (const void*)k_dp_seam<4, 2>,
+                           (const void*)k_dp_seam<8, 2>, (const void*)k_dp_seam<16, 1>}) {
+        ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kDpSmemBudget),
+           "cudaFuncSetAttribute(dp smem)");
+        c.smem_set[fn] = kDpSmemBudget;
+    }
+}
 
 struct Dp2Plan {
     const Dp2Variant* v;
@@ -313,6 +353,8 @@ Dp2Plan dp2_plan(int W, int H) {
             const int ncl = (W + v.cols() - 1) / v.cols();
             const size_t smem = v.smem(nblk);
             if (ncl > (pass == 0 ? max_ncl : 16) || smem > size_t(kDpSmemBudget)) continue;
+            // columns read past the image edge must stay inside the +inf pad
+            if (ncl * v.cols() - W + v.K + 32 * v.C > EPAD_R) continue;
             return Dp2Plan{&v, ncl, nblk, smem};
         }
     }
@@ -325,14 +367,8 @@ void launch_dp2(Ctx& c, const Dp2Plan& pl, Dp2Params p, int nimg, cudaStream_t s
     p.G = pl.ncl * v.NW;
     p.nblk = pl.nblk;
     p.dbg = env_int("CARVE_DP_DBG", 0);
-    auto it = c.smem_set.find(v.fn);
-    if (it == c.smem_set.end()) {
-        ck(cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kDpSmemBudget),
-           "cudaFuncSetAttribute(dp2 smem)");
-        ck(cudaFuncSetAttribute(v.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
-           "cudaFuncSetAttribute(dp2 cluster)");
-        c.smem_set[v.fn] = kDpSmemBudget;
-    }
+    const void* fn = p.m_out ? v.fn_tables : v.fn;
+    if (c.smem_set.find(fn) == c.smem_set.end()) fail(CARVE_E_CUDA, "DP kernel attributes not initialised");
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(nimg * pl.ncl));
     cfg.blockDim = dim3(unsigned(v.NW * 32));
@@ -346,7 +382,7 @@ void launch_dp2(Ctx& c, const Dp2Plan& pl, Dp2Params p, int nimg, cudaStream_t s
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     void* args[] = {&p};
-    ck(cudaLaunchKernelExC(&cfg, v.fn, args), "launch k_dp2");
+    ck(cudaLaunchKernelExC(&cfg, fn, args), "launch k_dp2");
     LAUNCHED("k_dp2");
 }
 
@@ -371,6 +407,8 @@ struct CarveGeometry {
     int nseams;
     int mpitch;       // M-boundary row pitch (doubles)
     long long mb_istride;
+    int epitch_a, epitch_b;  // padded energy-plane pitches per phase
+    size_t eplane;           // doubles per image energy plane (max over phases, incl. pads)
 };
 
 CarveGeometry geometry(int w, int h, int tw, int th) {
@@ -388,6 +426,10 @@ CarveGeometry geometry(int w, int h, int tw, int th) {
     g.seam_ints = size_t(w - tw) * h + size_t(h - th) * tw;
     g.nseams = (w - tw) + (h - th);
     g.mpitch = std::max(g.pitch_a, g.pitch_b);
+    g.epitch_a = padded_epitch(w);
+    g.epitch_b = padded_epitch(h);
+    g.eplane = size_t(g.epitch_a) * (h + EPAD_B);
+    if (th != h) g.eplane = std::max(g.eplane, size_t(g.epitch_b) * (tw + EPAD_B));
     g.mb_istride = (long long)((g.dir_rows + LBLK - 1) / LBLK + 1) * g.mpitch;
     return g;
 }
@@ -409,7 +451,8 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
                size_t seam_istride, unsigned long long* d_stamps, cudaStream_t s) {
     const long long in_is = (long long)g.w * g.h * 3, out_is = (long long)g.tw * g.th * 3;
     uint32_t* rgb[2] = {c.rgb[0].as<uint32_t>(), c.rgb[1].as<uint32_t>()};
-    double* e[2] = {c.e[0].as<double>(), c.e[1].as<double>()};
+    double* e[2] = {c.e[0].as<double>() + EPAD_L, c.e[1].as<double>() + EPAD_L};  // logical column 0
+    const long long eis = (long long)g.eplane;
     uint8_t* dir = c.dir.as<uint8_t>();
     const long long pis = (long long)g.plane;
     const long long dis = (long long)g.dpitch * g.dir_rows;
@@ -421,23 +464,27 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
         launch_unpack(c, d_in, g.w, g.h, rgb[cur], g.pitch_a, nimg, in_is, pis, s);
     }
 
-    auto phase = [&](int W0, int H, int ntake, int pitch, int seam_base, int stamp_seam0, int estamp) {
+    auto phase = [&](int W0, int H, int ntake, int pitch, int epitch, int seam_base, int stamp_seam0, int estamp) {
         if (ntake <= 0) return;
         {
             // algorithmic bytes: 3 B RGB read + 8 B FP64 write per pixel
             Prof pr(c, s, KK_ENERGY, 11.0 * W0 * H * nimg);
-            launch_energy(rgb[cur], pitch, W0, H, e[cur], nimg, pis, s);
+            launch_energy(rgb[cur], pitch, W0, H, e[cur], epitch, nimg, pis, eis, s);
         }
+        // both ping-pong planes: compaction keeps the right pad growing by one +inf column per seam
+        launch_fill_pads(e[cur], epitch, W0, H, nimg, eis, s);
+        launch_fill_pads(e[cur ^ 1], epitch, W0, H, nimg, eis, s);
         (void)estamp;
         for (int k = 0; k < ntake; ++k) {
             const int W = W0 - k;
+            t_dbg_tag = W;
             DpParams p{};
             p.seam = d_seams + seam_base + size_t(k) * H;
             p.stamps = d_stamps ? d_stamps + size_t(stamp_seam0 + k) * 4 : nullptr;
             if (dp_v1) {
                 const DpShape d = dp_shape(W, H);
                 p.e = e[cur];
-                p.epitch = pitch;
+                p.epitch = epitch;
                 p.W = W;
                 p.H = H;
                 p.dir = dir;
@@ -445,7 +492,7 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
                 p.R = d.R;
                 p.nblk = d.nblk;
                 p.nwin = d.nwin;
-                p.e_istride = pis;
+                p.e_istride = eis;
                 p.d_istride = dis;
                 p.s_istride = (long long)seam_istride;
                 p.st_istride = (long long)sw;
@@ -456,14 +503,14 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
                 const Dp2Plan pl = dp2_plan(W, H);
                 Dp2Params q{};
                 q.e = e[cur];
-                q.epitch = pitch;
+                q.epitch = epitch;
                 q.W = W;
                 q.H = H;
                 q.mbound = c.mbound.as<double>();
                 q.mpitch = g.mpitch;
                 q.seam = p.seam;
                 q.stamps = p.stamps;
-                q.e_istride = pis;
+                q.e_istride = eis;
                 q.mb_istride = g.mb_istride;
                 q.s_istride = (long long)seam_istride;
                 q.st_istride = (long long)sw;
@@ -478,11 +525,13 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
             q.e_in = last ? nullptr : e[cur];  // the final width needs no energy
             q.e_out = e[cur ^ 1];
             q.pitch = pitch;
+            q.epitch = epitch;
             q.W = W;
             q.H = H;
             q.seam = p.seam;
             q.stamps = d_stamps ? d_stamps + size_t(stamp_seam0 + k) * 4 + 2 : nullptr;
             q.p_istride = pis;
+            q.e_istride = eis;
             q.s_istride = (long long)seam_istride;
             q.st_istride = (long long)sw;
             {
@@ -493,14 +542,14 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
             cur ^= 1;
         }
     };
-    phase(g.w, g.h, g.w - g.tw, g.pitch_a, 0, 0, 0);
+    phase(g.w, g.h, g.w - g.tw, g.pitch_a, g.epitch_a, 0, 0, 0);
     if (g.th != g.h) {
         {
             Prof pr(c, s, KK_TRANSPOSE, 8.0 * g.tw * g.h * nimg);
             launch_transpose(rgb[cur], g.pitch_a, g.tw, g.h, rgb[cur ^ 1], g.pitch_b, nimg, pis, pis, s);
         }
         cur ^= 1;
-        phase(g.h, g.tw, g.h - g.th, g.pitch_b, (g.w - g.tw) * g.h, g.w - g.tw, 2);
+        phase(g.h, g.tw, g.h - g.th, g.pitch_b, g.epitch_b, (g.w - g.tw) * g.h, g.w - g.tw, 2);
         Prof pr(c, s, KK_PACK, 7.0 * g.tw * g.th * nimg);
         launch_pack(c, rgb[cur], g.pitch_b, g.tw, g.th, true, d_out, nimg, pis, out_is, s);
     } else {
@@ -512,7 +561,7 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
 void ensure_carve_buffers(Ctx& c, const CarveGeometry& g, int nimg) {
     for (int k = 0; k < 2; ++k) {
         c.rgb[k].ensure(g.plane * 4 * nimg);
-        c.e[k].ensure(g.plane * 8 * nimg);
+        c.e[k].ensure(g.eplane * 8 * nimg);
     }
     c.dir.ensure(size_t(g.dpitch) * g.dir_rows * nimg + 256);
     c.mbound.ensure(size_t(g.mb_istride) * 8 * nimg);
@@ -689,7 +738,7 @@ carve_status carve_cuda_energy_e1_rgb(const uint8_t* rgb, int w, int h, double* 
         double* e = static_cast<double*>(c.e[0].ensure(size_t(pitch) * h * 8));
         ck(cudaMemcpyAsync(d_in, rgb, size_t(w) * h * 3, cudaMemcpyHostToDevice, c.stream), "H2D");
         launch_unpack(c, d_in, w, h, plane, pitch, 1, 0, 0, c.stream);
-        launch_energy(plane, pitch, w, h, e, 1, 0, c.stream);
+        launch_energy(plane, pitch, w, h, e, pitch, 1, 0, 0, c.stream);
         ck(cudaMemcpy2DAsync(e_out, size_t(w) * 8, e, size_t(pitch) * 8, size_t(w) * 8, h, cudaMemcpyDeviceToHost,
                              c.stream),
            "D2H");
@@ -736,7 +785,8 @@ carve_status carve_cuda_dp_seam(const double* e, int w, int h, double* m_out, in
         Ctx& c = ctx();
         const Dp2Plan pl = dp2_plan(w, h);
         const int pitch = int(round_up(w, 32));
-        double* de = static_cast<double*>(c.e[0].ensure(size_t(pitch) * h * 8));
+        const int epitch = padded_epitch(w);
+        double* de = static_cast<double*>(c.e[0].ensure(size_t(epitch) * (h + EPAD_B) * 8)) + EPAD_L;
         double* mb = static_cast<double*>(c.mbound.ensure(size_t(pl.nblk + 1) * pitch * 8));
         int* dseam = static_cast<int*>(c.seams.ensure(size_t(h) * 4));
         double* dm = nullptr;
@@ -745,12 +795,13 @@ carve_status carve_cuda_dp_seam(const double* e, int w, int h, double* m_out, in
             dm = static_cast<double*>(c.scratch_a.ensure(size_t(w) * h * 8));
             db = static_cast<int*>(c.scratch_b.ensure(size_t(w) * h * 4));
         }
-        ck(cudaMemcpy2DAsync(de, size_t(pitch) * 8, e, size_t(w) * 8, size_t(w) * 8, h, cudaMemcpyHostToDevice,
+        ck(cudaMemcpy2DAsync(de, size_t(epitch) * 8, e, size_t(w) * 8, size_t(w) * 8, h, cudaMemcpyHostToDevice,
                              c.stream),
            "H2D energy");
+        launch_fill_pads(de, epitch, w, h, 1, 0, c.stream);
         Dp2Params p{};
         p.e = de;
-        p.epitch = pitch;
+        p.epitch = epitch;
         p.W = w;
         p.H = h;
         p.mbound = mb;

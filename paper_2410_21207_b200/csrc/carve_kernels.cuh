@@ -24,6 +24,15 @@ namespace carve_dev {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+// Energy-plane padding: every FP64 energy row carries EPAD_L
+// columns of +inf before logical column 0 and at least EPAD_R columns of +inf
+// after the last live column, and the plane has EPAD_B spare rows at the
+// bottom, so the DP's row loads are unconditional aligned 128-bit loads and
+// out-of-image neighbours are +inf by construction (SPEC.md:315 exclusion).
+// EPAD_R covers the widest overhang of a DP cluster past the image edge
+// (one CTA's useful columns + halo + a warp's span; checked on the host).
+constexpr int EPAD_L = 128, EPAD_R = 2304, EPAD_B = 16;
+
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -167,6 +176,19 @@ __global__ void __launch_bounds__(256) k_energy_full(const uint32_t* __restrict_
     rgb += blockIdx.z * rgb_istride;
     e += blockIdx.z * e_istride;
     k1_tile(rgb, pitch, W, H, e, epitch, blockIdx.y * K1_TH, blockIdx.x * K1_TW, L);
+}
+
+// +inf into the left/right pad columns of rows [0, H) (e points at logical column 0)
+__global__ void k_fill_pads(double* __restrict__ e, int epitch, int W, int H, long long e_istride) {
+    e += blockIdx.y * e_istride;
+    const double inf = dinf();
+    constexpr int N = EPAD_L + EPAD_R;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < (long long)H * N;
+         k += (long long)gridDim.x * blockDim.x) {
+        const int i = int(k / N), c = int(k - (long long)i * N);
+        const int j = c < EPAD_L ? c - EPAD_L : W + (c - EPAD_L);
+        e[(long long)i * epitch + j] = inf;
+    }
 }
 
 // Luma plane -> e1 (the LumaGrid overload of energy_e1, energy.hpp:89-98).
@@ -546,11 +568,12 @@ struct CompactParams {
     uint32_t* rgb_out;
     const double* e_in;  // nullable: RGB-only removal
     double* e_out;
-    int pitch;  // shared by rgb and energy planes
+    int pitch;   // RGBX plane pitch (elements)
+    int epitch;  // energy plane pitch (doubles); e_in/e_out point at logical column 0
     int W, H;
     const int* seam;
     unsigned long long* stamps;  // optional [start, end] per image (written by block 0 / last block)
-    long long p_istride, s_istride, st_istride;
+    long long p_istride, e_istride, s_istride, st_istride;
 };
 
 __global__ void __launch_bounds__(256) k_compact(CompactParams p) {
@@ -565,9 +588,16 @@ __global__ void __launch_bounds__(256) k_compact(CompactParams p) {
         const int s = __ldg(seam + i);
         const long long ro = (long long)i * p.pitch;
         compact_row<uint32_t>(rgb_in + ro, rgb_out + ro, p.W, s, lane, nullptr, 0, 0, nullptr, 0, false);
-        if (p.e_in)
-            compact_row<double>(p.e_in + img * p.p_istride + ro, p.e_out + img * p.p_istride + ro, p.W, s, lane,
-                                rgb_in, p.pitch, p.H, seam, i, true);
+        if (p.e_in) {
+            const long long eo = img * p.e_istride + (long long)i * p.epitch;
+            compact_row<double>(p.e_in + eo, p.e_out + eo, p.W, s, lane, rgb_in, p.pitch, p.H, seam, i, true);
+            // the vacated column joins the +inf pad; so does the column this plane
+            // last held live (planes alternate, so it may still be stale)
+            if (lane == 0) {
+                p.e_out[eo + p.W - 1] = dinf();
+                p.e_out[eo + p.W] = dinf();
+            }
+        }
     }
     if (p.stamps && threadIdx.x == 0) {
         // last block to finish stamps the end (monotonic max)

@@ -68,17 +68,16 @@ struct Dp2Params {
     int dbg;           // debugging: bit0 skips phase 2, bit1 skips phase 1, bit2 skips the walk
 };
 
-// smem layout (dynamic): labels int8 [nblk][NWARP*S] | mailbox | cb | phase-2 dirs | reduce
+// smem layout (dynamic): labels int8 [nblk][NWARP*S] | mailbox | phase-2 dirs | reduce
 template <int C, int K, int NWARP>
 struct Dp2Smem {
     static constexpr int S = 32 * C - 2 * K;
     static constexpr int COLS = NWARP * S;  // useful columns per CTA
     __host__ __device__ static size_t labels_bytes(int nblk) { return (size_t(nblk) * COLS + 15) & ~size_t(15); }
     static constexpr size_t mail_bytes = size_t(2) * NWARP * 2 * K * (8 + 4);
-    __host__ __device__ static size_t cb_bytes(int nblk) { return (size_t(nblk + 1) * 4 + 15) & ~size_t(15); }
     static constexpr size_t p2_bytes = size_t(NWARP) * LBLK * P2_COLS;
     static constexpr size_t red_bytes = 64 * 16;
-    __host__ __device__ static size_t total(int nblk) { return labels_bytes(nblk) + mail_bytes + cb_bytes(nblk) + p2_bytes + red_bytes; }
+    __host__ __device__ static size_t total(int nblk) { return labels_bytes(nblk) + mail_bytes + p2_bytes + red_bytes; }
 };
 
 // the 9-instruction cell update shared by the forward pass and phase 2
@@ -94,23 +93,16 @@ __device__ __forceinline__ void dp_cell(double L, double M, double R, int lL, in
     lab = bl;
 }
 
+// C consecutive energies starting at col0 (even): unconditional aligned
+// 128-bit loads — the padded plane (EPAD_L/EPAD_R, +inf) covers every column a
+// warp or a phase-2 window can touch.
 template <int C>
-__device__ __forceinline__ void load_row(const double* __restrict__ row, int col0, int W, double (&v)[C]) {
-    // C consecutive columns starting at col0 (even); +inf outside the image
-    if (col0 >= 0 && col0 + C <= W) {
+__device__ __forceinline__ void load_row(const double* __restrict__ row, int col0, double (&v)[C]) {
 #pragma unroll
-        for (int k = 0; k < C; k += 2) {
-            DP2_ALIGN(row + col0 + k, 16, "load_row");
-            const double2 x = __ldg(reinterpret_cast<const double2*>(row + col0 + k));
-            v[k] = x.x;
-            v[k + 1] = x.y;
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < C; ++k) {
-            const int j = col0 + k;
-            v[k] = (j >= 0 && j < W) ? __ldg(row + j) : dinf();
-        }
+    for (int k = 0; k < C; k += 2) {
+        const double2 x = __ldg(reinterpret_cast<const double2*>(row + col0 + k));
+        v[k] = x.x;
+        v[k + 1] = x.y;
     }
 }
 
@@ -118,7 +110,7 @@ __device__ __forceinline__ void argmin_combine(double& v, int& i, double ov, int
     if (ov < v || (ov == v && oi < i)) { v = ov; i = oi; }
 }
 
-template <int C, int K, int NWARP, int D>
+template <int C, int K, int NWARP, int D, bool TABLES>
 __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     static_assert(K % C == 0 && (32 * C) > 2 * K, "halo must be whole lanes and leave useful columns");
     using SM = Dp2Smem<C, K, NWARP>;
@@ -143,15 +135,11 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     int8_t* labels = reinterpret_cast<int8_t*>(dsm);
     double* mail_m = reinterpret_cast<double*>(dsm + SM::labels_bytes(nblk));  // [2][NWARP][2][K]
     int* mail_l = reinterpret_cast<int*>(mail_m + 2 * NWARP * 2 * K);
-    int* cb = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(mail_l + 2 * NWARP * 2 * K));
-    uint8_t* p2 = reinterpret_cast<uint8_t*>(cb) + SM::cb_bytes(nblk);
+    uint8_t* p2 = reinterpret_cast<uint8_t*>(mail_l + 2 * NWARP * 2 * K);
     double* red_v = reinterpret_cast<double*>(p2 + SM::p2_bytes);
     int* red_i = reinterpret_cast<int*>(red_v + 32);
 
     if (p.stamps && cta == 0 && threadIdx.x == 0) p.stamps[img * p.st_istride + 0] = globaltimer();
-    DP2_ALIGN(mail_m, 16, "mail_m");
-    DP2_ALIGN(red_v, 16, "red_v");
-    DP2_ALIGN(mbound, 16, "mbound");
 
     // which of my C columns are useful (inside my segment and the image)
     uint32_t useful = 0;
@@ -163,14 +151,14 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
 
     double m[C];
     int lab[C];
-    load_row<C>(e, col0, W, m);
+    load_row<C>(e, col0, m);
 #pragma unroll
     for (int k = 0; k < C; ++k) lab[k] = col0 + k;
     // M-boundary row 0 (block 0 starts from it)
 #pragma unroll
     for (int k = 0; k < C; ++k)
         if (useful >> k & 1) mbound[col0 + k] = m[k];
-    if (p.m_out) {
+    if constexpr (TABLES) {
 #pragma unroll
         for (int k = 0; k < C; ++k)
             if (useful >> k & 1) { p.m_out[col0 + k] = m[k]; p.b_out[col0 + k] = col0 + k; }
@@ -194,26 +182,19 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     const int* my_l = mail_l + (warp * 2) * K;
     constexpr int PSTRIDE = NWARP * 2 * K;
 
-    // register ring: energy rows i+1 .. i+D are in flight while row i computes
+    // Forward pass. Rows 1..H-1 run in K-row blocks, each fully unrolled so
+    // the ring slot, the halo exchange point and the loop control are
+    // compile-time; energy rows i+1..i+D are in flight while row i computes
+    // (slot (i-1) % D is consumed, then refilled with row i+D).
     double ring[D][C];
+    const double* nrow = e + p.epitch;  // next row to load (rows past H-1 are the plane's spare rows)
 #pragma unroll
-    for (int u = 0; u < D; ++u)
-        if (1 + u < H) load_row<C>(e + (long long)(1 + u) * p.epitch, col0, W, ring[u]);
+    for (int u = 0; u < D; ++u) {
+        load_row<C>(nrow, col0, ring[u]);
+        nrow += p.epitch;
+    }
 
-    int kt = 0, lt = 0, blk = 0, par = 0;
-    for (int i0 = 1; i0 < H; i0 += D) {
-#pragma unroll
-      for (int u = 0; u < D; ++u) {
-        const int i = i0 + u;
-        if (i >= H) break;
-        double ecur[C];
-#pragma unroll
-        for (int k = 0; k < C; ++k) ecur[k] = ring[u][k];
-        if (i + D < H) load_row<C>(e + (long long)(i + D) * p.epitch, col0, W, ring[u]);
-        if (lt == 0) {
-#pragma unroll
-            for (int k = 0; k < C; ++k) lab[k] = col0 + k;
-        }
+    auto step = [&](double (&ev)[C], int i) {
         const double lm = __shfl_up_sync(FULL, m[C - 1], 1);
         const int ll = __shfl_up_sync(FULL, lab[C - 1], 1);
         const double rm = __shfl_down_sync(FULL, m[0], 1);
@@ -228,12 +209,12 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
             const double nm = (k + 1 < C) ? m[k + 1] : rm;
             const int nl = (k + 1 < C) ? lab[k + 1] : rl;
             int d;
-            dp_cell(pm, cm, nm, pl, cl, nl, ecur[k], m[k], lab[k], d);
+            dp_cell(pm, cm, nm, pl, cl, nl, ev[k], m[k], lab[k], d);
             dbits |= uint32_t(d) << (2 * k);
             pm = cm;
             pl = cl;
         }
-        if (p.m_out) {  // parity API only: full cost / predecessor tables
+        if constexpr (TABLES) {  // parity API only: full cost / predecessor tables
 #pragma unroll
             for (int k = 0; k < C; ++k)
                 if (useful >> k & 1) {
@@ -241,55 +222,85 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
                     p.b_out[(long long)i * W + col0 + k] = col0 + k + int(dbits >> (2 * k) & 3) - 1;
                 }
         }
-        if (lt == LBLK - 1 || i == H - 1) {  // block's last row: labels to smem, M to the boundary plane
+        (void)dbits;
+        // refill this slot with row i + D
+        load_row<C>(nrow, col0, ev);
+        nrow += p.epitch;
+    };
+    auto block_end = [&](int i, int blk) {  // last row of a label block: labels to smem, M to global
+#pragma unroll
+        for (int k = 0; k < C; ++k)
+            if (useful >> k & 1) labels[blk * SM::COLS + (col0 + k - cta_col0)] = int8_t(lab[k] - (col0 + k));
+        if (i != H - 1) {
 #pragma unroll
             for (int k = 0; k < C; ++k)
-                if (useful >> k & 1) labels[blk * SM::COLS + (col0 + k - cta_col0)] = int8_t(lab[k] - (col0 + k));
-            if (i != H - 1) {
+                if (useful >> k & 1) mbound[(long long)(blk + 1) * p.mpitch + col0 + k] = m[k];
+        }
+    };
+    auto reset_labels = [&]() {
 #pragma unroll
-                for (int k = 0; k < C; ++k)
-                    if (useful >> k & 1) mbound[(long long)(blk + 1) * p.mpitch + col0 + k] = m[k];
+        for (int k = 0; k < C; ++k) lab[k] = col0 + k;
+    };
+    int par = 0;
+    auto exchange = [&]() {
+        // send my K leftmost / rightmost useful columns to the neighbours' halos
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            const int wi = lane * C + k;
+            if (wi >= K && wi < 2 * K && nb_left_m) {
+                nb_left_m[par * PSTRIDE + wi - K] = m[k];
+                nb_left_l[par * PSTRIDE + wi - K] = lab[k];
+            }
+            if (wi >= 32 * C - 2 * K && wi < 32 * C - K && nb_right_m) {
+                nb_right_m[par * PSTRIDE + wi - (32 * C - 2 * K)] = m[k];
+                nb_right_l[par * PSTRIDE + wi - (32 * C - 2 * K)] = lab[k];
             }
         }
-        if (++lt == LBLK) { lt = 0; ++blk; }
-        if (++kt == K && i + 1 < H) {
-            kt = 0;
-            // send my K leftmost / rightmost useful columns to the neighbours' halos
+        if (ncl > 1) cluster.sync();
+        else __syncthreads();
+        if (lane < KL) {
 #pragma unroll
             for (int k = 0; k < C; ++k) {
                 const int wi = lane * C + k;
-                if (wi >= K && wi < 2 * K && nb_left_m) {
-                    DP2_ALIGN(&nb_left_m[par * PSTRIDE + wi - K], 8, "mail_left");
-                    nb_left_m[par * PSTRIDE + wi - K] = m[k];
-                    nb_left_l[par * PSTRIDE + wi - K] = lab[k];
-                }
-                if (wi >= 32 * C - 2 * K && wi < 32 * C - K && nb_right_m) {
-                    DP2_ALIGN(&nb_right_m[par * PSTRIDE + wi - (32 * C - 2 * K)], 8, "mail_right");
-                    nb_right_m[par * PSTRIDE + wi - (32 * C - 2 * K)] = m[k];
-                    nb_right_l[par * PSTRIDE + wi - (32 * C - 2 * K)] = lab[k];
-                }
+                m[k] = gl >= 0 ? my_m[par * PSTRIDE + wi] : dinf();
+                lab[k] = gl >= 0 ? my_l[par * PSTRIDE + wi] : 0;
             }
-            if (ncl > 1) cluster.sync();
-            else __syncthreads();
-            if (lane < KL) {
-#pragma unroll
-                for (int k = 0; k < C; ++k) {
-                    const int wi = lane * C + k;
-                    m[k] = gl >= 0 ? my_m[par * PSTRIDE + wi] : dinf();
-                    lab[k] = gl >= 0 ? my_l[par * PSTRIDE + wi] : 0;
-                }
-            }
-            if (lane >= 32 - KL) {
-#pragma unroll
-                for (int k = 0; k < C; ++k) {
-                    const int wi = lane * C + k - (32 * C - K);
-                    m[k] = gr < G ? my_m[par * PSTRIDE + K + wi] : dinf();
-                    lab[k] = gr < G ? my_l[par * PSTRIDE + K + wi] : 0;
-                }
-            }
-            par ^= 1;
         }
-      }
+        if (lane >= 32 - KL) {
+#pragma unroll
+            for (int k = 0; k < C; ++k) {
+                const int wi = lane * C + k - (32 * C - K);
+                m[k] = gr < G ? my_m[par * PSTRIDE + K + wi] : dinf();
+                lab[k] = gr < G ? my_l[par * PSTRIDE + K + wi] : 0;
+            }
+        }
+        par ^= 1;
+    };
+
+    static_assert(LBLK % K == 0 && K % D == 0, "K-blocks tile label blocks; the ring tiles K-blocks");
+    const int nkb = (H - 1) / K;  // full K-row blocks
+    for (int q = 0; q < nkb; ++q) {
+        const int i0 = 1 + q * K;
+        const int lpos = (q * K) % LBLK, blk = (q * K) / LBLK;
+        if (lpos == 0) reset_labels();
+#pragma unroll
+        for (int t = 0; t < K; ++t) step(ring[t % D], i0 + t);
+        // K divides LBLK, so label blocks end only on a K-block's last row
+        if (lpos + K == LBLK || i0 + K - 1 == H - 1) block_end(i0 + K - 1, blk);
+        if (i0 + K < H) exchange();
+    }
+    {  // tail: the last (H-1) % K rows
+        const int i0 = 1 + nkb * K;
+        if (i0 < H) {
+            const int lpos = (nkb * K) % LBLK, blk = (nkb * K) / LBLK;
+            if (lpos == 0) reset_labels();
+#pragma unroll
+            for (int t = 0; t < K; ++t) {
+                if (i0 + t >= H) break;
+                step(ring[t % D], i0 + t);
+            }
+            block_end(H - 1, blk);  // the tail always ends the image (and its label block)
+        }
     }
 
     // ---- K3a: argmin of the bottom row over useful columns (solvers.hpp:94-99)
@@ -321,24 +332,25 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
         int c = bi;
         seam[H - 1] = c;
         for (int b = nblk - 1; b >= 0; --b) {
-            cb[b] = c;
             const int owner = (c / S) / NWARP;
             const int8_t* lb = cluster.map_shared_rank(labels, owner);
             c += lb[b * SM::COLS + (c - owner * SM::COLS)];
             if (b > 0) seam[LBLK * b] = c;  // row 32b = last row of block b-1
         }
         if (nblk > 0) seam[0] = c;
+        __threadfence();
     }
+    // after this barrier no CTA touches another CTA's shared memory, so CTAs
+    // may finish phase 2 and exit independently
     if (ncl > 1) cluster.sync();
     else __syncthreads();
 
     // ---- K3b phase 2: every warp recomputes blocks g, g+G, ... in a 128-column window
     {
-        const int* cb0 = cluster.map_shared_rank(cb, 0);
         uint8_t* dirs = p2 + size_t(warp) * LBLK * P2_COLS;
         for (int b = g; b < nblk && !(p.dbg & 1); b += G) {
-            const int c1 = cb0[b];
             const int r0 = 1 + LBLK * b, r1 = min(LBLK * (b + 1), H - 1);
+            const int c1 = __ldcg(seam + r1);  // phase 1 left the block's bottom column in global memory
             const int wbase = (c1 - P2_COLS / 2) & ~1;  // even: 16-byte aligned double2 loads
             const int wc0 = wbase + lane * 4;
             double mm[4];
@@ -350,12 +362,12 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
                 ll4[k] = 0;
             }
             double en[4];
-            load_row<4>(e + (long long)r0 * p.epitch, wc0, W, en);
+            load_row<4>(e + (long long)r0 * p.epitch, wc0, en);
             for (int r = r0; r <= r1; ++r) {
                 double ec[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) ec[k] = en[k];
-                if (r + 1 <= r1) load_row<4>(e + (long long)(r + 1) * p.epitch, wc0, W, en);
+                if (r + 1 <= r1) load_row<4>(e + (long long)(r + 1) * p.epitch, wc0, en);
                 const double lm = __shfl_up_sync(FULL, mm[3], 1);
                 const double rm = __shfl_down_sync(FULL, mm[0], 1);
                 double pm = lane == 0 ? dinf() : lm;
