@@ -8,7 +8,7 @@ NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -fmad=false -Xcompiler -fPIC -Xptxas
 PKG := paper_2410_21207_b200
 LIB := $(PKG)/libcarve_cuda.so
 SRC := $(PKG)/csrc/carve_cuda.cu
-HDR := $(PKG)/csrc/carve_kernels.cuh include/carve_cuda.h
+HDR := $(wildcard $(PKG)/csrc/*.cuh) include/carve_cuda.h
 
 all: $(LIB) oracle tools
 

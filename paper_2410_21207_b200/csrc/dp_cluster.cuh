@@ -76,7 +76,7 @@ struct Dp2Smem {
     __host__ __device__ static size_t labels_bytes(int nblk) { return (size_t(nblk) * COLS + 15) & ~size_t(15); }
     static constexpr size_t mail_bytes = size_t(2) * NWARP * 2 * K * (8 + 4);
     static constexpr size_t p2_bytes = size_t(NWARP) * LBLK * P2_COLS;
-    static constexpr size_t red_bytes = 64 * 16;
+    static constexpr size_t red_bytes = 64 * 16 + NWARP * 2 * 8;  // argmin scratch + halo mbarriers
     __host__ __device__ static size_t total(int nblk) { return labels_bytes(nblk) + mail_bytes + p2_bytes + red_bytes; }
 };
 
@@ -104,6 +104,39 @@ __device__ __forceinline__ void load_row(const double* __restrict__ row, int col
         v[k] = x.x;
         v[k + 1] = x.y;
     }
+}
+
+// ---- DSMEM point-to-point halo transport (st.async + mbarrier complete_tx) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t a, uint32_t tx) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(tx) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t a, uint32_t phase) {
+    uint32_t ok;
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(a), "r"(phase)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void st_async_b64(uint32_t raddr, double v, uint32_t rmbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+                 "l"(__double_as_longlong(v)), "r"(rmbar)
+                 : "memory");
+}
+__device__ __forceinline__ void st_async_b32(uint32_t raddr, uint32_t v, uint32_t rmbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(raddr), "r"(v),
+                 "r"(rmbar)
+                 : "memory");
 }
 
 __device__ __forceinline__ void argmin_combine(double& v, int& i, double ov, int oi) {
@@ -138,6 +171,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     uint8_t* p2 = reinterpret_cast<uint8_t*>(mail_l + 2 * NWARP * 2 * K);
     double* red_v = reinterpret_cast<double*>(p2 + SM::p2_bytes);
     int* red_i = reinterpret_cast<int*>(red_v + 32);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(red_v + 64);  // [NWARP][2 parities]: my halos have landed
 
     if (p.stamps && cta == 0 && threadIdx.x == 0) p.stamps[img * p.st_istride + 0] = globaltimer();
 
@@ -164,23 +198,36 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
             if (useful >> k & 1) { p.m_out[col0 + k] = m[k]; p.b_out[col0 + k] = col0 + k; }
     }
 
-    // mailbox pointers of my neighbours (possibly in other CTAs of the cluster)
+    // Halo mailboxes. My left neighbour's right-halo slot (side 1) and my right
+    // neighbour's left-halo slot (side 0), as shared::cluster addresses (the
+    // neighbour may live in another CTA), plus their "landed" mbarriers.
     const int gl = g - 1, gr = g + 1;
-    double* nb_left_m = nullptr;  // left neighbour's right-halo slot (side 1)
-    int* nb_left_l = nullptr;
-    double* nb_right_m = nullptr; // right neighbour's left-halo slot (side 0)
-    int* nb_right_l = nullptr;
+    constexpr int PSTRIDE = NWARP * 2 * K;  // elements per parity
+    uint32_t nl_m = 0, nl_l = 0, nl_b = 0, nr_m = 0, nr_l = 0, nr_b = 0;
     if (gl >= 0) {
-        nb_left_m = cluster.map_shared_rank(mail_m, gl / NWARP) + ((gl % NWARP) * 2 + 1) * K;
-        nb_left_l = cluster.map_shared_rank(mail_l, gl / NWARP) + ((gl % NWARP) * 2 + 1) * K;
+        const uint32_t rk = uint32_t(gl / NWARP), w = uint32_t(gl % NWARP);
+        nl_m = mapa_u32(smem_u32(mail_m + (w * 2 + 1) * K), rk);
+        nl_l = mapa_u32(smem_u32(mail_l + (w * 2 + 1) * K), rk);
+        nl_b = mapa_u32(smem_u32(mbar + w * 2), rk);
     }
     if (gr < G) {
-        nb_right_m = cluster.map_shared_rank(mail_m, gr / NWARP) + ((gr % NWARP) * 2 + 0) * K;
-        nb_right_l = cluster.map_shared_rank(mail_l, gr / NWARP) + ((gr % NWARP) * 2 + 0) * K;
+        const uint32_t rk = uint32_t(gr / NWARP), w = uint32_t(gr % NWARP);
+        nr_m = mapa_u32(smem_u32(mail_m + (w * 2 + 0) * K), rk);
+        nr_l = mapa_u32(smem_u32(mail_l + (w * 2 + 0) * K), rk);
+        nr_b = mapa_u32(smem_u32(mbar + w * 2), rk);
     }
-    const double* my_m = mail_m + (warp * 2) * K;  // + side*K, + parity*(NWARP*2*K)
+    const double* my_m = mail_m + (warp * 2) * K;  // + side*K, + parity*PSTRIDE
     const int* my_l = mail_l + (warp * 2) * K;
-    constexpr int PSTRIDE = NWARP * 2 * K;
+    const uint32_t my_b = smem_u32(mbar + warp * 2);  // + parity*8
+    const uint32_t halo_tx = uint32_t(((gl >= 0) + (gr < G)) * K * (8 + 4));
+    if (lane == 0) {
+        mbar_init(my_b, 1);
+        mbar_init(my_b + 8, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // every mbarrier of the cluster is initialised before any halo is sent
+    if (ncl > 1) cluster.sync();
+    else __syncthreads();
 
     // Forward pass. Rows 1..H-1 run in K-row blocks, each fully unrolled so
     // the ring slot, the halo exchange point and the loop control are
@@ -242,22 +289,29 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
         for (int k = 0; k < C; ++k) lab[k] = col0 + k;
     };
     int par = 0;
+    uint32_t phases = 0;  // bit p: phase parity of my mbarrier for mailbox parity p
     auto exchange = [&]() {
-        // send my K leftmost / rightmost useful columns to the neighbours' halos
+        // send my K leftmost / rightmost useful columns straight into the
+        // neighbours' halo mailboxes; each store completes bytes on the
+        // neighbour's mbarrier (no cluster-wide barrier, no memory fence)
+        const uint32_t mo = uint32_t(par * PSTRIDE);
 #pragma unroll
         for (int k = 0; k < C; ++k) {
             const int wi = lane * C + k;
-            if (wi >= K && wi < 2 * K && nb_left_m) {
-                nb_left_m[par * PSTRIDE + wi - K] = m[k];
-                nb_left_l[par * PSTRIDE + wi - K] = lab[k];
+            if (wi >= K && wi < 2 * K && gl >= 0) {
+                st_async_b64(nl_m + (mo + wi - K) * 8, m[k], nl_b + par * 8);
+                st_async_b32(nl_l + (mo + wi - K) * 4, uint32_t(lab[k]), nl_b + par * 8);
             }
-            if (wi >= 32 * C - 2 * K && wi < 32 * C - K && nb_right_m) {
-                nb_right_m[par * PSTRIDE + wi - (32 * C - 2 * K)] = m[k];
-                nb_right_l[par * PSTRIDE + wi - (32 * C - 2 * K)] = lab[k];
+            if (wi >= 32 * C - 2 * K && wi < 32 * C - K && gr < G) {
+                st_async_b64(nr_m + (mo + wi - (32 * C - 2 * K)) * 8, m[k], nr_b + par * 8);
+                st_async_b32(nr_l + (mo + wi - (32 * C - 2 * K)) * 4, uint32_t(lab[k]), nr_b + par * 8);
             }
         }
-        if (ncl > 1) cluster.sync();
-        else __syncthreads();
+        // wait until both neighbours' halos for this parity have landed here
+        if (lane == 0) mbar_arrive_expect_tx(my_b + par * 8, halo_tx);
+        while (!mbar_try_wait(my_b + par * 8, (phases >> par) & 1)) {
+        }
+        phases ^= 1u << par;
         if (lane < KL) {
 #pragma unroll
             for (int k = 0; k < C; ++k) {
