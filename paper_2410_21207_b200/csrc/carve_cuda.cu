@@ -288,7 +288,7 @@ struct Dp2Variant {
     int C, K, NW, D;
     const void* fn;        // hot kernel (no tables)
     const void* fn_tables; // parity-API kernel (writes the full cost / predecessor tables)
-    size_t (*smem)(int nblk);
+    size_t (*smem)(int nblk, int D);
     int S() const { return 32 * C - 2 * K; }
     int cols() const { return NW * S(); }
 };
@@ -351,7 +351,7 @@ Dp2Plan dp2_plan(int W, int H) {
             if (forced >= 0 && k != forced) continue;
             const Dp2Variant& v = kDp2Variants[k];
             const int ncl = (W + v.cols() - 1) / v.cols();
-            const size_t smem = v.smem(nblk);
+            const size_t smem = v.smem(nblk, v.D);
             if (ncl > (pass == 0 ? max_ncl : 16) || smem > size_t(kDpSmemBudget)) continue;
             // columns read past the image edge must stay inside the +inf pad
             if (ncl * v.cols() - W + v.K + 32 * v.C > EPAD_R) continue;

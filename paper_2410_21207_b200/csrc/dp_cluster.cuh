@@ -77,7 +77,10 @@ struct Dp2Smem {
     static constexpr size_t mail_bytes = size_t(2) * NWARP * 2 * K * (8 + 4);
     static constexpr size_t p2_bytes = size_t(NWARP) * LBLK * P2_COLS;
     static constexpr size_t red_bytes = 64 * 16 + NWARP * 2 * 8;  // argmin scratch + halo mbarriers
-    __host__ __device__ static size_t total(int nblk) { return labels_bytes(nblk) + mail_bytes + p2_bytes + red_bytes; }
+    static constexpr size_t ring_bytes(int D) { return size_t(NWARP) * D * 32 * C * 8; }
+    __host__ __device__ static size_t total(int nblk, int D) {
+        return labels_bytes(nblk) + mail_bytes + p2_bytes + red_bytes + ring_bytes(D);
+    }
 };
 
 // the 9-instruction cell update shared by the forward pass and phase 2
@@ -122,7 +125,7 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t a, uint32_t tx) {
 __device__ __forceinline__ bool mbar_try_wait(uint32_t a, uint32_t phase) {
     uint32_t ok;
     asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
         : "=r"(ok)
         : "r"(a), "r"(phase)
         : "memory");
@@ -138,6 +141,14 @@ __device__ __forceinline__ void st_async_b32(uint32_t raddr, uint32_t v, uint32_
                  "r"(rmbar)
                  : "memory");
 }
+
+// ---- energy-row ring: per-lane cp.async (LDGSTS) into shared memory ----------
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ void argmin_combine(double& v, int& i, double ov, int oi) {
     if (ov < v || (ov == v && oi < i)) { v = ov; i = oi; }
@@ -172,6 +183,9 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     double* red_v = reinterpret_cast<double*>(p2 + SM::p2_bytes);
     int* red_i = reinterpret_cast<int*>(red_v + 32);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(red_v + 64);  // [NWARP][2 parities]: my halos have landed
+    double* ring_s = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(red_v) + SM::red_bytes);
+    // this lane's C doubles of stage u: ring_s[((warp * D + u) * 32 + lane) * C]
+    const uint32_t ring_lane = smem_u32(ring_s + (size_t(warp) * D * 32 + lane) * C);
 
     if (p.stamps && cta == 0 && threadIdx.x == 0) p.stamps[img * p.st_istride + 0] = globaltimer();
 
@@ -233,15 +247,29 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     // the ring slot, the halo exchange point and the loop control are
     // compile-time; energy rows i+1..i+D are in flight while row i computes
     // (slot (i-1) % D is consumed, then refilled with row i+D).
-    double ring[D][C];
-    const double* nrow = e + p.epitch;  // next row to load (rows past H-1 are the plane's spare rows)
+    const double* nrow = e + p.epitch + col0;
+    static_assert(C % 2 == 0, "cp.async moves 16-byte pairs of doubles");  // my slice of the next row to fetch (spare rows past H-1 are harmless)
+    auto fetch = [&](int u) {  // this lane's C energies of row `nrow` -> ring stage u, one commit group per row
 #pragma unroll
-    for (int u = 0; u < D; ++u) {
-        load_row<C>(nrow, col0, ring[u]);
+        for (int k = 0; k < C; k += 2) cp_async16(ring_lane + uint32_t(u * 32 * C * 8 + k * 8), nrow + k);
+        cp_async_commit();
         nrow += p.epitch;
-    }
+    };
+#pragma unroll
+    for (int u = 0; u < D; ++u) fetch(u);
 
-    auto step = [&](double (&ev)[C], int i) {
+    auto step = [&](int u, int i) {
+        cp_async_wait<D - 1>();  // row i (the oldest of the D groups in flight) has landed
+        double ev[C];
+        {
+            const double* src = ring_s + ((size_t(warp) * D + u) * 32 + lane) * C;
+#pragma unroll
+            for (int k = 0; k < C; k += 2) {
+                const double2 x = *reinterpret_cast<const double2*>(src + k);
+                ev[k] = x.x;
+                ev[k + 1] = x.y;
+            }
+        }
         const double lm = __shfl_up_sync(FULL, m[C - 1], 1);
         const int ll = __shfl_up_sync(FULL, lab[C - 1], 1);
         const double rm = __shfl_down_sync(FULL, m[0], 1);
@@ -270,9 +298,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
                 }
         }
         (void)dbits;
-        // refill this slot with row i + D
-        load_row<C>(nrow, col0, ev);
-        nrow += p.epitch;
+        fetch(u);  // refill this stage with row i + D (own lane's bytes only: no cross-lane hazard)
     };
     auto block_end = [&](int i, int blk) {  // last row of a label block: labels to smem, M to global
 #pragma unroll
@@ -338,7 +364,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
         const int lpos = (q * K) % LBLK, blk = (q * K) / LBLK;
         if (lpos == 0) reset_labels();
 #pragma unroll
-        for (int t = 0; t < K; ++t) step(ring[t % D], i0 + t);
+        for (int t = 0; t < K; ++t) step(t % D, i0 + t);
         // K divides LBLK, so label blocks end only on a K-block's last row
         if (lpos + K == LBLK || i0 + K - 1 == H - 1) block_end(i0 + K - 1, blk);
         if (i0 + K < H) exchange();
@@ -351,7 +377,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
 #pragma unroll
             for (int t = 0; t < K; ++t) {
                 if (i0 + t >= H) break;
-                step(ring[t % D], i0 + t);
+                step(t % D, i0 + t);
             }
             block_end(H - 1, blk);  // the tail always ends the image (and its label block)
         }
