@@ -387,9 +387,9 @@ void launch_dp2(Ctx& c, const Dp2Plan& pl, Dp2Params p, int nimg, cudaStream_t s
 }
 
 void launch_compact(const CompactParams& p, int nimg, cudaStream_t s) {
-    const int wpb = 8;
-    dim3 grid((p.H + wpb - 1) / wpb, nimg);
-    k_compact<<<grid, wpb * 32, 0, s>>>(p);
+    const int per_cta = CP_THREADS * CP_CHUNK;
+    dim3 grid((p.W - 1 + per_cta - 1) / per_cta, p.H, nimg);
+    k_compact<<<grid, CP_THREADS, 0, s>>>(p);
     LAUNCHED("k_compact");
 }
 

@@ -576,33 +576,67 @@ struct CompactParams {
     long long p_istride, e_istride, s_istride, st_istride;
 };
 
-__global__ void __launch_bounds__(256) k_compact(CompactParams p) {
-    const int img = blockIdx.y;
-    const uint32_t* rgb_in = p.rgb_in + img * p.p_istride;
-    uint32_t* rgb_out = p.rgb_out + img * p.p_istride;
-    const int* seam = p.seam + img * p.s_istride;
-    const int lane = threadIdx.x & 31;
-    const int wpb = blockDim.x >> 5;
-    if (p.stamps && blockIdx.x == 0 && threadIdx.x == 0) p.stamps[img * p.st_istride + 0] = globaltimer();
-    for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < p.H; i += gridDim.x * wpb) {
+// One thread per 4-pixel output chunk: 128-bit RGBX load + the next pixel,
+// two 128-bit energy loads + the next energy, 128-bit stores. Every thread is
+// independent, so a row is served by many warps with all loads in flight
+// (the earlier one-warp-per-row loop was latency-bound at ~0.25 IPC).
+constexpr int CP_CHUNK = 4, CP_THREADS = 256;
+
+__global__ void __launch_bounds__(CP_THREADS) k_compact(CompactParams p) {
+    const int img = blockIdx.z;
+    const int i = blockIdx.y;
+    const uint32_t* __restrict__ rgb_in = p.rgb_in + img * p.p_istride;
+    uint32_t* __restrict__ rgb_out = p.rgb_out + img * p.p_istride;
+    const int* __restrict__ seam = p.seam + img * p.s_istride;
+    if (p.stamps && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+        atomicCAS(&p.stamps[img * p.st_istride + 0], 0ull, (unsigned long long)globaltimer());
+    const int W = p.W, Wn = W - 1;
+    const int base = (blockIdx.x * CP_THREADS + threadIdx.x) * CP_CHUNK;
+    if (base < Wn) {
         const int s = __ldg(seam + i);
-        const long long ro = (long long)i * p.pitch;
-        compact_row<uint32_t>(rgb_in + ro, rgb_out + ro, p.W, s, lane, nullptr, 0, 0, nullptr, 0, false);
+        // RGBX plane
+        {
+            const uint32_t* in = rgb_in + (long long)i * p.pitch;
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(in + base));
+            const uint32_t a[5] = {v.x, v.y, v.z, v.w, base + 4 < W ? __ldg(in + base + 4) : 0u};
+            uint32_t o[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) o[u] = (base + u >= s) ? a[u + 1] : a[u];
+            uint32_t* out = rgb_out + (long long)i * p.pitch;
+            if (base + 4 <= Wn) *reinterpret_cast<uint4*>(out + base) = make_uint4(o[0], o[1], o[2], o[3]);
+            else
+                for (int u = 0; u < 4 && base + u < Wn; ++u) out[base + u] = o[u];
+        }
         if (p.e_in) {
             const long long eo = img * p.e_istride + (long long)i * p.epitch;
-            compact_row<double>(p.e_in + eo, p.e_out + eo, p.W, s, lane, rgb_in, p.pitch, p.H, seam, i, true);
+            const double* in = p.e_in + eo;
+            const double2 v0 = __ldg(reinterpret_cast<const double2*>(in + base));
+            const double2 v1 = __ldg(reinterpret_cast<const double2*>(in + base + 2));
+            const double a[5] = {v0.x, v0.y, v1.x, v1.y, base + 4 < W ? __ldg(in + base + 4) : 0.0};
+            double o[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int x = base + u;
+                o[u] = (x >= s) ? a[u + 1] : a[u];
+                // K1 fix-up: the two new-grid columns whose stencil changed
+                if ((x == s - 1 || x == s) && x < Wn) o[u] = fixup_energy(rgb_in, p.pitch, Wn, p.H, seam, i, x);
+            }
+            double* out = p.e_out + eo;
+            if (base + 4 <= Wn) {
+                *reinterpret_cast<double2*>(out + base) = make_double2(o[0], o[1]);
+                *reinterpret_cast<double2*>(out + base + 2) = make_double2(o[2], o[3]);
+            } else {
+                for (int u = 0; u < 4 && base + u < Wn; ++u) out[base + u] = o[u];
+            }
             // the vacated column joins the +inf pad; so does the column this plane
             // last held live (planes alternate, so it may still be stale)
-            if (lane == 0) {
-                p.e_out[eo + p.W - 1] = dinf();
-                p.e_out[eo + p.W] = dinf();
+            if (base + 4 >= Wn) {
+                out[Wn] = dinf();
+                out[W] = dinf();
             }
         }
     }
-    if (p.stamps && threadIdx.x == 0) {
-        // last block to finish stamps the end (monotonic max)
-        atomicMax(&p.stamps[img * p.st_istride + 1], (unsigned long long)globaltimer());
-    }
+    if (p.stamps && threadIdx.x == 0) atomicMax(&p.stamps[img * p.st_istride + 1], (unsigned long long)globaltimer());
 }
 
 }  // namespace carve_dev
