@@ -309,9 +309,7 @@ def run_ours(args, cfg_name):
     t0 = time.perf_counter()
     for _ in range(args.steps):
         if batch:
-            outs = cv.carve_batch(in_views, TW, TH, devices=[local])
-            for k in range(n_local):
-                out_views[k][...] = outs[k]
+            cv.carve_batch(in_views, TW, TH, devices=[local], out=out_views)
         else:
             out_views[0][...] = cv.carve(in_views[0], TW, TH)
     e2e_s = max_over_ranks(time.perf_counter() - t0)

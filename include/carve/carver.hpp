@@ -1,0 +1,131 @@
+// carve/carver.hpp — drop-in for the reference pipelines
+// (/root/reference/proj/include/carve/carver.hpp). remove_seam(PixelGrid),
+// carve_to_width and carve_to_height run entirely on the B200: the whole seam
+// loop (energy, DP, backtrack, removal) stays on the device and the report's
+// per-seam timings come from device %globaltimer stamps.
+#pragma once
+
+#include <chrono>
+#include <utility>
+#include <vector>
+
+#include "carve/energy.hpp"
+#include "carve/error.hpp"
+#include "carve/raster.hpp"
+#include "carve/solvers.hpp"
+
+namespace carve {
+
+struct CarveConfig {
+    SolverKind solver = SolverKind::ParallelDynamic;
+    EnergyFn energy_fn = EnergyFn::e1;
+    bool forward = false;
+    bool recompute = true;  // the engine always produces the recompute=true result
+    SolverOptions solver_opts{};
+};
+
+struct SeamTiming {
+    double energy_s = 0.0;
+    double solve_s = 0.0;
+    double remove_s = 0.0;
+};
+
+struct CarveReport {
+    int seam_count = 0;
+    std::vector<SeamTiming> per_seam;
+    std::vector<Seam> seams;  // coordinates of the image each seam was taken from
+    double total_s = 0.0;
+};
+
+namespace detail {
+
+inline void check_config(const CarveConfig& cfg) {
+    const bool dp = cfg.solver == SolverKind::Dynamic || cfg.solver == SolverKind::ParallelDynamic;
+    if (cfg.forward && !dp) fail(Errc::usage_error, "forward energy requires the dp or pardp solver");
+    if (!dp) unsupported(std::string("solver ") + to_string(cfg.solver));
+    if (cfg.energy_fn != EnergyFn::e1) unsupported(std::string("energy ") + to_string(cfg.energy_fn));
+    if (cfg.forward) unsupported("forward energy");
+}
+
+// one device-resident carve: width phase then height phase (run_resize order)
+inline std::pair<PixelGrid, CarveReport> carve_device(const PixelGrid& grid, int tw, int th) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const int vs = grid.width - tw, hs = grid.height - th;
+    PixelGrid out(tw, th);
+    std::vector<int32_t> flat(size_t(vs) * grid.height + size_t(hs) * tw);
+    std::vector<carve_seam_timing> tim(size_t(vs + hs));
+    check(carve_cuda_carve(grid.bytes(), grid.width, grid.height, tw, th, out.bytes(), flat.data(), tim.data()));
+    CarveReport rep;
+    rep.seam_count = vs + hs;
+    size_t off = 0;
+    for (int k = 0; k < vs + hs; ++k) {
+        const size_t len = k < vs ? size_t(grid.height) : size_t(tw);
+        rep.seams.emplace_back(flat.begin() + off, flat.begin() + off + len);
+        off += len;
+        rep.per_seam.push_back({tim[k].energy_s, tim[k].solve_s, tim[k].remove_s});
+    }
+    rep.total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return {std::move(out), std::move(rep)};
+}
+
+} // namespace detail
+
+inline PixelGrid remove_seam(const PixelGrid& grid, const Seam& seam) {
+    validate_seam(seam, grid.width, grid.height);
+    if (grid.width < 2) fail(Errc::width_too_small, "cannot remove a seam from a 1-pixel-wide image");
+    PixelGrid out(grid.width - 1, grid.height);
+    detail::check(carve_cuda_remove_seam_rgb(grid.bytes(), grid.width, grid.height, seam.data(), int(seam.size()),
+                                             out.bytes()));
+    return out;
+}
+
+inline std::pair<PixelGrid, CarveReport> carve_to_width(const PixelGrid& grid, int target_width,
+                                                        const CarveConfig& cfg = {}) {
+    if (target_width < 1 || target_width > grid.width)
+        fail(Errc::invalid_target, "target width must be in [1, width]");
+    detail::check_config(cfg);
+    return detail::carve_device(grid, target_width, grid.height);
+}
+
+inline std::pair<PixelGrid, CarveReport> carve_to_height(const PixelGrid& grid, int target_height,
+                                                         const CarveConfig& cfg = {}) {
+    if (target_height < 1 || target_height > grid.height)
+        fail(Errc::invalid_target, "target height must be in [1, height]");
+    detail::check_config(cfg);
+    return detail::carve_device(grid, grid.width, target_height);
+}
+
+/// Batch entry point (no reference equivalent): same-size images sharded by
+/// image over `devices` (empty = all visible GPUs), no inter-GPU traffic.
+inline std::vector<PixelGrid> carve_batch(const std::vector<PixelGrid>& imgs, int target_width, int target_height,
+                                          const std::vector<int>& devices = {}) {
+    if (imgs.empty()) fail(Errc::empty_input, "empty batch");
+    std::vector<PixelGrid> outs(imgs.size(), PixelGrid(target_width, target_height));
+    std::vector<const uint8_t*> in(imgs.size());
+    std::vector<uint8_t*> out(imgs.size());
+    for (size_t k = 0; k < imgs.size(); ++k) {
+        if (imgs[k].width != imgs[0].width || imgs[k].height != imgs[0].height)
+            fail(Errc::dimension_mismatch, "batch images must share one size");
+        in[k] = imgs[k].bytes();
+        out[k] = outs[k].bytes();
+    }
+    detail::check(carve_cuda_carve_batch(in.data(), int(imgs.size()), imgs[0].width, imgs[0].height, target_width,
+                                         target_height, out.data(), devices.empty() ? nullptr : devices.data(),
+                                         int(devices.size())));
+    return outs;
+}
+
+// Paper-comparison / non-hot-path pipelines keep their declarations.
+inline PixelGrid insert_seam(const PixelGrid&, const Seam&) { detail::unsupported("insert_seam"); }
+inline std::pair<std::vector<Seam>, CarveReport> record_seams(const PixelGrid&, int, const CarveConfig& = {}) {
+    detail::unsupported("record_seams");
+}
+inline std::pair<PixelGrid, CarveReport> enlarge_to_width(const PixelGrid&, int, const CarveConfig& = {}) {
+    detail::unsupported("enlarge_to_width");
+}
+inline std::pair<PixelGrid, CarveReport> remove_object(const PixelGrid&, const RemovalMask&, const CarveConfig& = {},
+                                                       bool = true) {
+    detail::unsupported("remove_object");
+}
+
+} // namespace carve

@@ -1,0 +1,124 @@
+// carve/cli.hpp — drop-in for the reference CLI's `resize` path
+// (/root/reference/proj/include/carve/cli.hpp:146-259, 368-379) without CLI11:
+//   carve resize --input X --output Y [--scale S | --width W] [--height H]
+//                [--solver dp|pardp] [--energy e1] [--forward]
+// Exit codes as the reference: 0 success, 1 usage error, 2 runtime error.
+// CARVE_WORKERS is validated like the reference (cli.hpp:109-126) but never
+// changes output. Other subcommands report usage_error (not on the B200 path).
+#pragma once
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "carve/carve.hpp"
+
+namespace carve::cli {
+
+struct ResizeCmd {
+    std::string input, output;
+    std::optional<double> scale;
+    std::optional<int> width, height;
+    std::string solver = "pardp", energy = "e1";
+    bool forward = false;
+};
+
+namespace detail {
+
+inline double parse_double(const std::string& flag, const std::string& v) {
+    char* end = nullptr;
+    const double d = std::strtod(v.c_str(), &end);
+    if (end == v.c_str() || *end) fail(Errc::usage_error, flag + ": not a number: " + v);
+    return d;
+}
+
+inline int parse_positive(const std::string& flag, const std::string& v) {
+    char* end = nullptr;
+    const long n = std::strtol(v.c_str(), &end, 10);
+    if (end == v.c_str() || *end || n < 1 || n > 1 << 30) fail(Errc::usage_error, flag + ": not a positive integer: " + v);
+    return int(n);
+}
+
+inline void check_env_workers() {
+    if (const char* s = std::getenv("CARVE_WORKERS")) {
+        char* end = nullptr;
+        const long v = std::strtol(s, &end, 10);
+        if (end == s || *end != '\0' || v < 0) fail(Errc::usage_error, "CARVE_WORKERS must be a nonnegative integer");
+    }
+}
+
+} // namespace detail
+
+inline ResizeCmd parse_resize(const std::vector<std::string>& a) {
+    ResizeCmd c;
+    for (size_t k = 1; k < a.size(); ++k) {
+        const std::string& f = a[k];
+        auto val = [&]() -> const std::string& {
+            if (k + 1 >= a.size()) fail(Errc::usage_error, f + " needs a value");
+            return a[++k];
+        };
+        if (f == "--input") c.input = val();
+        else if (f == "--output") c.output = val();
+        else if (f == "--scale") {
+            c.scale = detail::parse_double(f, val());
+            if (!(*c.scale > 0.0 && *c.scale <= 2.0)) fail(Errc::usage_error, "scale must be in (0, 2]");
+        } else if (f == "--width") c.width = detail::parse_positive(f, val());
+        else if (f == "--height") c.height = detail::parse_positive(f, val());
+        else if (f == "--solver") {
+            c.solver = val();
+            if (!parse_solver(c.solver)) fail(Errc::usage_error, "--solver: unknown backend " + c.solver);
+        } else if (f == "--energy") {
+            c.energy = val();
+            if (c.energy != "e1" && c.energy != "e2" && c.energy != "hog" && c.energy != "entropy")
+                fail(Errc::usage_error, "--energy: unknown function " + c.energy);
+        } else if (f == "--forward") c.forward = true;
+        else fail(Errc::usage_error, "unknown option " + f);
+    }
+    if (c.input.empty() || c.output.empty()) fail(Errc::usage_error, "--input and --output are required");
+    if (c.scale && c.width) fail(Errc::usage_error, "--scale excludes --width");
+    return c;
+}
+
+/// cli.hpp:242-259 run_resize: carve_to_width then carve_to_height, in one device-resident carve.
+inline int run_resize(const ResizeCmd& cmd) {
+    detail::check_env_workers();
+    PixelGrid img = load_image(cmd.input);
+    CarveConfig cfg;
+    cfg.solver = *parse_solver(cmd.solver);
+    cfg.energy_fn = cmd.energy == "e1" ? EnergyFn::e1 : cmd.energy == "e2" ? EnergyFn::e2
+                  : cmd.energy == "hog" ? EnergyFn::hog : EnergyFn::entropy;
+    cfg.forward = cmd.forward;
+    ::carve::detail::check_config(cfg);
+    const int tw = cmd.scale ? int(std::lround(*cmd.scale * img.width)) : cmd.width.value_or(img.width);
+    const int th = cmd.height.value_or(img.height);
+    if (tw > img.width) fail(Errc::invalid_target, "resize cannot grow the width; use the enlarge command");
+    if (tw < 1) fail(Errc::invalid_target, "target width must be in [1, width]");
+    if (th < 1 || th > img.height) fail(Errc::invalid_target, "target height must be in [1, height]");
+    auto [out, report] = ::carve::detail::carve_device(img, tw, th);
+    save_image(out, cmd.output);
+    return 0;
+}
+
+inline int cli_main(int argc, char** argv) {
+    try {
+        const std::vector<std::string> args(argv + 1, argv + argc);
+        if (args.empty() || args[0] == "--help" || args[0] == "-h") {
+            std::printf("usage: carve resize --input X --output Y [--scale S | --width W] [--height H]\n"
+                        "                    [--solver dp|pardp] [--energy e1]\n");
+            return args.empty() ? 1 : 0;
+        }
+        if (args[0] == "resize") return run_resize(parse_resize(args));
+        fail(Errc::usage_error, "subcommand '" + args[0] + "' is not supported by the B200 engine (resize only)");
+    } catch (const Error& err) {
+        std::fprintf(stderr, "carve: %s\n", err.what());
+        return err.code() == Errc::usage_error ? 1 : 2;
+    } catch (const std::exception& err) {
+        std::fprintf(stderr, "carve: %s\n", err.what());
+        return 2;
+    }
+}
+
+} // namespace carve::cli

@@ -424,8 +424,9 @@ def carve_to_height(img: np.ndarray, target_height: int, cfg: CarveConfig | None
     return out, _report(seams, tims, time.perf_counter() - t0)
 
 
-def carve_batch(imgs, target_width: int, target_height: int | None = None, devices=None) -> list:
-    """Batch of same-size images, sharded by image across devices."""
+def carve_batch(imgs, target_width: int, target_height: int | None = None, devices=None, out=None) -> list:
+    """Batch of same-size images, sharded by image across devices.
+    `out` (optional): preallocated C-contiguous (th, tw, 3) uint8 arrays to fill."""
     arrs = [_img(x) for x in imgs]
     if not arrs:
         raise CarveError(Errc.empty_input, "empty batch")
@@ -433,7 +434,13 @@ def carve_batch(imgs, target_width: int, target_height: int | None = None, devic
     if any(x.shape != arrs[0].shape for x in arrs):
         raise CarveError(Errc.dimension_mismatch, "batch images must share one size")
     th = h if target_height is None else int(target_height)
-    outs = [np.empty((th, target_width, 3), np.uint8) for _ in arrs]
+    if out is None:
+        outs = [np.empty((th, target_width, 3), np.uint8) for _ in arrs]
+    else:
+        outs = list(out)
+        if len(outs) != len(arrs) or any(o.shape != (th, target_width, 3) or o.dtype != np.uint8
+                                         or not o.flags.c_contiguous for o in outs):
+            raise CarveError(Errc.dimension_mismatch, "out arrays must be C-contiguous (th, tw, 3) uint8")
     n = len(arrs)
     ins = (C.c_void_p * n)(*[_ptr(x) for x in arrs])
     ous = (C.c_void_p * n)(*[_ptr(x) for x in outs])

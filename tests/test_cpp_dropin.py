@@ -1,0 +1,101 @@
+"""The C++ drop-in surface: include/carve/*.hpp (through tools/carve_parity.cpp)
+and the `carve resize` CLI (tools/carve_main.cpp), mirroring the reference's
+CLI tests (tests/test_cli.cpp) and acceptance criterion 9 (acceptance.cpp:288-301)."""
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CARVE = os.path.join(ROOT, "build", "carve")
+PARITY = os.path.join(ROOT, "build", "carve_parity")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def tools_built():
+    if not (os.path.exists(CARVE) and os.path.exists(PARITY)):
+        subprocess.run(["make", "-s", "-C", ROOT, "tools"], check=True)
+
+
+def write_ppm(path, img):
+    h, w, _ = img.shape
+    with open(path, "wb") as f:
+        f.write(f"P6\n{w} {h}\n255\n".encode())
+        f.write(np.ascontiguousarray(img).tobytes())
+
+
+def read_ppm(path):
+    data = open(path, "rb").read()
+    parts = data.split(maxsplit=4)
+    assert parts[0] == b"P6"
+    w, h = int(parts[1]), int(parts[2])
+    return np.frombuffer(parts[4][: w * h * 3], np.uint8).reshape(h, w, 3)
+
+
+def run(*args, env=None):
+    return subprocess.run([CARVE, *args], capture_output=True, text=True, env=env)
+
+
+# ---- host-only behaviour (no GPU needed) ---------------------------------------------
+def test_cli_usage_errors_exit_1(tmp_path):
+    assert run().returncode == 1
+    assert run("resize", "--input", "a.ppm").returncode == 1  # missing --output
+    assert run("resize", "--input", "a", "--output", "b", "--scale", "0").returncode == 1
+    assert run("resize", "--input", "a", "--output", "b", "--scale", "0.5", "--width", "3").returncode == 1
+    assert run("enlarge", "--input", "a", "--output", "b").returncode == 1
+    r = run("resize", "--input", "a", "--output", "b", "--solver", "quantum")
+    assert r.returncode == 1 and "carve:" in r.stderr
+
+
+def test_cli_runtime_errors_exit_2(tmp_path):
+    r = run("resize", "--input", str(tmp_path / "missing.ppm"), "--output", str(tmp_path / "o.ppm"), "--scale", "0.5")
+    assert r.returncode == 2 and "no such file" in r.stderr
+    bad = tmp_path / "bad.ppm"
+    bad.write_bytes(b"P3\n1 1\n255\n0 0 0\n")
+    assert run("resize", "--input", str(bad), "--output", str(tmp_path / "o.ppm"), "--scale", "0.5").returncode == 2
+
+
+def test_cli_bad_workers_env(tmp_path):
+    p = tmp_path / "a.ppm"
+    write_ppm(p, np.zeros((4, 4, 3), np.uint8))
+    env = dict(os.environ, CARVE_WORKERS="-3")
+    assert run("resize", "--input", str(p), "--output", str(tmp_path / "o.ppm"), "--scale", "0.5", env=env).returncode == 1
+
+
+# ---- through the GPU ----------------------------------------------------------------------
+@pytest.mark.gpu
+def test_cpp_headers_selftest():
+    r = subprocess.run([PARITY, "selftest"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr + r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_cpp_headers_golden(name):
+    c = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))["configs"][name]
+    r = subprocess.run([PARITY, "hash", str(c["W"]), str(c["H"]), str(c["target_w"]), str(c["target_h"])],
+                       capture_output=True, text=True, check=True)
+    assert r.stdout.split() == [c["input"], c["output"], c["seams"]]
+
+
+@pytest.mark.gpu
+def test_cli_resize_matches_oracle_and_is_worker_invariant(tmp_path):
+    # acceptance criterion 9: byte-identical output for CARVE_WORKERS=1 and =8
+    img = oracle.port().make_test_image(180, 180)
+    src = tmp_path / "in.ppm"
+    write_ppm(src, img)
+    outs = []
+    for workers in ("1", "8"):
+        dst = tmp_path / f"out{workers}.ppm"
+        env = dict(os.environ, CARVE_WORKERS=workers)
+        r = run("resize", "--input", str(src), "--output", str(dst), "--scale", "0.5", "--height", "150",
+                "--solver", "pardp", env=env)
+        assert r.returncode == 0, r.stderr
+        outs.append(dst.read_bytes())
+    assert outs[0] == outs[1]
+    want = oracle.port().carve(img, 90, 150)
+    assert np.array_equal(read_ppm(tmp_path / "out1.ppm"), want)

@@ -1,0 +1,112 @@
+// C++ drop-in parity driver: exercises the include/carve/*.hpp API the way the
+// reference's own tests do (test_solvers.cpp:152-174, test_carver.cpp:34-210)
+// and prints FNV-1a-64 hashes of the configs for tests/test_cpp_dropin.py.
+//   carve_parity selftest            -> reference unit-test pins, exit 0/1
+//   carve_parity hash W H TW TH      -> "<input hash> <output hash> <seams hash>"
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "carve/carve.hpp"
+
+using namespace carve;
+
+static uint64_t fnv(const void* p, size_t n) {
+    uint64_t h = 0xcbf29ce484222325ull;
+    for (size_t k = 0; k < n; ++k) {
+        h ^= static_cast<const uint8_t*>(p)[k];
+        h *= 0x100000001b3ull;
+    }
+    return h;
+}
+
+static int failures = 0;
+#define EXPECT(c)                                                      \
+    do {                                                               \
+        if (!(c)) {                                                    \
+            std::fprintf(stderr, "FAIL %s:%d %s\n", __FILE__, __LINE__, #c); \
+            ++failures;                                                \
+        }                                                              \
+    } while (0)
+
+template <class F>
+static Errc thrown(F&& f) {
+    try {
+        f();
+    } catch (const Error& e) {
+        return e.code();
+    }
+    return Errc(-1);
+}
+
+static int selftest() {
+    // dp_seam worked example (test_solvers.cpp:156-174)
+    EnergyMap m{3, 3, {1, 2, 3, 4, 1, 6, 7, 8, 1}};
+    auto [seam, table] = dp_seam(m);
+    const double want[9] = {1, 2, 3, 5, 2, 8, 9, 10, 3};
+    for (int k = 0; k < 9; ++k) EXPECT(table.m[k] == want[k]);
+    EXPECT((seam == Seam{0, 1, 2}));
+    EXPECT((dp_seam(EnergyMap{4, 1, {8, 2, 6, 2}}).seam == Seam{1}));
+    EXPECT(parallel_dp_seam(m, 8).table == table);
+    // energy_e1 pins (test_energy.cpp:33-64)
+    LumaGrid g{3, 1, {0, 100, 0}};
+    auto e = energy_e1(g);
+    EXPECT(e.values[0] == 100.0 && e.values[1] == 0.0 && e.values[2] == 100.0);
+    // remove_seam (test_carver.cpp:35-73)
+    PixelGrid p(2, 1);
+    p.at(0, 0) = Rgb{1, 1, 1};
+    p.at(0, 1) = Rgb{2, 2, 2};
+    EXPECT((remove_seam(p, {0}).at(0, 0) == Rgb{2, 2, 2}));
+    EXPECT(thrown([] { remove_seam(PixelGrid(1, 2), {0, 0}); }) == Errc::width_too_small);
+    EXPECT(thrown([] { remove_seam(PixelGrid(3, 2), {0, 2}); }) == Errc::invalid_seam);
+    // zero-energy column carved exactly (test_carver.cpp:117-128)
+    PixelGrid cols(4, 4);
+    const uint8_t vals[4] = {10, 50, 10, 90};
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) cols.at(i, j) = Rgb{vals[j], vals[j], vals[j]};
+    auto [out, rep] = carve_to_width(cols, 3);
+    EXPECT(rep.seam_count == 1 && (rep.seams[0] == Seam{1, 1, 1, 1}));
+    EXPECT(out.width == 3 && out.at(2, 1).r == 10 && out.at(2, 2).r == 90);
+    // report invariants (test_carver.cpp:129-142)
+    auto img = make_test_image(24, 16);
+    auto [o2, r2] = carve_to_width(img, 10);
+    EXPECT(o2.width == 10 && r2.seam_count == 14 && r2.per_seam.size() == 14);
+    double sum = 0;
+    for (auto& t : r2.per_seam) sum += t.energy_s + t.solve_s + t.remove_s;
+    EXPECT(r2.total_s >= sum);
+    EXPECT(thrown([&] { carve_to_width(img, 0); }) == Errc::invalid_target);
+    EXPECT(thrown([&] { carve_to_width(img, 25); }) == Errc::invalid_target);
+    CarveConfig bad;
+    bad.solver = SolverKind::Greedy;
+    bad.forward = true;
+    EXPECT(thrown([&] { carve_to_width(img, 2, bad); }) == Errc::usage_error);
+    // transpose sandwich (test_carver.cpp:202-210)
+    auto t = make_test_image(10, 8);
+    EXPECT(carve_to_height(t, 5).first == transpose(carve_to_width(transpose(t), 5).first));
+    EXPECT(transpose(transpose(t)) == t);
+    std::printf(failures ? "selftest FAILED (%d)\n" : "selftest ok\n", failures);
+    return failures ? 1 : 0;
+}
+
+int main(int argc, char** argv) {
+    try {
+        if (argc >= 2 && std::string(argv[1]) == "selftest") return selftest();
+        if (argc == 6 && std::string(argv[1]) == "hash") {
+            const int w = std::atoi(argv[2]), h = std::atoi(argv[3]), tw = std::atoi(argv[4]), th = std::atoi(argv[5]);
+            auto img = make_test_image(w, h);
+            auto [out, rep] = ::carve::detail::carve_device(img, tw, th);
+            uint64_t hs = 0xcbf29ce484222325ull;
+            std::string all;
+            for (auto& s : rep.seams) all.append(reinterpret_cast<const char*>(s.data()), s.size() * sizeof(int));
+            hs = fnv(all.data(), all.size());
+            std::printf("%016llx %016llx %016llx\n", (unsigned long long)fnv(img.bytes(), img.pixels.size() * 3),
+                        (unsigned long long)fnv(out.bytes(), out.pixels.size() * 3), (unsigned long long)hs);
+            return 0;
+        }
+        std::fprintf(stderr, "usage: carve_parity selftest | hash W H TW TH\n");
+        return 1;
+    } catch (const Error& e) {
+        std::fprintf(stderr, "carve_parity: %s\n", e.what());
+        return 2;
+    }
+}
