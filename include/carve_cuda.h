@@ -103,6 +103,9 @@ carve_status carve_cuda_transpose_rgb(const uint8_t* rgb, int w, int h, uint8_t*
  * when non-NULL; seam_out receives h column indices, top row first.
  * Bit-identical for every input and independent of any worker count. */
 carve_status carve_cuda_dp_seam(const double* e, int w, int h, double* m_out, int32_t* b_out, int32_t* seam_out);
+/* Tools: run the DP once on e with per-warp clock64 phase counters
+ * ([warp][8]: forward, halo wait, argmin+phase1, phase2, H). */
+carve_status carve_cuda_dp_profile(const double* e, int w, int h, long long* counters, int ncounters, int* warps);
 /* replaces validate_seam (solvers.hpp:69-78); pure host check */
 carve_status carve_cuda_validate_seam(const int32_t* seam, int n, int w, int h);
 

@@ -288,6 +288,7 @@ struct Dp2Variant {
     int C, K, NW, D;
     const void* fn;        // hot kernel (no tables)
     const void* fn_tables; // parity-API kernel (writes the full cost / predecessor tables)
+    const void* fn_prof;   // hot kernel + clock64 phase counters (tools)
     size_t (*smem)(int nblk, int D);
     int S() const { return 32 * C - 2 * K; }
     int cols() const { return NW * S(); }
@@ -295,28 +296,36 @@ struct Dp2Variant {
 
 template <int C, int K, int NW, int D>
 constexpr Dp2Variant dp2_variant() {
-    return Dp2Variant{C, K, NW, D, (const void*)k_dp2<C, K, NW, D, false>, (const void*)k_dp2<C, K, NW, D, true>,
-                      &Dp2Smem<C, K, NW>::total};
+    return Dp2Variant{C, K, NW, D, (const void*)k_dp2<C, K, NW, D, 0>, (const void*)k_dp2<C, K, NW, D, 1>,
+                      (const void*)k_dp2<C, K, NW, D, 2>, &Dp2Smem<C, K, NW>::total};
 }
 
 // preference order: the first variant whose cluster fits (<= 8 CTAs, then <= 16) wins
 const Dp2Variant kDp2Variants[] = {
-    dp2_variant<4, 16, 4, 8>(),   // 0: S=96,  384 cols/CTA
-    dp2_variant<8, 16, 4, 4>(),   // 1: S=224, 896 cols/CTA
-    dp2_variant<8, 16, 8, 4>(),   // 2: S=224, 1792 cols/CTA
-    dp2_variant<4, 8, 4, 8>(),    // 3: S=112, 448 cols/CTA
-    dp2_variant<8, 32, 4, 4>(),   // 4: S=192, 768 cols/CTA
-    dp2_variant<4, 16, 8, 8>(),   // 5: S=96,  768 cols/CTA
-    dp2_variant<2, 8, 8, 8>(),    // 6: S=48,  384 cols/CTA
-    dp2_variant<2, 8, 16, 8>(),   // 7: S=48,  768 cols/CTA
-    dp2_variant<2, 16, 8, 8>(),   // 8: S=32,  256 cols/CTA
-    dp2_variant<4, 32, 4, 8>(),   // 9: S=64,  256 cols/CTA
+    dp2_variant<2, 16, 8, 8>(),   // 0: S=32,  256 cols/CTA
+    dp2_variant<4, 32, 4, 8>(),   // 1: S=64,  256 cols/CTA
+    dp2_variant<4, 16, 4, 8>(),   // 2: S=96,  384 cols/CTA
+    dp2_variant<2, 8, 8, 8>(),    // 3: S=48,  384 cols/CTA
+    dp2_variant<4, 16, 8, 8>(),   // 4: S=96,  768 cols/CTA
+    dp2_variant<2, 8, 16, 8>(),   // 5: S=48,  768 cols/CTA
+    dp2_variant<8, 16, 4, 4>(),   // 6: S=224, 896 cols/CTA
+    dp2_variant<2, 16, 4, 8>(),   // 7: S=32,  128 cols/CTA (1 warp per scheduler)
+    dp2_variant<2, 8, 4, 8>(),    // 8: S=48,  192 cols/CTA (1 warp per scheduler)
+    dp2_variant<4, 16, 2, 8>(),   // 9: S=96,  192 cols/CTA
+    dp2_variant<4, 8, 4, 8>(),    // 10: S=112, 448 cols/CTA
+    dp2_variant<8, 32, 4, 4>(),   // 11: S=192, 768 cols/CTA
+    dp2_variant<2, 16, 4, 16>(),  // 12: as 7, 16-row ring
+    dp2_variant<2, 16, 8, 16>(),  // 13: as 0, 16-row ring
+    dp2_variant<4, 16, 4, 16>(),  // 14: as 2, 16-row ring
+    dp2_variant<4, 32, 4, 16>(),  // 15: as 1, 16-row ring
+    dp2_variant<2, 16, 16, 16>(), // 16: S=32,  512 cols/CTA (wide rows, 4 warps per scheduler)
+    dp2_variant<4, 16, 8, 16>(),  // 17: as 4, 16-row ring
 };
 constexpr int kNumDp2Variants = int(sizeof(kDp2Variants) / sizeof(kDp2Variants[0]));
 
 void init_kernel_attributes(Ctx& c) {
     for (const Dp2Variant& v : kDp2Variants)
-        for (const void* fn : {v.fn, v.fn_tables}) {
+        for (const void* fn : {v.fn, v.fn_tables, v.fn_prof}) {
             ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kDpSmemBudget),
                "cudaFuncSetAttribute(dp2 smem)");
             ck(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
@@ -342,12 +351,16 @@ int env_int(const char* name, int dflt) {
     return s && *s ? std::atoi(s) : dflt;
 }
 
+// Preference order (measured on B200, tools/sweep_dp.py): the first variant
+// whose cluster fits wins. Narrow rows favour one C=2 warp per scheduler.
+const int kDp2Order[] = {12, 13, 0, 16, 17, 4, 14, 5, 2, 7, 15, 1, 3, 8, 9, 10, 6, 11};
+
 Dp2Plan dp2_plan(int W, int H) {
     const int nblk = H > 1 ? (H - 1 + LBLK - 1) / LBLK : 0;
     const int forced = env_int("CARVE_DP_VARIANT", -1);
-    const int max_ncl = env_int("CARVE_DP_MAX_NCL", 8);
+    const int max_ncl = env_int("CARVE_DP_MAX_NCL", 16);
     for (int pass = 0; pass < 2; ++pass) {
-        for (int k = 0; k < kNumDp2Variants; ++k) {
+        for (int k : kDp2Order) {
             if (forced >= 0 && k != forced) continue;
             const Dp2Variant& v = kDp2Variants[k];
             const int ncl = (W + v.cols() - 1) / v.cols();
@@ -367,7 +380,7 @@ void launch_dp2(Ctx& c, const Dp2Plan& pl, Dp2Params p, int nimg, cudaStream_t s
     p.G = pl.ncl * v.NW;
     p.nblk = pl.nblk;
     p.dbg = env_int("CARVE_DP_DBG", 0);
-    const void* fn = p.m_out ? v.fn_tables : v.fn;
+    const void* fn = p.m_out ? v.fn_tables : (p.prof ? v.fn_prof : v.fn);
     if (c.smem_set.find(fn) == c.smem_set.end()) fail(CARVE_E_CUDA, "DP kernel attributes not initialised");
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(nimg * pl.ncl));
@@ -816,6 +829,39 @@ carve_status carve_cuda_dp_seam(const double* e, int w, int h, double* m_out, in
             ck(cudaMemcpyAsync(b_out, db, size_t(w) * h * 4, cudaMemcpyDeviceToHost, c.stream), "D2H b");
         }
         sync(c);
+    });
+}
+
+carve_status carve_cuda_dp_profile(const double* e, int w, int h, long long* counters, int ncounters, int* warps) {
+    return guarded([&] {
+        if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "image is empty");
+        Ctx& c = ctx();
+        const Dp2Plan pl = dp2_plan(w, h);
+        const int pitch = int(round_up(w, 32));
+        const int epitch = padded_epitch(w);
+        double* de = static_cast<double*>(c.e[0].ensure(size_t(epitch) * (h + EPAD_B) * 8)) + EPAD_L;
+        double* mb = static_cast<double*>(c.mbound.ensure(size_t(pl.nblk + 1) * pitch * 8));
+        int* dseam = static_cast<int*>(c.seams.ensure(size_t(h) * 4));
+        const int G = pl.ncl * pl.v->NW;
+        long long* dprof = static_cast<long long*>(c.scratch_a.ensure(size_t(G) * 8 * 8));
+        ck(cudaMemcpy2DAsync(de, size_t(epitch) * 8, e, size_t(w) * 8, size_t(w) * 8, h, cudaMemcpyHostToDevice,
+                             c.stream),
+           "H2D energy");
+        launch_fill_pads(de, epitch, w, h, 1, 0, c.stream);
+        Dp2Params p{};
+        p.e = de;
+        p.epitch = epitch;
+        p.W = w;
+        p.H = h;
+        p.mbound = mb;
+        p.mpitch = pitch;
+        p.seam = dseam;
+        p.prof = dprof;
+        launch_dp2(c, pl, p, 1, c.stream);
+        ck(cudaMemcpyAsync(counters, dprof, size_t(std::min(ncounters, G * 8)) * 8, cudaMemcpyDeviceToHost, c.stream),
+           "D2H prof");
+        sync(c);
+        *warps = G;
     });
 }
 

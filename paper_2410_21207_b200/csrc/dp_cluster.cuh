@@ -66,6 +66,7 @@ struct Dp2Params {
     unsigned long long* stamps;  // optional [start, end]
     long long e_istride, mb_istride, s_istride, st_istride;
     int dbg;           // debugging: bit0 skips phase 2, bit1 skips phase 1, bit2 skips the walk
+    long long* prof;   // MODE 2 only: [G][8] per-warp clock64 counters
 };
 
 // smem layout (dynamic): labels int8 [nblk][NWARP*S] | mailbox | phase-2 dirs | reduce
@@ -99,6 +100,22 @@ __device__ __forceinline__ void dp_cell(double L, double M, double R, int lL, in
 // C consecutive energies starting at col0 (even): unconditional aligned
 // 128-bit loads — the padded plane (EPAD_L/EPAD_R, +inf) covers every column a
 // warp or a phase-2 window can touch.
+// Same result and tie-break as dp_cell, but the left candidate (the one that
+// arrives last, by shuffle, for a lane's first column) is combined last:
+// t = argmin(M, R) with M winning ties, then L wins if L <= t. The scan order
+// L, M, R with strict < selects exactly this cell, so the seam is unchanged,
+// while only one compare-select sits between the shuffle and the add.
+__device__ __forceinline__ void dp_cell_left_last(double L, double M, double R, int lL, int lM, int lR, double e,
+                                                  double& out, int& lab, int& d) {
+    double t = M;
+    int tl = lM, td = 1;
+    if (R < t) { t = R; tl = lR; td = 2; }
+    const bool left = L <= t;
+    out = __dadd_rn(e, left ? L : t);
+    lab = left ? lL : tl;
+    d = left ? 0 : td;
+}
+
 template <int C>
 __device__ __forceinline__ void load_row(const double* __restrict__ row, int col0, double (&v)[C]) {
 #pragma unroll
@@ -154,8 +171,14 @@ __device__ __forceinline__ void argmin_combine(double& v, int& i, double ov, int
     if (ov < v || (ov == v && oi < i)) { v = ov; i = oi; }
 }
 
-template <int C, int K, int NWARP, int D, bool TABLES>
+// MODE 0: hot kernel; 1: also writes the full cost/predecessor tables (parity
+// API); 2: hot kernel + per-warp clock64 phase counters into p.prof (tools only)
+template <int C, int K, int NWARP, int D, int MODE>
 __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
+    constexpr bool TABLES = MODE == 1;
+    constexpr bool PROF = MODE == 2;
+    long long pf_t0 = 0, pf_wait = 0;
+    if constexpr (PROF) pf_t0 = clock64();
     static_assert(K % C == 0 && (32 * C) > 2 * K, "halo must be whole lanes and leave useful columns");
     using SM = Dp2Smem<C, K, NWARP>;
     constexpr int S = SM::S;
@@ -284,7 +307,8 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
             const double nm = (k + 1 < C) ? m[k + 1] : rm;
             const int nl = (k + 1 < C) ? lab[k + 1] : rl;
             int d;
-            dp_cell(pm, cm, nm, pl, cl, nl, ev[k], m[k], lab[k], d);
+            if (k == 0) dp_cell_left_last(pm, cm, nm, pl, cl, nl, ev[k], m[k], lab[k], d);
+            else dp_cell(pm, cm, nm, pl, cl, nl, ev[k], m[k], lab[k], d);
             dbits |= uint32_t(d) << (2 * k);
             pm = cm;
             pl = cl;
@@ -335,8 +359,11 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
         }
         // wait until both neighbours' halos for this parity have landed here
         if (lane == 0) mbar_arrive_expect_tx(my_b + par * 8, halo_tx);
+        long long w0 = 0;
+        if constexpr (PROF) w0 = clock64();
         while (!mbar_try_wait(my_b + par * 8, (phases >> par) & 1)) {
         }
+        if constexpr (PROF) pf_wait += clock64() - w0;
         phases ^= 1u << par;
         if (lane < KL) {
 #pragma unroll
@@ -383,6 +410,9 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
         }
     }
 
+    cp_async_wait<0>();  // the ring's trailing prefetches (rows past H-1) land before the region is reused
+    long long pf_fwd = 0;
+    if constexpr (PROF) pf_fwd = clock64();
     // ---- K3a: argmin of the bottom row over useful columns (solvers.hpp:94-99)
     double bv = dinf();
     int bi = 0x7fffffff;
@@ -425,29 +455,49 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     if (ncl > 1) cluster.sync();
     else __syncthreads();
 
+    long long pf_p1 = 0;
+    if constexpr (PROF) pf_p1 = clock64();
     // ---- K3b phase 2: every warp recomputes blocks g, g+G, ... in a 128-column window
     {
         uint8_t* dirs = p2 + size_t(warp) * LBLK * P2_COLS;
+        // phase-2 ring: this warp's forward-ring region, P2D rows of 128 doubles
+        constexpr int P2D = (D * C) / 4;
+        static_assert(P2D >= 2, "phase-2 ring needs at least two stages");
+        const double* p2ring_ptr = ring_s + size_t(warp) * D * 32 * C + lane * 4;
+        const uint32_t p2ring = smem_u32(p2ring_ptr);
         for (int b = g; b < nblk && !(p.dbg & 1); b += G) {
             const int r0 = 1 + LBLK * b, r1 = min(LBLK * (b + 1), H - 1);
             const int c1 = __ldcg(seam + r1);  // phase 1 left the block's bottom column in global memory
             const int wbase = (c1 - P2_COLS / 2) & ~1;  // even: 16-byte aligned double2 loads
             const int wc0 = wbase + lane * 4;
             double mm[4];
-            int ll4[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int j = wc0 + k;
                 mm[k] = (j >= 0 && j < W) ? mbound[(long long)b * p.mpitch + j] : dinf();
-                ll4[k] = 0;
             }
-            double en[4];
-            load_row<4>(e + (long long)r0 * p.epitch, wc0, en);
-            for (int r = r0; r <= r1; ++r) {
-                double ec[4];
+            // the block's energy rows stream through this warp's (now idle) forward ring,
+            // P2D rows in flight via cp.async
+            auto p2fetch = [&](int r, int slot) {
+                const double* src = e + (long long)min(r, r1) * p.epitch + wc0;
+                const uint32_t dst = p2ring + uint32_t(slot * P2_COLS * 8);
+                cp_async16(dst, src);
+                cp_async16(dst + 16, src + 2);
+                cp_async_commit();
+            };
 #pragma unroll
-                for (int k = 0; k < 4; ++k) ec[k] = en[k];
-                if (r + 1 <= r1) load_row<4>(e + (long long)(r + 1) * p.epitch, wc0, en);
+            for (int u = 0; u < P2D; ++u) p2fetch(r0 + u, u);
+            for (int r = r0; r <= r1; ++r) {
+                const int slot = (r - r0) % P2D;
+                cp_async_wait<P2D - 1>();
+                double ec[4];
+                {
+                    const double* src = p2ring_ptr + slot * P2_COLS;
+                    const double2 x0 = *reinterpret_cast<const double2*>(src);
+                    const double2 x1 = *reinterpret_cast<const double2*>(src + 2);
+                    ec[0] = x0.x; ec[1] = x0.y; ec[2] = x1.x; ec[3] = x1.y;
+                }
+                p2fetch(r + P2D, slot);
                 const double lm = __shfl_up_sync(FULL, mm[3], 1);
                 const double rm = __shfl_down_sync(FULL, mm[0], 1);
                 double pm = lane == 0 ? dinf() : lm;
@@ -462,10 +512,9 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
                     db |= uint32_t(d) << (8 * k);
                     pm = cm;
                 }
-                DP2_ALIGN(dirs + (r - r0) * P2_COLS + 4 * lane, 4, "dirs");
                 reinterpret_cast<uint32_t*>(dirs + (r - r0) * P2_COLS)[lane] = db;
-                (void)ll4;
             }
+            cp_async_wait<0>();
             __syncwarp();
             if (lane == 0 && !(p.dbg & 4)) {
                 int c = c1;
@@ -475,6 +524,16 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
                 }
             }
             __syncwarp();
+        }
+    }
+    if constexpr (PROF) {
+        if (lane == 0) {
+            long long* o = p.prof + g * 8;
+            o[0] = pf_fwd - pf_t0;   // forward pass (incl. waits)
+            o[1] = pf_wait;          // of which: waiting for halos
+            o[2] = pf_p1 - pf_fwd;   // argmin + phase 1 + barriers
+            o[3] = clock64() - pf_p1;  // phase 2
+            o[4] = H;
         }
     }
     if (p.stamps) {

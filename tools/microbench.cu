@@ -83,7 +83,7 @@ void run(const char* name, F launch, int n, int per) {
     cudaFree(d);
 }
 
-int main() {
+int main1() {
     double* buf;
     cudaMalloc(&buf, 1 << 20);
     cudaMemset(buf, 0, 1 << 20);
@@ -102,3 +102,94 @@ int main() {
     printf("status %s\n", cudaGetErrorString(e));
     return 0;
 }
+
+// 5) row step + labels (+ optional cp.async ring of D rows), one warp, no exchange
+template <int C, bool LABELS, int D>
+__global__ void k_row2(const double* __restrict__ e, int pitch, double* out, int n, long long* cyc) {
+    __shared__ __align__(16) double ring[D > 0 ? D : 1][32 * C];
+    const int lane = threadIdx.x & 31;
+    double m[C];
+    int lab[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) { m[k] = out[lane * C + k]; lab[k] = lane * C + k; }
+    const double* nrow = e + lane * C;
+    auto fetch = [&](int u) {
+        if constexpr (D > 0) {
+            const uint32_t dst = uint32_t(__cvta_generic_to_shared(&ring[u][lane * C]));
+#pragma unroll
+            for (int k = 0; k < C; k += 2)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + k * 8), "l"(nrow + k) : "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            nrow += pitch;
+        }
+    };
+#pragma unroll
+    for (int u = 0; u < (D > 0 ? D : 1); ++u) fetch(u);
+    uint64_t t0 = clk();
+    for (int i0 = 0; i0 < n; i0 += (D > 0 ? D : 1)) {
+#pragma unroll
+        for (int u = 0; u < (D > 0 ? D : 1); ++u) {
+            double ev[C];
+            if constexpr (D > 0) {
+                asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
+#pragma unroll
+                for (int k = 0; k < C; k += 2) {
+                    const double2 x = *reinterpret_cast<const double2*>(&ring[u][lane * C + k]);
+                    ev[k] = x.x; ev[k + 1] = x.y;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < C; ++k) ev[k] = 1.0;
+            }
+            const double lm = __shfl_up_sync(0xffffffffu, m[C - 1], 1);
+            const double rm = __shfl_down_sync(0xffffffffu, m[0], 1);
+            int ll = 0, rl = 0;
+            if constexpr (LABELS) {
+                ll = __shfl_up_sync(0xffffffffu, lab[C - 1], 1);
+                rl = __shfl_down_sync(0xffffffffu, lab[0], 1);
+            }
+            double pm = lm;
+            int pl = ll;
+#pragma unroll
+            for (int k = 0; k < C; ++k) {
+                const double cm = m[k];
+                const int cl = lab[k];
+                const double nm = (k + 1 < C) ? m[k + 1] : rm;
+                const int nl = (k + 1 < C) ? lab[k + 1] : rl;
+                double best = pm;
+                int bl = pl;
+                if (cm < best) { best = cm; bl = cl; }
+                if (nm < best) { best = nm; bl = nl; }
+                m[k] = __dadd_rn(ev[k], best);
+                if constexpr (LABELS) lab[k] = bl;
+                pm = cm;
+                pl = cl;
+            }
+            fetch(u);
+        }
+    }
+    uint64_t t1 = clk();
+#pragma unroll
+    for (int k = 0; k < C; ++k) out[lane * C + k] = m[k] + lab[k];
+    if (threadIdx.x == 0) cyc[0] = (long long)(t1 - t0);
+}
+
+int main2() {
+    double* buf;
+    cudaMalloc(&buf, 1 << 20);
+    cudaMemset(buf, 0, 1 << 20);
+    double* e;
+    const int rows = 4096 + 64, pitch = 256;
+    cudaMalloc(&e, size_t(rows) * pitch * 8);
+    cudaMemset(e, 0, size_t(rows) * pitch * 8);
+    const int n = 4096;
+    run("row2 C=2 plain", [&](int n, long long* d) { k_row2<2, false, 0><<<1, 32>>>(e, pitch, buf, n, d); }, n, 1);
+    run("row2 C=2 labels", [&](int n, long long* d) { k_row2<2, true, 0><<<1, 32>>>(e, pitch, buf, n, d); }, n, 1);
+    run("row2 C=2 ring8", [&](int n, long long* d) { k_row2<2, false, 8><<<1, 32>>>(e, pitch, buf, n, d); }, n, 1);
+    run("row2 C=2 labels+ring8", [&](int n, long long* d) { k_row2<2, true, 8><<<1, 32>>>(e, pitch, buf, n, d); }, n, 1);
+    run("row2 C=4 plain", [&](int n, long long* d) { k_row2<4, false, 0><<<1, 32>>>(e, pitch, buf, n, d); }, n, 1);
+    run("row2 C=4 labels+ring8", [&](int n, long long* d) { k_row2<4, true, 8><<<1, 32>>>(e, pitch, buf, n, d); }, n, 1);
+    printf("status %s\n", cudaGetErrorString(cudaGetLastError()));
+    return 0;
+}
+int main() { main1(); return main2(); }
