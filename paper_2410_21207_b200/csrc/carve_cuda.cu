@@ -225,63 +225,6 @@ void launch_fill_pads(double* e, int epitch, int W, int H, int nimg, long long e
 int padded_epitch(int w) { return int(round_up(size_t(EPAD_L) + w + EPAD_R, 32)); }
 
 constexpr int kDpSmemBudget = 220 * 1024;
-constexpr int kMaxWinWarps = 16;
-
-struct DpShape {
-    int C, threads, R, nblk, nwin;
-    size_t smem;
-};
-
-DpShape dp_shape(int W, int H) {
-    DpShape d{};
-    const int cands[] = {1, 2, 4, 8, 16};
-    d.C = 0;
-    for (int C : cands) {
-        const int maxt = C >= 8 ? 512 : 1024;
-        if ((W + C - 1) / C <= maxt) {
-            d.C = C;
-            break;
-        }
-    }
-    if (!d.C) fail(CARVE_E_IMAGE_TOO_LARGE, "width " + std::to_string(W) + " exceeds the single-CTA DP limit of 8192");
-    d.threads = int(round_up(std::max(1, (W + d.C - 1) / d.C), 32));
-    const int nw = d.threads / 32;
-    d.nwin = std::min(nw, kMaxWinWarps);
-    const size_t Wl = round_up(W, 8);
-    const size_t win = size_t(d.nwin) * WIN_ROWS * WIN_BYTES;
-    const int rows = H - 1;  // rows carrying a direction
-    if (rows <= 0) {
-        d.R = 1;
-        d.nblk = 0;
-    } else {
-        const size_t budget = kDpSmemBudget - win - 1024;
-        int max_blocks = int(std::max<size_t>(1, budget / (Wl * 2)));
-        int nblk = std::min((rows + 31) / 32, max_blocks);
-        d.R = (rows + nblk - 1) / nblk;
-        d.nblk = (rows + d.R - 1) / d.R;
-    }
-    d.nwin = std::min(d.nwin, std::max(1, d.nblk));
-    d.smem = round_up(size_t(d.nblk) * Wl * 2, 16) + round_up(size_t(d.nblk + 1) * 4, 16) +
-             size_t(d.nwin) * WIN_ROWS * WIN_BYTES;
-    return d;
-}
-
-template <int C, int D>
-void launch_dp_t(Ctx& c, const DpShape& d, const DpParams& p, int nimg, cudaStream_t s) {
-    auto k = k_dp_seam<C, D>;
-    k<<<nimg, d.threads, d.smem, s>>>(p);
-    LAUNCHED("k_dp_seam");
-}
-
-void launch_dp(Ctx& c, const DpShape& d, const DpParams& p, int nimg, cudaStream_t s) {
-    switch (d.C) {
-        case 1: launch_dp_t<1, 4>(c, d, p, nimg, s); break;
-        case 2: launch_dp_t<2, 4>(c, d, p, nimg, s); break;
-        case 4: launch_dp_t<4, 2>(c, d, p, nimg, s); break;
-        case 8: launch_dp_t<8, 2>(c, d, p, nimg, s); break;
-        default: launch_dp_t<16, 1>(c, d, p, nimg, s); break;
-    }
-}
 
 // ---- K2+K3 v2: cluster trapezoid DP (dp_cluster.cuh) ------------------------
 struct Dp2Variant {
@@ -332,12 +275,6 @@ void init_kernel_attributes(Ctx& c) {
                "cudaFuncSetAttribute(dp2 cluster)");
             c.smem_set[fn] = kDpSmemBudget;
         }
-    for (const void* fn : {(const void*)k_dp_seam<1, 4>, (const void*)k_dp_seam<2, 4>, (const void*)k_dp_seam<4, 2>,
-                           (const void*)k_dp_seam<8, 2>, (const void*)k_dp_seam<16, 1>}) {
-        ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kDpSmemBudget),
-           "cudaFuncSetAttribute(dp smem)");
-        c.smem_set[fn] = kDpSmemBudget;
-    }
 }
 
 struct Dp2Plan {
@@ -397,6 +334,21 @@ void launch_dp2(Ctx& c, const Dp2Plan& pl, Dp2Params p, int nimg, cudaStream_t s
     void* args[] = {&p};
     ck(cudaLaunchKernelExC(&cfg, fn, args), "launch k_dp2");
     LAUNCHED("k_dp2");
+}
+
+void launch_compact_inplace(const CompactParams& p, int nimg, cudaStream_t s) {
+    dim3 grid(p.H, nimg);
+    const int W = p.W;
+    if (W <= 4 * 1024) {
+        k_compact_inplace<4><<<grid, int(round_up((W + 3) / 4, 32)), 0, s>>>(p);
+    } else if (W <= 8 * 1024) {
+        k_compact_inplace<8><<<grid, int(round_up((W + 7) / 8, 32)), 0, s>>>(p);
+    } else if (W <= 16 * 1024) {
+        k_compact_inplace<16><<<grid, int(round_up((W + 15) / 16, 32)), 0, s>>>(p);
+    } else {
+        fail(CARVE_E_IMAGE_TOO_LARGE, "width exceeds the in-place removal limit of 16384");
+    }
+    LAUNCHED("k_compact_inplace");
 }
 
 void launch_compact(const CompactParams& p, int nimg, cudaStream_t s) {
@@ -463,106 +415,88 @@ size_t stamp_words(const CarveGeometry& g) { return size_t(g.nseams) * 4 + 4; }
 void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const CarveGeometry& g, int* d_seams,
                size_t seam_istride, unsigned long long* d_stamps, cudaStream_t s) {
     const long long in_is = (long long)g.w * g.h * 3, out_is = (long long)g.tw * g.th * 3;
-    uint32_t* rgb[2] = {c.rgb[0].as<uint32_t>(), c.rgb[1].as<uint32_t>()};
-    double* e[2] = {c.e[0].as<double>() + EPAD_L, c.e[1].as<double>() + EPAD_L};  // logical column 0
+    uint32_t* rgb[2] = {c.rgb[0].as<uint32_t>(), c.rgb[1].as<uint32_t>()};  // [1]: transpose target only
+    double* e = c.e[0].as<double>() + EPAD_L;                                 // logical column 0
     const long long eis = (long long)g.eplane;
-    uint8_t* dir = c.dir.as<uint8_t>();
     const long long pis = (long long)g.plane;
-    const long long dis = (long long)g.dpitch * g.dir_rows;
     const size_t sw = stamp_words(g);
-    const bool dp_v1 = env_int("CARVE_DP", 2) == 1;
     int cur = 0;
     {
         Prof pr(c, s, KK_UNPACK, 7.0 * g.w * g.h * nimg);
         launch_unpack(c, d_in, g.w, g.h, rgb[cur], g.pitch_a, nimg, in_is, pis, s);
     }
 
-    auto phase = [&](int W0, int H, int ntake, int pitch, int epitch, int seam_base, int stamp_seam0, int estamp) {
+    // One orientation's seam loop: K1 once, then per seam the DP (whose
+    // prologue applies the previous removal's 2-column energy fix-up) and the
+    // in-place removal. Nothing returns to the host between seams.
+    auto phase = [&](int W0, int H, int ntake, int pitch, int epitch, int seam_base, int stamp_seam0) {
         if (ntake <= 0) return;
         {
             // algorithmic bytes: 3 B RGB read + 8 B FP64 write per pixel
             Prof pr(c, s, KK_ENERGY, 11.0 * W0 * H * nimg);
-            launch_energy(rgb[cur], pitch, W0, H, e[cur], epitch, nimg, pis, eis, s);
+            launch_energy(rgb[cur], pitch, W0, H, e, epitch, nimg, pis, eis, s);
         }
-        // both ping-pong planes: compaction keeps the right pad growing by one +inf column per seam
-        launch_fill_pads(e[cur], epitch, W0, H, nimg, eis, s);
-        launch_fill_pads(e[cur ^ 1], epitch, W0, H, nimg, eis, s);
-        (void)estamp;
+        launch_fill_pads(e, epitch, W0, H, nimg, eis, s);
         for (int k = 0; k < ntake; ++k) {
             const int W = W0 - k;
             t_dbg_tag = W;
-            DpParams p{};
-            p.seam = d_seams + seam_base + size_t(k) * H;
-            p.stamps = d_stamps ? d_stamps + size_t(stamp_seam0 + k) * 4 : nullptr;
-            if (dp_v1) {
-                const DpShape d = dp_shape(W, H);
-                p.e = e[cur];
-                p.epitch = epitch;
-                p.W = W;
-                p.H = H;
-                p.dir = dir;
-                p.dpitch = g.dpitch;
-                p.R = d.R;
-                p.nblk = d.nblk;
-                p.nwin = d.nwin;
-                p.e_istride = eis;
-                p.d_istride = dis;
-                p.s_istride = (long long)seam_istride;
-                p.st_istride = (long long)sw;
-                // 8 B FP64 energy read + 1 B direction write per cell
-                Prof pr(c, s, KK_DP, 9.0 * W * H * nimg);
-                launch_dp(c, d, p, nimg, s);
-            } else {
+            int* seam = d_seams + seam_base + size_t(k) * H;
+            unsigned long long* st = d_stamps ? d_stamps + size_t(stamp_seam0 + k) * 4 : nullptr;
+            {
                 const Dp2Plan pl = dp2_plan(W, H);
                 Dp2Params q{};
-                q.e = e[cur];
+                q.e = e;
                 q.epitch = epitch;
                 q.W = W;
                 q.H = H;
                 q.mbound = c.mbound.as<double>();
                 q.mpitch = g.mpitch;
-                q.seam = p.seam;
-                q.stamps = p.stamps;
+                q.seam = seam;
+                q.stamps = st;
                 q.e_istride = eis;
                 q.mb_istride = g.mb_istride;
                 q.s_istride = (long long)seam_istride;
                 q.st_istride = (long long)sw;
+                if (k > 0) {  // fix up the energy around the previous seam (removed from width W + 1)
+                    q.prev_seam = seam - H;
+                    q.rgb = rgb[cur];
+                    q.rpitch = pitch;
+                    q.rgb_istride = pis;
+                }
                 // algorithmic: 8 B FP64 energy read per cell (no direction plane)
                 Prof pr(c, s, KK_DP, 8.0 * W * H * nimg);
                 launch_dp2(c, pl, q, nimg, s);
             }
             CompactParams q{};
-            q.rgb_in = rgb[cur];
-            q.rgb_out = rgb[cur ^ 1];
             const bool last = (k + 1 == ntake);
-            q.e_in = last ? nullptr : e[cur];  // the final width needs no energy
-            q.e_out = e[cur ^ 1];
+            q.rgb_in = q.rgb_out = rgb[cur];
+            q.e_in = q.e_out = last ? nullptr : e;  // the final width needs no energy
             q.pitch = pitch;
             q.epitch = epitch;
             q.W = W;
             q.H = H;
-            q.seam = p.seam;
-            q.stamps = d_stamps ? d_stamps + size_t(stamp_seam0 + k) * 4 + 2 : nullptr;
+            q.seam = seam;
+            q.stamps = st ? st + 2 : nullptr;
             q.p_istride = pis;
             q.e_istride = eis;
             q.s_istride = (long long)seam_istride;
             q.st_istride = (long long)sw;
             {
-                // read W, write W-1 per row: 3 B RGB (+ 8 B FP64 energy) per element
+                // algorithmic: read W + write W-1 per row, 3 B RGB (+ 8 B FP64) per
+                // element, although the in-place kernel moves only the part right of the seam
                 Prof pr(c, s, KK_COMPACT, (last ? 3.0 : 11.0) * H * (2.0 * W - 1) * nimg);
-                launch_compact(q, nimg, s);
+                launch_compact_inplace(q, nimg, s);
             }
-            cur ^= 1;
         }
     };
-    phase(g.w, g.h, g.w - g.tw, g.pitch_a, g.epitch_a, 0, 0, 0);
+    phase(g.w, g.h, g.w - g.tw, g.pitch_a, g.epitch_a, 0, 0);
     if (g.th != g.h) {
         {
             Prof pr(c, s, KK_TRANSPOSE, 8.0 * g.tw * g.h * nimg);
             launch_transpose(rgb[cur], g.pitch_a, g.tw, g.h, rgb[cur ^ 1], g.pitch_b, nimg, pis, pis, s);
         }
         cur ^= 1;
-        phase(g.h, g.tw, g.h - g.th, g.pitch_b, g.epitch_b, (g.w - g.tw) * g.h, g.w - g.tw, 2);
+        phase(g.h, g.tw, g.h - g.th, g.pitch_b, g.epitch_b, (g.w - g.tw) * g.h, g.w - g.tw);
         Prof pr(c, s, KK_PACK, 7.0 * g.tw * g.th * nimg);
         launch_pack(c, rgb[cur], g.pitch_b, g.tw, g.th, true, d_out, nimg, pis, out_is, s);
     } else {
@@ -572,11 +506,9 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
 }
 
 void ensure_carve_buffers(Ctx& c, const CarveGeometry& g, int nimg) {
-    for (int k = 0; k < 2; ++k) {
-        c.rgb[k].ensure(g.plane * 4 * nimg);
-        c.e[k].ensure(g.eplane * 8 * nimg);
-    }
-    c.dir.ensure(size_t(g.dpitch) * g.dir_rows * nimg + 256);
+    c.rgb[0].ensure(g.plane * 4 * nimg);
+    if (g.th != g.h) c.rgb[1].ensure(g.plane * 4 * nimg);
+    c.e[0].ensure(g.eplane * 8 * nimg);
     c.mbound.ensure(size_t(g.mb_istride) * 8 * nimg);
 }
 
@@ -945,7 +877,8 @@ carve_status carve_cuda_carve_batch(const uint8_t* const* rgb, int n, int w, int
         const CarveGeometry g = geometry(w, h, target_w, target_h);
         const size_t in_bytes = size_t(w) * h * 3, out_bytes = size_t(target_w) * target_h * 3;
         // per-image device footprint -> chunk size (keep well inside 180 GB HBM)
-        const size_t per_img = g.plane * 24 + size_t(g.dpitch) * g.dir_rows + in_bytes + out_bytes + g.seam_ints * 4;
+        const size_t per_img = g.plane * 8 + g.eplane * 8 + size_t(g.mb_istride) * 8 + in_bytes + out_bytes +
+                               g.seam_ints * 4;
         const int chunk_cap = int(std::max<size_t>(1, (size_t(48) << 30) / per_img));
         std::vector<int> status(ndev, CARVE_OK);
         std::vector<std::string> msgs(ndev);

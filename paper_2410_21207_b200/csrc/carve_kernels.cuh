@@ -1,11 +1,12 @@
 // carve_kernels.cuh — the four sm_100a kernels of the seam-carving hot path.
 //
 //   K1  energy stencil        k_energy_full   (energy.hpp:82-98 + raster.hpp:61-71)
-//       + 2-column fix-up     inside k_compact
-//   K2  cumulative-energy DP  k_dp_seam       (solvers.hpp:116-157, 263-289)
-//   K3  argmin + backtrack    tail of k_dp_seam (solvers.hpp:94-111)
-//   K4  seam removal          k_compact       (carver.hpp:71-98), transposing
-//                             variants for horizontal seams (carver.hpp:216-222)
+//       + 2-column fix-up     prologue of k_dp2
+//   K2  cumulative-energy DP  k_dp2 (dp_cluster.cuh) (solvers.hpp:116-157, 263-289)
+//   K3  argmin + backtrack    tail of k_dp2 (solvers.hpp:94-111)
+//   K4  seam removal          k_compact_inplace (carve loop), k_compact (the
+//                             remove_seam API) (carver.hpp:71-98); transpose
+//                             kernels for horizontal seams (carver.hpp:216-222)
 //
 // Arithmetic contract: every FP64 operation is an
 // explicit round-to-nearest intrinsic (__dmul_rn/__dadd_rn/__dsub_rn) so no
@@ -212,280 +213,6 @@ __global__ void k_luma(const uint32_t* __restrict__ rgb, int pitch, int W, int H
 }
 
 // ---------------------------------------------------------------------------
-// K2 + K3 — cumulative-energy DP, argmin and backtrack for one image per CTA.
-//
-// Thread t owns C consecutive columns [t*C, t*C+C) and keeps the previous
-// row's cumulative cost M in registers. Neighbour values cross lanes with
-// warp shuffles and cross warps through a double-buffered shared-memory edge
-// slot, one __syncthreads per row. Out-of-range neighbours are +inf, which is
-// equivalent to the reference's candidate exclusion because
-// the middle candidate is always finite. The scan order left, mid, right with
-// strict < reproduces fill_row_span's tie-break (solvers.hpp:136-145).
-//
-// Backtrack without a serial H-step chain: rows 1..H-1 are cut into nblk
-// blocks of R rows. Alongside M each cell carries a label = the column at
-// the row above the block from which its optimal path descends (propagated
-// with the same neighbour exchange as M). The label row of each block's last
-// row is kept in shared memory, so the block-boundary columns of the seam
-// follow from nblk shared-memory lookups (phase 1). Each block's rows are
-// then recovered in parallel, one warp per block, from the stored per-cell
-// directions, 32 rows at a time through a 32x80-byte shared-memory window
-// loaded with independent 128-bit loads (phase 2).
-
-struct DpParams {
-    const double* e;
-    int epitch;
-    int W, H;
-    uint8_t* dir;
-    int dpitch;
-    int R, nblk, nwin;
-    int* seam;
-    double* m_out;  // optional full cost table (pitch W)
-    int* b_out;     // optional predecessor table (pitch W)
-    unsigned long long* stamps;  // optional [start, end] per image
-    long long e_istride, d_istride, s_istride, st_istride;
-};
-
-constexpr int WIN_ROWS = 32, WIN_BYTES = 80;
-
-template <int C>
-__device__ __forceinline__ void load_cols(const double* __restrict__ row, int j0, int W, double (&v)[C]) {
-    if (j0 + C <= W) {
-        if constexpr (C == 1) {
-            v[0] = __ldg(row + j0);
-        } else {
-#pragma unroll
-            for (int k = 0; k < C; k += 2) {
-                const double2 x = __ldg(reinterpret_cast<const double2*>(row + j0 + k));
-                v[k] = x.x;
-                v[k + 1] = x.y;
-            }
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < C; ++k) v[k] = (j0 + k < W) ? __ldg(row + j0 + k) : 0.0;
-    }
-}
-
-template <int C>
-__device__ __forceinline__ void store_dirs(uint8_t* p, const uint32_t (&dw)[(C + 3) / 4]) {
-    if constexpr (C == 1) *p = uint8_t(dw[0]);
-    else if constexpr (C == 2) *reinterpret_cast<uint16_t*>(p) = uint16_t(dw[0]);
-    else if constexpr (C == 4) *reinterpret_cast<uint32_t*>(p) = dw[0];
-    else if constexpr (C == 8) *reinterpret_cast<uint2*>(p) = make_uint2(dw[0], dw[1]);
-    else *reinterpret_cast<uint4*>(p) = make_uint4(dw[0], dw[1], dw[2], dw[3]);
-}
-
-// columns per thread -> max threads per CTA (register budget: C >= 8 needs > 64 regs)
-template <int C>
-constexpr int dp_max_threads() { return C >= 8 ? 512 : 1024; }
-
-template <int C, int D>
-__global__ void __launch_bounds__(dp_max_threads<C>(), 1) k_dp_seam(DpParams p) {
-    extern __shared__ __align__(16) unsigned char dsm[];
-    __shared__ double s_em[2][2][32];  // [buf][side: 0 = first col of warp, 1 = last col][warp]
-    __shared__ int s_el[2][2][32];
-    __shared__ double s_rv[32];
-    __shared__ int s_ri[32];
-
-    const int img = blockIdx.x;
-    const double* __restrict__ e = p.e + img * p.e_istride;
-    uint8_t* __restrict__ dir = p.dir + img * p.d_istride;
-    int* __restrict__ seam = p.seam + img * p.s_istride;
-    const int W = p.W, H = p.H, R = p.R, nblk = p.nblk;
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
-    const int j0 = t * C;
-    const int Wl = (W + 7) & ~7;
-    int16_t* labels = reinterpret_cast<int16_t*>(dsm);                          // nblk x Wl
-    int* cb = reinterpret_cast<int*>(dsm + ((size_t(nblk) * Wl * 2 + 15) & ~size_t(15)));  // nblk + 1
-    uint8_t* win = reinterpret_cast<uint8_t*>(cb) + ((size_t(nblk + 1) * 4 + 15) & ~size_t(15));
-
-    if (p.stamps && t == 0) p.stamps[img * p.st_istride + 0] = globaltimer();
-
-    const double INF = dinf();
-    double m[C];
-    int lab[C];
-    {
-        double v[C];
-        load_cols<C>(e, j0, W, v);
-#pragma unroll
-        for (int k = 0; k < C; ++k) {
-            m[k] = (j0 + k < W) ? v[k] : INF;
-            lab[k] = j0 + k;
-        }
-        if (p.m_out) {
-#pragma unroll
-            for (int k = 0; k < C; ++k)
-                if (j0 + k < W) {
-                    p.m_out[j0 + k] = m[k];
-                    p.b_out[j0 + k] = j0 + k;
-                }
-        }
-    }
-
-    // publish row 0's warp-edge values for row 1 (buffer (1-1)&1 = 0)
-    if (lane == 0) { s_em[0][0][warp] = m[0]; s_el[0][0][warp] = lab[0]; }
-    if (lane == 31) { s_em[0][1][warp] = m[C - 1]; s_el[0][1][warp] = lab[C - 1]; }
-    __syncthreads();
-
-    // register ring of D prefetched energy rows
-    double ring[D][C];
-#pragma unroll
-    for (int u = 0; u < D; ++u)
-        if (1 + u < H) load_cols<C>(e + (long long)(1 + u) * p.epitch, j0, W, ring[u]);
-
-    int blk = 0, inblk = 0;  // block of the current row and its offset in the block
-    for (int i0 = 1; i0 < H; i0 += D) {
-#pragma unroll
-        for (int u = 0; u < D; ++u) {
-            const int i = i0 + u;
-            if (i >= H) break;
-            double ecur[C];
-#pragma unroll
-            for (int k = 0; k < C; ++k) ecur[k] = ring[u][k];
-            if (i + D < H) load_cols<C>(e + (long long)(i + D) * p.epitch, j0, W, ring[u]);
-
-            // previous-row neighbours
-            const int pb = (i - 1) & 1;
-            double lm = __shfl_up_sync(FULL, m[C - 1], 1);
-            int ll = __shfl_up_sync(FULL, lab[C - 1], 1);
-            double rm = __shfl_down_sync(FULL, m[0], 1);
-            int rl = __shfl_down_sync(FULL, lab[0], 1);
-            if (lane == 0) {
-                lm = warp > 0 ? s_em[pb][1][warp - 1] : INF;
-                ll = warp > 0 ? s_el[pb][1][warp - 1] : 0;
-            }
-            if (lane == 31) {
-                rm = warp + 1 < nw ? s_em[pb][0][warp + 1] : INF;
-                rl = warp + 1 < nw ? s_el[pb][0][warp + 1] : 0;
-            }
-            if (inblk == 0) {  // block start: labels restart as identity
-                ll = j0 - 1;
-                rl = j0 + C;
-#pragma unroll
-                for (int k = 0; k < C; ++k) lab[k] = j0 + k;
-            }
-
-            uint32_t dw[(C + 3) / 4];
-#pragma unroll
-            for (int q = 0; q < (C + 3) / 4; ++q) dw[q] = 0;
-            double pm = lm;
-            int pl = ll;
-#pragma unroll
-            for (int k = 0; k < C; ++k) {
-                const double cm = m[k];
-                const int cl = lab[k];
-                const double nm = (k + 1 < C) ? m[k + 1] : rm;
-                const int nl = (k + 1 < C) ? lab[k + 1] : rl;
-                // solvers.hpp:136-145: best = left; mid < best; right < best
-                double best = pm;
-                int d = 0, bl = pl;
-                if (cm < best) { best = cm; d = 1; bl = cl; }
-                if (nm < best) { best = nm; d = 2; bl = nl; }
-                m[k] = (j0 + k < W) ? __dadd_rn(ecur[k], best) : INF;  // solvers.hpp:146
-                lab[k] = bl;
-                dw[k >> 2] |= uint32_t(d) << (8 * (k & 3));
-                pm = cm;
-                pl = cl;
-            }
-            if (j0 < W) store_dirs<C>(dir + (long long)i * p.dpitch + j0, dw);
-            if (p.m_out) {
-#pragma unroll
-                for (int k = 0; k < C; ++k)
-                    if (j0 + k < W) {
-                        const int d = int((dw[k >> 2] >> (8 * (k & 3))) & 0xffu);
-                        p.m_out[(long long)i * W + j0 + k] = m[k];
-                        p.b_out[(long long)i * W + j0 + k] = j0 + k + d - 1;
-                    }
-            }
-            if (inblk == R - 1 || i == H - 1) {  // block's last row: keep its labels
-#pragma unroll
-                for (int k = 0; k < C; ++k)
-                    if (j0 + k < W) labels[(size_t)blk * Wl + j0 + k] = int16_t(lab[k] - (j0 + k));
-            }
-            if (++inblk == R) {
-                inblk = 0;
-                ++blk;
-            }
-            const int cbuf = i & 1;
-            if (lane == 0) { s_em[cbuf][0][warp] = m[0]; s_el[cbuf][0][warp] = lab[0]; }
-            if (lane == 31) { s_em[cbuf][1][warp] = m[C - 1]; s_el[cbuf][1][warp] = lab[C - 1]; }
-            __syncthreads();
-        }
-    }
-
-    // K3a: argmin of the bottom row, first index of the minimum (solvers.hpp:94-99)
-    double bv = INF;
-    int bi = 0x7fffffff;
-#pragma unroll
-    for (int k = 0; k < C; ++k)
-        if (j0 + k < W && m[k] < bv) { bv = m[k]; bi = j0 + k; }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(FULL, bv, o);
-        const int oi = __shfl_xor_sync(FULL, bi, o);
-        if (ov < bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-    }
-    if (lane == 0) { s_rv[warp] = bv; s_ri[warp] = bi; }
-    __syncthreads();
-    if (warp == 0) {
-        bv = lane < nw ? s_rv[lane] : INF;
-        bi = lane < nw ? s_ri[lane] : 0x7fffffff;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(FULL, bv, o);
-            const int oi = __shfl_xor_sync(FULL, bi, o);
-            if (ov < bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-        }
-        // K3b phase 1: block-boundary columns through the stored labels
-        if (lane == 0) {
-            int c = bi;
-            seam[H - 1] = c;
-            for (int b = nblk - 1; b >= 0; --b) {
-                cb[b] = c;
-                c += labels[(size_t)b * Wl + c];
-            }
-            if (nblk > 0) seam[0] = c;
-        }
-    }
-    __syncthreads();
-
-    // K3b phase 2: per-block walks, one warp per block, 32-row windows
-    if (warp < p.nwin) {
-        uint8_t* w = win + warp * (WIN_ROWS * WIN_BYTES);
-        for (int b = warp; b < nblk; b += p.nwin) {
-            const int r0 = 1 + b * R, r1 = min(r0 + R - 1, H - 1);
-            int c = cb[b];
-            int i = r1;
-            while (i >= r0) {
-                const int nrows = min(WIN_ROWS, i - r0 + 1);
-                const int base = max(c - 32, 0) & ~15;
-                if (lane < nrows) {
-                    const uint4* src = reinterpret_cast<const uint4*>(dir + (long long)(i - lane) * p.dpitch + base);
-                    uint4* dst = reinterpret_cast<uint4*>(w + lane * WIN_BYTES);
-#pragma unroll
-                    for (int q = 0; q < WIN_BYTES / 16; ++q) dst[q] = src[q];
-                }
-                __syncwarp();
-                if (lane == 0) {
-                    for (int k = 0; k < nrows; ++k) {
-                        c += int(w[k * WIN_BYTES + (c - base)]) - 1;
-                        seam[i - k - 1] = c;
-                    }
-                }
-                c = __shfl_sync(FULL, c, 0);
-                i -= nrows;
-                __syncwarp();
-            }
-        }
-    }
-    if (p.stamps) {
-        __syncthreads();
-        if (t == 0) p.stamps[img * p.st_istride + 1] = globaltimer();
-    }
-}
-
-// ---------------------------------------------------------------------------
 // K4 — seam removal: out[i][j] = in[i][j < s[i] ? j : j+1] (carver.hpp:71-82)
 // for the RGBX plane and the FP64 energy plane, fused with the K1 fix-up of
 // the (at most) two new-grid columns s[i]-1 and s[i] whose stencil changed
@@ -636,6 +363,70 @@ __global__ void __launch_bounds__(CP_THREADS) k_compact(CompactParams p) {
             }
         }
     }
+    if (p.stamps && threadIdx.x == 0) atomicMax(&p.stamps[img * p.st_istride + 1], (unsigned long long)globaltimer());
+}
+
+// K4 in place (the carve loop's removal): one CTA per row; only pixels at or
+// right of the seam move (on average half the row), RGBX and FP64 energy.
+// Every thread loads its shifted source chunk, the CTA synchronises, then the
+// chunks are stored back, so the left shift by one is race-free within the row
+// and rows are independent. The energy fix-up of the two new-grid columns runs
+// in the next DP launch (Dp2Params::prev_seam), once every row is compacted.
+template <int CH>  // pixels per thread
+__global__ void __launch_bounds__(1024) k_compact_inplace(CompactParams p) {
+    const int img = blockIdx.y, i = blockIdx.x;
+    const int W = p.W, Wn = W - 1;
+    const int s = __ldg(p.seam + img * p.s_istride + i);
+    const int base = threadIdx.x * CH;
+    if (p.stamps && i == 0 && threadIdx.x == 0)
+        atomicCAS(&p.stamps[img * p.st_istride + 0], 0ull, (unsigned long long)globaltimer());
+    const bool active = base + CH > s && base < Wn;
+    uint32_t* rgb = p.rgb_out + img * p.p_istride + (long long)i * p.pitch;
+    double* e = p.e_out ? p.e_out + img * p.e_istride + (long long)i * p.epitch : nullptr;
+    uint32_t o[CH];
+    double oe[CH];
+    if (active) {
+        uint32_t a[CH + 1];
+#pragma unroll
+        for (int q = 0; q < CH; q += 4) {
+            const uint4 v = *reinterpret_cast<const uint4*>(rgb + base + q);
+            a[q] = v.x; a[q + 1] = v.y; a[q + 2] = v.z; a[q + 3] = v.w;
+        }
+        a[CH] = base + CH < W ? rgb[base + CH] : 0u;
+#pragma unroll
+        for (int u = 0; u < CH; ++u) o[u] = (base + u >= s) ? a[u + 1] : a[u];
+        if (e) {
+            double b[CH + 1];
+#pragma unroll
+            for (int q = 0; q < CH; q += 2) {
+                const double2 v = *reinterpret_cast<const double2*>(e + base + q);
+                b[q] = v.x; b[q + 1] = v.y;
+            }
+            b[CH] = base + CH < W ? e[base + CH] : 0.0;
+#pragma unroll
+            for (int u = 0; u < CH; ++u) oe[u] = (base + u >= s) ? b[u + 1] : b[u];
+        }
+    }
+    __syncthreads();
+    if (active) {
+        if (base + CH <= Wn) {
+#pragma unroll
+            for (int q = 0; q < CH; q += 4)
+                *reinterpret_cast<uint4*>(rgb + base + q) = make_uint4(o[q], o[q + 1], o[q + 2], o[q + 3]);
+            if (e) {
+#pragma unroll
+                for (int q = 0; q < CH; q += 2) *reinterpret_cast<double2*>(e + base + q) = make_double2(oe[q], oe[q + 1]);
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < CH; ++u)
+                if (base + u < Wn) {
+                    rgb[base + u] = o[u];
+                    if (e) e[base + u] = oe[u];
+                }
+        }
+    }
+    if (e && threadIdx.x == 0) e[Wn] = dinf();  // the vacated column joins the +inf pad
     if (p.stamps && threadIdx.x == 0) atomicMax(&p.stamps[img * p.st_istride + 1], (unsigned long long)globaltimer());
 }
 

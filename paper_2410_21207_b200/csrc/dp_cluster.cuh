@@ -53,7 +53,7 @@ constexpr int LBLK = 32;      // label / M-boundary block height (rows)
 constexpr int P2_COLS = 128;  // phase-2 window: 32 lanes x 4 columns
 
 struct Dp2Params {
-    const double* e;   // energy plane (pitch epitch), image stride e_istride
+    double* e;         // energy plane (pitch epitch), image stride e_istride
     int epitch;
     int W, H;
     int G;             // warps in the cluster (= ncl * NWARP)
@@ -67,6 +67,13 @@ struct Dp2Params {
     long long e_istride, mb_istride, s_istride, st_istride;
     int dbg;           // debugging: bit0 skips phase 2, bit1 skips phase 1, bit2 skips the walk
     long long* prof;   // MODE 2 only: [G][8] per-warp clock64 counters
+    // K1 fix-up for the previous seam (nullable): the removal kernel shifted
+    // the planes in place; the two new-grid columns per row around the
+    // previous seam get their energy recomputed here from the compacted RGBX
+    const int* prev_seam;  // image stride s_istride
+    const uint32_t* rgb;   // RGBX plane (pitch rpitch), image stride rgb_istride
+    int rpitch;
+    long long rgb_istride;
 };
 
 // smem layout (dynamic): labels int8 [nblk][NWARP*S] | mailbox | phase-2 dirs | reduce
@@ -189,7 +196,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     const int cta = int(cluster.block_rank());
     const int img = blockIdx.x / ncl;
 
-    const double* __restrict__ e = p.e + img * p.e_istride;
+    double* __restrict__ e = p.e + img * p.e_istride;
     double* __restrict__ mbound = p.mbound + img * p.mb_istride;
     int* __restrict__ seam = p.seam + img * p.s_istride;
     const int W = p.W, H = p.H, G = p.G, nblk = p.nblk;
@@ -212,6 +219,26 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
 
     if (p.stamps && cta == 0 && threadIdx.x == 0) p.stamps[img * p.st_istride + 0] = globaltimer();
 
+    // K1 fix-up of the previous removal: rows are
+    // spread over every thread of the cluster; made visible by the barrier below
+    if (p.prev_seam) {
+        const int* ps = p.prev_seam + img * p.s_istride;
+        const uint32_t* rgb = p.rgb + img * p.rgb_istride;
+        const int nthr = ncl * NWARP * 32, tid = cta * NWARP * 32 + threadIdx.x;
+        for (int i = tid; i < H; i += nthr) {
+            const int sp = __ldg(ps + i);
+            const uint32_t* row = rgb + (long long)i * p.rpitch;
+            const uint32_t* up = rgb + (long long)max(i - 1, 0) * p.rpitch;
+            const uint32_t* dn = rgb + (long long)min(i + 1, H - 1) * p.rpitch;
+#pragma unroll
+            for (int x = sp - 1; x <= sp; ++x)
+                if (x >= 0 && x < W)
+                    e[(long long)i * p.epitch + x] =
+                        e1(luma(row[max(x - 1, 0)]), luma(row[min(x + 1, W - 1)]), luma(up[x]), luma(dn[x]));
+        }
+        __threadfence();
+    }
+
     // which of my C columns are useful (inside my segment and the image)
     uint32_t useful = 0;
 #pragma unroll
@@ -222,18 +249,6 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
 
     double m[C];
     int lab[C];
-    load_row<C>(e, col0, m);
-#pragma unroll
-    for (int k = 0; k < C; ++k) lab[k] = col0 + k;
-    // M-boundary row 0 (block 0 starts from it)
-#pragma unroll
-    for (int k = 0; k < C; ++k)
-        if (useful >> k & 1) mbound[col0 + k] = m[k];
-    if constexpr (TABLES) {
-#pragma unroll
-        for (int k = 0; k < C; ++k)
-            if (useful >> k & 1) { p.m_out[col0 + k] = m[k]; p.b_out[col0 + k] = col0 + k; }
-    }
 
     // Halo mailboxes. My left neighbour's right-halo slot (side 1) and my right
     // neighbour's left-halo slot (side 0), as shared::cluster addresses (the
@@ -262,9 +277,23 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
         mbar_init(my_b + 8, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // every mbarrier of the cluster is initialised before any halo is sent
+    // every mbarrier of the cluster is initialised before any halo is sent, and
+    // every fix-up store is visible before any energy row is read
     if (ncl > 1) cluster.sync();
     else __syncthreads();
+
+    load_row<C>(e, col0, m);
+#pragma unroll
+    for (int k = 0; k < C; ++k) lab[k] = col0 + k;
+    // M-boundary row 0 (block 0 starts from it)
+#pragma unroll
+    for (int k = 0; k < C; ++k)
+        if (useful >> k & 1) mbound[col0 + k] = m[k];
+    if constexpr (TABLES) {
+#pragma unroll
+        for (int k = 0; k < C; ++k)
+            if (useful >> k & 1) { p.m_out[col0 + k] = m[k]; p.b_out[col0 + k] = col0 + k; }
+    }
 
     // Forward pass. Rows 1..H-1 run in K-row blocks, each fully unrolled so
     // the ring slot, the halo exchange point and the loop control are

@@ -247,5 +247,5 @@ def test_batch_golden_sample(gold):
 def test_native_kernels_launched():
     cv.reset_launch_count()
     cv.carve(cv.make_test_image(64, 32), 60)
-    # unpack + energy + 2 pad fills + 4 x (dp + compact) + pack
-    assert cv.launch_count() == 13
+    # unpack + energy + pad fill + 4 x (dp + in-place removal) + pack
+    assert cv.launch_count() == 12
