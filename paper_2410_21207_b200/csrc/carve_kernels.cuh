@@ -366,26 +366,31 @@ __global__ void __launch_bounds__(CP_THREADS) k_compact(CompactParams p) {
     if (p.stamps && threadIdx.x == 0) atomicMax(&p.stamps[img * p.st_istride + 1], (unsigned long long)globaltimer());
 }
 
-// K4 in place (the carve loop's removal): one CTA per row; only pixels at or
+// K4 in place (the carve loop's removal): RPB rows per CTA; only pixels at or
 // right of the seam move (on average half the row), RGBX and FP64 energy.
 // Every thread loads its shifted source chunk, the CTA synchronises, then the
 // chunks are stored back, so the left shift by one is race-free within the row
 // and rows are independent. The energy fix-up of the two new-grid columns runs
 // in the next DP launch (Dp2Params::prev_seam), once every row is compacted.
-template <int CH>  // pixels per thread
+template <int CH, int RPB>  // pixels per thread, rows per CTA (loads of all rows in flight before one barrier)
 __global__ void __launch_bounds__(1024) k_compact_inplace(CompactParams p) {
-    const int img = blockIdx.y, i = blockIdx.x;
+    const int img = blockIdx.y;
     const int W = p.W, Wn = W - 1;
-    const int s = __ldg(p.seam + img * p.s_istride + i);
     const int base = threadIdx.x * CH;
-    if (p.stamps && i == 0 && threadIdx.x == 0)
+    if (p.stamps && blockIdx.x == 0 && threadIdx.x == 0)
         atomicCAS(&p.stamps[img * p.st_istride + 0], 0ull, (unsigned long long)globaltimer());
-    const bool active = base + CH > s && base < Wn;
-    uint32_t* rgb = p.rgb_out + img * p.p_istride + (long long)i * p.pitch;
-    double* e = p.e_out ? p.e_out + img * p.e_istride + (long long)i * p.epitch : nullptr;
-    uint32_t o[CH];
-    double oe[CH];
-    if (active) {
+    uint32_t o[RPB][CH];
+    double oe[RPB][CH];
+    bool act[RPB];
+#pragma unroll
+    for (int r = 0; r < RPB; ++r) {
+        const int i = blockIdx.x * RPB + r;
+        act[r] = false;
+        if (i >= p.H) continue;
+        const int s = __ldg(p.seam + img * p.s_istride + i);
+        act[r] = base + CH > s && base < Wn;
+        if (!act[r]) continue;
+        const uint32_t* rgb = p.rgb_out + img * p.p_istride + (long long)i * p.pitch;
         uint32_t a[CH + 1];
 #pragma unroll
         for (int q = 0; q < CH; q += 4) {
@@ -394,8 +399,9 @@ __global__ void __launch_bounds__(1024) k_compact_inplace(CompactParams p) {
         }
         a[CH] = base + CH < W ? rgb[base + CH] : 0u;
 #pragma unroll
-        for (int u = 0; u < CH; ++u) o[u] = (base + u >= s) ? a[u + 1] : a[u];
-        if (e) {
+        for (int u = 0; u < CH; ++u) o[r][u] = (base + u >= s) ? a[u + 1] : a[u];
+        if (p.e_out) {
+            const double* e = p.e_out + img * p.e_istride + (long long)i * p.epitch;
             double b[CH + 1];
 #pragma unroll
             for (int q = 0; q < CH; q += 2) {
@@ -404,29 +410,38 @@ __global__ void __launch_bounds__(1024) k_compact_inplace(CompactParams p) {
             }
             b[CH] = base + CH < W ? e[base + CH] : 0.0;
 #pragma unroll
-            for (int u = 0; u < CH; ++u) oe[u] = (base + u >= s) ? b[u + 1] : b[u];
+            for (int u = 0; u < CH; ++u) oe[r][u] = (base + u >= s) ? b[u + 1] : b[u];
         }
     }
     __syncthreads();
-    if (active) {
-        if (base + CH <= Wn) {
 #pragma unroll
-            for (int q = 0; q < CH; q += 4)
-                *reinterpret_cast<uint4*>(rgb + base + q) = make_uint4(o[q], o[q + 1], o[q + 2], o[q + 3]);
-            if (e) {
+    for (int r = 0; r < RPB; ++r) {
+        const int i = blockIdx.x * RPB + r;
+        if (i >= p.H) continue;
+        double* e = p.e_out ? p.e_out + img * p.e_istride + (long long)i * p.epitch : nullptr;
+        if (act[r]) {
+            uint32_t* rgb = p.rgb_out + img * p.p_istride + (long long)i * p.pitch;
+            if (base + CH <= Wn) {
 #pragma unroll
-                for (int q = 0; q < CH; q += 2) *reinterpret_cast<double2*>(e + base + q) = make_double2(oe[q], oe[q + 1]);
-            }
-        } else {
+                for (int q = 0; q < CH; q += 4)
+                    *reinterpret_cast<uint4*>(rgb + base + q) =
+                        make_uint4(o[r][q], o[r][q + 1], o[r][q + 2], o[r][q + 3]);
+                if (e) {
 #pragma unroll
-            for (int u = 0; u < CH; ++u)
-                if (base + u < Wn) {
-                    rgb[base + u] = o[u];
-                    if (e) e[base + u] = oe[u];
+                    for (int q = 0; q < CH; q += 2)
+                        *reinterpret_cast<double2*>(e + base + q) = make_double2(oe[r][q], oe[r][q + 1]);
                 }
+            } else {
+#pragma unroll
+                for (int u = 0; u < CH; ++u)
+                    if (base + u < Wn) {
+                        rgb[base + u] = o[r][u];
+                        if (e) e[base + u] = oe[r][u];
+                    }
+            }
         }
+        if (e && threadIdx.x == 0) e[Wn] = dinf();  // the vacated column joins the +inf pad
     }
-    if (e && threadIdx.x == 0) e[Wn] = dinf();  // the vacated column joins the +inf pad
     if (p.stamps && threadIdx.x == 0) atomicMax(&p.stamps[img * p.st_istride + 1], (unsigned long long)globaltimer());
 }
 
