@@ -222,6 +222,12 @@ void launch_fill_pads(double* e, int epitch, int W, int H, int nimg, long long e
     LAUNCHED("k_fill_pads");
 }
 
+void launch_rgb_edges(uint32_t* rgb, int pitch, int W, int H, int nimg, long long is, cudaStream_t s) {
+    dim3 grid(grid_for(H, 256), nimg);
+    k_rgb_edges<<<grid, 256, 0, s>>>(rgb, pitch, W, H, is);
+    LAUNCHED("k_rgb_edges");
+}
+
 int padded_epitch(int w) { return int(round_up(size_t(EPAD_L) + w + EPAD_R, 32)); }
 
 constexpr int kDpSmemBudget = 220 * 1024;
@@ -232,6 +238,7 @@ struct Dp2Variant {
     const void* fn;        // hot kernel (no tables)
     const void* fn_tables; // parity-API kernel (writes the full cost / predecessor tables)
     const void* fn_prof;   // hot kernel + clock64 phase counters (tools)
+    const void* fn_fused;  // hot kernel, energy recomputed from RGBX (batch mode)
     size_t (*smem)(int nblk, int D);
     int S() const { return 32 * C - 2 * K; }
     int cols() const { return NW * S(); }
@@ -240,7 +247,8 @@ struct Dp2Variant {
 template <int C, int K, int NW, int D>
 constexpr Dp2Variant dp2_variant() {
     return Dp2Variant{C, K, NW, D, (const void*)k_dp2<C, K, NW, D, 0>, (const void*)k_dp2<C, K, NW, D, 1>,
-                      (const void*)k_dp2<C, K, NW, D, 2>, &Dp2Smem<C, K, NW>::total};
+                      (const void*)k_dp2<C, K, NW, D, 2>, (const void*)k_dp2<C, K, NW, D, 0, true>,
+                      &Dp2Smem<C, K, NW>::total};
 }
 
 // preference order: the first variant whose cluster fits (<= 8 CTAs, then <= 16) wins
@@ -272,7 +280,7 @@ constexpr int kNumDp2Variants = int(sizeof(kDp2Variants) / sizeof(kDp2Variants[0
 
 void init_kernel_attributes(Ctx& c) {
     for (const Dp2Variant& v : kDp2Variants)
-        for (const void* fn : {v.fn, v.fn_tables, v.fn_prof}) {
+        for (const void* fn : {v.fn, v.fn_tables, v.fn_prof, v.fn_fused}) {
             ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kDpSmemBudget),
                "cudaFuncSetAttribute(dp2 smem)");
             ck(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
@@ -316,12 +324,12 @@ Dp2Plan dp2_plan(int W, int H) {
                                       std::to_string(H));
 }
 
-void launch_dp2(Ctx& c, const Dp2Plan& pl, Dp2Params p, int nimg, cudaStream_t s) {
+void launch_dp2(Ctx& c, const Dp2Plan& pl, Dp2Params p, int nimg, cudaStream_t s, bool fused = false) {
     const Dp2Variant& v = *pl.v;
     p.G = pl.ncl * v.NW;
     p.nblk = pl.nblk;
     p.dbg = env_int("CARVE_DP_DBG", 0);
-    const void* fn = p.m_out ? v.fn_tables : (p.prof ? v.fn_prof : v.fn);
+    const void* fn = fused ? v.fn_fused : p.m_out ? v.fn_tables : (p.prof ? v.fn_prof : v.fn);
     if (c.smem_set.find(fn) == c.smem_set.end()) fail(CARVE_E_CUDA, "DP kernel attributes not initialised");
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(nimg * pl.ncl));
@@ -387,10 +395,13 @@ CarveGeometry geometry(int w, int h, int tw, int th) {
     g.h = h;
     g.tw = tw;
     g.th = th;
-    g.pitch_a = int(round_up(w, 32));
-    g.pitch_b = int(round_up(h, 32));
-    g.plane = size_t(g.pitch_a) * h;
-    if (th != h) g.plane = std::max(g.plane, size_t(g.pitch_b) * tw);
+    // RGBX planes share the energy planes' padded geometry: logical column 0 at
+    // EPAD_L, >= EPAD_R columns after the live width, EPAD_B spare rows. The
+    // fused DP reads RGBX rows exactly like energy rows (unconditional loads).
+    g.pitch_a = padded_epitch(w);
+    g.pitch_b = padded_epitch(h);
+    g.plane = size_t(g.pitch_a) * (h + EPAD_B);
+    if (th != h) g.plane = std::max(g.plane, size_t(g.pitch_b) * (tw + EPAD_B));
     g.dpitch = int(round_up(std::max(w, h), 16) + 128);
     g.dir_rows = std::max(h, tw);
     g.seam_ints = size_t(w - tw) * h + size_t(h - th) * tw;
@@ -420,7 +431,8 @@ size_t stamp_words(const CarveGeometry& g) { return size_t(g.nseams) * 4 + 4; }
 void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const CarveGeometry& g, int* d_seams,
                size_t seam_istride, unsigned long long* d_stamps, cudaStream_t s) {
     const long long in_is = (long long)g.w * g.h * 3, out_is = (long long)g.tw * g.th * 3;
-    uint32_t* rgb[2] = {c.rgb[0].as<uint32_t>(), c.rgb[1].as<uint32_t>()};  // [1]: transpose target only
+    // logical column 0 of each padded RGBX plane ([1]: transpose target only)
+    uint32_t* rgb[2] = {c.rgb[0].as<uint32_t>() + EPAD_L, c.rgb[1].p ? c.rgb[1].as<uint32_t>() + EPAD_L : nullptr};
     double* e = c.e[0].as<double>() + EPAD_L;                                 // logical column 0
     const long long eis = (long long)g.eplane;
     const long long pis = (long long)g.plane;
@@ -434,14 +446,22 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
     // One orientation's seam loop: K1 once, then per seam the DP (whose
     // prologue applies the previous removal's 2-column energy fix-up) and the
     // in-place removal. Nothing returns to the host between seams.
+    // Batches run the fused DP (energy recomputed from RGBX, no energy plane);
+    // single images keep the incremental energy plane. CARVE_FUSED=0/1 overrides.
+    const int fused_env = env_int("CARVE_FUSED", -1);
+    const bool fused = fused_env >= 0 ? fused_env != 0 : nimg > 1;
     auto phase = [&](int W0, int H, int ntake, int pitch, int epitch, int seam_base, int stamp_seam0) {
         if (ntake <= 0) return;
-        {
-            // algorithmic bytes: 3 B RGB read + 8 B FP64 write per pixel
-            Prof pr(c, s, KK_ENERGY, 11.0 * W0 * H * nimg);
-            launch_energy(rgb[cur], pitch, W0, H, e, epitch, nimg, pis, eis, s);
+        if (fused) {
+            launch_rgb_edges(rgb[cur], pitch, W0, H, nimg, pis, s);
+        } else {
+            {
+                // algorithmic bytes: 3 B RGB read + 8 B FP64 write per pixel
+                Prof pr(c, s, KK_ENERGY, 11.0 * W0 * H * nimg);
+                launch_energy(rgb[cur], pitch, W0, H, e, epitch, nimg, pis, eis, s);
+            }
+            launch_fill_pads(e, epitch, W0, H, nimg, eis, s);
         }
-        launch_fill_pads(e, epitch, W0, H, nimg, eis, s);
         for (int k = 0; k < ntake; ++k) {
             const int W = W0 - k;
             t_dbg_tag = W;
@@ -462,20 +482,21 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
                 q.mb_istride = g.mb_istride;
                 q.s_istride = (long long)seam_istride;
                 q.st_istride = (long long)sw;
-                if (k > 0) {  // fix up the energy around the previous seam (removed from width W + 1)
-                    q.prev_seam = seam - H;
-                    q.rgb = rgb[cur];
-                    q.rpitch = pitch;
-                    q.rgb_istride = pis;
-                }
-                // algorithmic: 8 B FP64 energy read per cell (no direction plane)
-                Prof pr(c, s, KK_DP, 8.0 * W * H * nimg);
-                launch_dp2(c, pl, q, nimg, s);
+                q.rgb = rgb[cur];
+                q.rpitch = pitch;
+                q.rgb_istride = pis;
+                // fix up the energy around the previous seam (removed from width W + 1)
+                if (k > 0 && !fused) q.prev_seam = seam - H;
+                // algorithmic: 8 B FP64 energy read per cell (no direction
+                // plane); fused: 4 B RGBX read per cell
+                Prof pr(c, s, KK_DP, (fused ? 4.0 : 8.0) * W * H * nimg);
+                launch_dp2(c, pl, q, nimg, s, fused);
             }
             CompactParams q{};
             const bool last = (k + 1 == ntake);
             q.rgb_in = q.rgb_out = rgb[cur];
-            q.e_in = q.e_out = last ? nullptr : e;  // the final width needs no energy
+            q.e_in = q.e_out = (last || fused) ? nullptr : e;  // the final width needs no energy
+            q.rgb_edges = fused && !last;
             q.pitch = pitch;
             q.epitch = epitch;
             q.W = W;
@@ -489,7 +510,7 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
             {
                 // algorithmic: read W + write W-1 per row, 3 B RGB (+ 8 B FP64) per
                 // element, although the in-place kernel moves only the part right of the seam
-                Prof pr(c, s, KK_COMPACT, (last ? 3.0 : 11.0) * H * (2.0 * W - 1) * nimg);
+                Prof pr(c, s, KK_COMPACT, ((last || fused) ? 3.0 : 11.0) * H * (2.0 * W - 1) * nimg);
                 launch_compact_inplace(q, nimg, s);
             }
         }

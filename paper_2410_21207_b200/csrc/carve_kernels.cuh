@@ -297,6 +297,7 @@ struct CompactParams {
     double* e_out;
     int pitch;   // RGBX plane pitch (elements)
     int epitch;  // energy plane pitch (doubles); e_in/e_out point at logical column 0
+    int rgb_edges;  // in-place kernel: keep the RGBX replica columns -1 and W-1 (fused DP)
     int W, H;
     const int* seam;
     unsigned long long* stamps;  // optional [start, end] per image (written by block 0 / last block)
@@ -442,7 +443,28 @@ __global__ void __launch_bounds__(1024) k_compact_inplace(CompactParams p) {
         }
         if (e && threadIdx.x == 0) e[Wn] = dinf();  // the vacated column joins the +inf pad
     }
+    if (p.rgb_edges) {  // replica columns for the fused DP's clamped stencil (raster.hpp:54-58)
+        __syncthreads();
+        if (threadIdx.x < RPB) {
+            const int i = blockIdx.x * RPB + threadIdx.x;
+            if (i < p.H) {
+                uint32_t* rgb = p.rgb_out + img * p.p_istride + (long long)i * p.pitch;
+                rgb[-1] = rgb[0];
+                rgb[Wn] = rgb[Wn - 1];
+            }
+        }
+    }
     if (p.stamps && threadIdx.x == 0) atomicMax(&p.stamps[img * p.st_istride + 1], (unsigned long long)globaltimer());
+}
+
+// RGBX replica columns -1 and W (edge replication, raster.hpp:54-58) for the fused DP.
+__global__ void k_rgb_edges(uint32_t* __restrict__ rgb, int pitch, int W, int H, long long istride) {
+    rgb += blockIdx.y * istride;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < H; i += gridDim.x * blockDim.x) {
+        uint32_t* row = rgb + (long long)i * pitch;
+        row[-1] = row[0];
+        row[W] = row[W - 1];
+    }
 }
 
 }  // namespace carve_dev

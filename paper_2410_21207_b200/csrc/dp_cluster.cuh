@@ -170,9 +170,40 @@ __device__ __forceinline__ void st_async_b32(uint32_t raddr, uint32_t v, uint32_
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
 }
+__device__ __forceinline__ void cp_async8(uint32_t saddr, const void* g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(saddr), "l"(g) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// e1 of a lane's C columns from three luma rows (up, cur, down); the columns
+// just outside the lane come from the neighbouring lanes (garbage at a warp's
+// outermost columns, which the trapezoid treats as invalid anyway); columns
+// outside the image are +inf (candidate exclusion).
+template <int C>
+__device__ __forceinline__ void energy_cols(const double (&Lp)[C], const double (&Lc)[C], const double (&Ln)[C],
+                                            uint32_t oob, double (&ev)[C]) {
+    const double lL = __shfl_up_sync(FULL, Lc[C - 1], 1);
+    const double lR = __shfl_down_sync(FULL, Lc[0], 1);
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+        const double left = k > 0 ? Lc[k - 1] : lL;
+        const double right = k + 1 < C ? Lc[k + 1] : lR;
+        ev[k] = e1(left, right, Lp[k], Ln[k]);
+    }
+    if (oob) {
+#pragma unroll
+        for (int k = 0; k < C; ++k)
+            if (oob >> k & 1) ev[k] = dinf();
+    }
+}
+
+template <int C>
+__device__ __forceinline__ void luma_cols(const uint32_t* px, double (&L)[C]) {
+#pragma unroll
+    for (int k = 0; k < C; ++k) L[k] = luma(px[k]);
+}
 
 __device__ __forceinline__ void argmin_combine(double& v, int& i, double ov, int oi) {
     if (ov < v || (ov == v && oi < i)) { v = ov; i = oi; }
@@ -180,7 +211,10 @@ __device__ __forceinline__ void argmin_combine(double& v, int& i, double ov, int
 
 // MODE 0: hot kernel; 1: also writes the full cost/predecessor tables (parity
 // API); 2: hot kernel + per-warp clock64 phase counters into p.prof (tools only)
-template <int C, int K, int NWARP, int D, int MODE>
+// FUSED: no energy plane — e1 is recomputed in registers from RGBX rows
+// streamed through the same ring (rolling three luma rows per lane). Used for
+// batches, where the energy plane's 16 B/px/seam of traffic bounds throughput.
+template <int C, int K, int NWARP, int D, int MODE, bool FUSED = false>
 __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     constexpr bool TABLES = MODE == 1;
     constexpr bool PROF = MODE == 2;
@@ -282,7 +316,28 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     if (ncl > 1) cluster.sync();
     else __syncthreads();
 
-    load_row<C>(e, col0, m);
+    // fused mode: rolling luma rows (i-1, i, i+1) of my columns; rows clamp at the borders
+    double Lp[C], Lc[C], Ln[C];
+    uint32_t oob = 0;
+    const uint32_t* rgbf = FUSED ? p.rgb + img * p.rgb_istride + col0 : nullptr;
+    if constexpr (FUSED) {
+#pragma unroll
+        for (int k = 0; k < C; ++k)
+            if (col0 + k < 0 || col0 + k >= W) oob |= 1u << k;
+        uint32_t px[C];
+#pragma unroll
+        for (int k = 0; k < C; ++k) px[k] = __ldg(rgbf + k);
+        luma_cols<C>(px, Lc);
+        const uint32_t* r1 = rgbf + (long long)min(1, H - 1) * p.rpitch;
+#pragma unroll
+        for (int k = 0; k < C; ++k) px[k] = __ldg(r1 + k);
+        luma_cols<C>(px, Ln);
+#pragma unroll
+        for (int k = 0; k < C; ++k) Lp[k] = Lc[k];
+        energy_cols<C>(Lp, Lc, Ln, oob, m);  // M[0] = e[0]
+    } else {
+        load_row<C>(e, col0, m);
+    }
 #pragma unroll
     for (int k = 0; k < C; ++k) lab[k] = col0 + k;
     // M-boundary row 0 (block 0 starts from it)
@@ -299,21 +354,42 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     // the ring slot, the halo exchange point and the loop control are
     // compile-time; energy rows i+1..i+D are in flight while row i computes
     // (slot (i-1) % D is consumed, then refilled with row i+D).
-    const double* nrow = e + p.epitch + col0;
-    static_assert(C % 2 == 0, "cp.async moves 16-byte pairs of doubles");  // my slice of the next row to fetch (spare rows past H-1 are harmless)
-    auto fetch = [&](int u) {  // this lane's C energies of row `nrow` -> ring stage u, one commit group per row
+    const double* nrow = e + p.epitch + col0;  // my slice of the next row to fetch (spare rows past H-1 are harmless)
+    static_assert(C % 2 == 0, "cp.async moves 16-byte pairs of doubles");
+    int frow = 2;  // fused: next RGBX row to fetch (the ring feeds luma row i+1 at row i)
+    auto fetch = [&](int u) {  // this lane's C values of the next row -> ring stage u, one commit group per row
+        if constexpr (FUSED) {
+            const uint32_t* src = rgbf + (long long)min(frow, H - 1) * p.rpitch;
+            const uint32_t dst = ring_lane + uint32_t(u * 32 * C * 8);
+            if constexpr (C == 2) cp_async8(dst, src);
+            else {
 #pragma unroll
-        for (int k = 0; k < C; k += 2) cp_async16(ring_lane + uint32_t(u * 32 * C * 8 + k * 8), nrow + k);
+                for (int k = 0; k < C; k += 4) cp_async16(dst + k * 4, src + k);
+            }
+            ++frow;
+        } else {
+#pragma unroll
+            for (int k = 0; k < C; k += 2) cp_async16(ring_lane + uint32_t(u * 32 * C * 8 + k * 8), nrow + k);
+            nrow += p.epitch;
+        }
         cp_async_commit();
-        nrow += p.epitch;
     };
 #pragma unroll
     for (int u = 0; u < D; ++u) fetch(u);
 
     auto step = [&](int u, int i) {
-        cp_async_wait<D - 1>();  // row i (the oldest of the D groups in flight) has landed
+        cp_async_wait<D - 1>();  // the oldest of the D groups in flight has landed
         double ev[C];
-        {
+        if constexpr (FUSED) {
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(ring_s + ((size_t(warp) * D + u) * 32 + lane) * C);
+            uint32_t px[C];
+#pragma unroll
+            for (int k = 0; k < C; ++k) px[k] = src[k];
+#pragma unroll
+            for (int k = 0; k < C; ++k) { Lp[k] = Lc[k]; Lc[k] = Ln[k]; }
+            luma_cols<C>(px, Ln);  // row i+1 (clamped at the bottom)
+            energy_cols<C>(Lp, Lc, Ln, oob, ev);
+        } else {
             const double* src = ring_s + ((size_t(warp) * D + u) * 32 + lane) * C;
 #pragma unroll
             for (int k = 0; k < C; k += 2) {
@@ -497,7 +573,8 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
         for (int b = g; b < nblk && !(p.dbg & 1); b += G) {
             const int r0 = 1 + LBLK * b, r1 = min(LBLK * (b + 1), H - 1);
             const int c1 = __ldcg(seam + r1);  // phase 1 left the block's bottom column in global memory
-            const int wbase = (c1 - P2_COLS / 2) & ~1;  // even: 16-byte aligned double2 loads
+            // 16-byte aligned lane slices: even column for double2 energies, multiple of 4 for RGBX
+            const int wbase = (c1 - P2_COLS / 2) & (FUSED ? ~3 : ~1);
             const int wc0 = wbase + lane * 4;
             double mm[4];
 #pragma unroll
@@ -507,11 +584,33 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
             }
             // the block's energy rows stream through this warp's (now idle) forward ring,
             // P2D rows in flight via cp.async
+            // fused: rolling luma rows of the window; the ring carries RGBX row r+1 at row r
+            double QLp[4], QLc[4], QLn[4];
+            uint32_t qoob = 0;
+            const uint32_t* wrgb = FUSED ? p.rgb + img * p.rgb_istride + wc0 : nullptr;
+            if constexpr (FUSED) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (wc0 + k < 0 || wc0 + k >= W) qoob |= 1u << k;
+                uint32_t px[4];
+                const uint32_t* ra = wrgb + (long long)(r0 - 1) * p.rpitch;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) px[k] = __ldg(ra + k);
+                luma_cols<4>(px, QLp);
+                const uint32_t* rb = wrgb + (long long)r0 * p.rpitch;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) px[k] = __ldg(rb + k);
+                luma_cols<4>(px, QLc);
+            }
             auto p2fetch = [&](int r, int slot) {
-                const double* src = e + (long long)min(r, r1) * p.epitch + wc0;
                 const uint32_t dst = p2ring + uint32_t(slot * P2_COLS * 8);
-                cp_async16(dst, src);
-                cp_async16(dst + 16, src + 2);
+                if constexpr (FUSED) {
+                    cp_async16(dst, wrgb + (long long)min(r + 1, H - 1) * p.rpitch);
+                } else {
+                    const double* src = e + (long long)min(r, r1) * p.epitch + wc0;
+                    cp_async16(dst, src);
+                    cp_async16(dst + 16, src + 2);
+                }
                 cp_async_commit();
             };
 #pragma unroll
@@ -520,7 +619,14 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
                 const int slot = (r - r0) % P2D;
                 cp_async_wait<P2D - 1>();
                 double ec[4];
-                {
+                if constexpr (FUSED) {
+                    const uint4 q = *reinterpret_cast<const uint4*>(p2ring_ptr + slot * P2_COLS);
+                    const uint32_t px[4] = {q.x, q.y, q.z, q.w};
+                    luma_cols<4>(px, QLn);
+                    energy_cols<4>(QLp, QLc, QLn, qoob, ec);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) { QLp[k] = QLc[k]; QLc[k] = QLn[k]; }
+                } else {
                     const double* src = p2ring_ptr + slot * P2_COLS;
                     const double2 x0 = *reinterpret_cast<const double2*>(src);
                     const double2 x1 = *reinterpret_cast<const double2*>(src + 2);

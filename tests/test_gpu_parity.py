@@ -157,7 +157,7 @@ def test_transpose(port):
 
 
 # -- whole pipeline -------------------------------------------------------------------
-def test_carve_small_golden():
+def test_carve_small_golden(dp_mode):
     z = np.load(os.path.join(GOLD, "small.npz"))
     for k in range(int(z["n"])):
         img = z[f"img{k}"]
@@ -170,9 +170,18 @@ def test_carve_small_golden():
         assert np.array_equal(bits(cv.energy_e1_rgb(img)), bits(z[f"e{k}"])), k
 
 
+@pytest.fixture(params=["plane", "fused"])
+def dp_mode(request, monkeypatch):
+    """Run a test under both DP modes: the incremental energy plane (single-image
+    default) and the fused RGBX-recompute mode (batch default), CARVE_FUSED."""
+    monkeypatch.setenv("CARVE_FUSED", "1" if request.param == "fused" else "0")
+    return request.param
+
+
 @pytest.mark.parametrize("w,h,tw,th", [(64, 48, 40, 48), (100, 80, 60, 50), (37, 120, 30, 100), (200, 3, 150, 3),
-                                       (5, 200, 5, 100), (260, 140, 129, 70)])
-def test_carve_vs_port(port, w, h, tw, th):
+                                       (5, 200, 5, 100), (260, 140, 129, 70), (2, 2, 1, 1), (3, 1, 1, 1),
+                                       (1, 9, 1, 4)])
+def test_carve_vs_port(port, dp_mode, w, h, tw, th):
     rng = np.random.default_rng(w + h)
     for img in (port.make_test_image(w, h), rng.integers(0, 256, (h, w, 3), dtype=np.uint8),
                 np.full((h, w, 3), 77, np.uint8)):
@@ -212,7 +221,7 @@ def test_carve_reference_api_contract():
 
 
 @pytest.mark.parametrize("name", ["C1", "C2"])
-def test_config_golden(gold, name):
+def test_config_golden(gold, dp_mode, name):
     c = gold["configs"][name]
     img = cv.make_test_image(c["W"], c["H"])
     assert f"{oracle.fnv1a64(img):016x}" == c["input"]
@@ -223,7 +232,7 @@ def test_config_golden(gold, name):
 
 @pytest.mark.slow
 @pytest.mark.parametrize("name", ["C3", "C4"])
-def test_config_golden_full(gold, name):
+def test_config_golden_full(gold, dp_mode, name):
     c = gold["configs"].get(name)
     if c is None:
         pytest.skip(f"{name} golden not generated")
@@ -234,7 +243,7 @@ def test_config_golden_full(gold, name):
     assert f"{oracle.fnv1a64(np.concatenate(seams)):016x}" == c["seams"]
 
 
-def test_batch_golden_sample(gold):
+def test_batch_golden_sample(gold, dp_mode):
     c = gold["configs"]["C5"]
     ks = [int(k) for k in c["samples"]]
     imgs = [cv.make_test_image(c["W"], c["H"], k) for k in ks]
