@@ -253,28 +253,15 @@ constexpr Dp2Variant dp2_variant() {
 
 // preference order: the first variant whose cluster fits (<= 8 CTAs, then <= 16) wins
 const Dp2Variant kDp2Variants[] = {
-    dp2_variant<2, 16, 8, 8>(),   // 0: S=32,  256 cols/CTA
-    dp2_variant<4, 32, 4, 8>(),   // 1: S=64,  256 cols/CTA
-    dp2_variant<4, 16, 4, 8>(),   // 2: S=96,  384 cols/CTA
-    dp2_variant<2, 8, 8, 8>(),    // 3: S=48,  384 cols/CTA
-    dp2_variant<4, 16, 8, 8>(),   // 4: S=96,  768 cols/CTA
-    dp2_variant<2, 8, 16, 8>(),   // 5: S=48,  768 cols/CTA
-    dp2_variant<8, 16, 4, 4>(),   // 6: S=224, 896 cols/CTA
-    dp2_variant<2, 16, 4, 8>(),   // 7: S=32,  128 cols/CTA (1 warp per scheduler)
-    dp2_variant<2, 8, 4, 8>(),    // 8: S=48,  192 cols/CTA (1 warp per scheduler)
-    dp2_variant<4, 16, 2, 8>(),   // 9: S=96,  192 cols/CTA
-    dp2_variant<4, 8, 4, 8>(),    // 10: S=112, 448 cols/CTA
-    dp2_variant<8, 32, 4, 4>(),   // 11: S=192, 768 cols/CTA
-    dp2_variant<2, 16, 4, 16>(),  // 12: as 7, 16-row ring
-    dp2_variant<2, 16, 8, 16>(),  // 13: as 0, 16-row ring
-    dp2_variant<4, 16, 4, 16>(),  // 14: as 2, 16-row ring
-    dp2_variant<4, 32, 4, 16>(),  // 15: as 1, 16-row ring
-    dp2_variant<2, 16, 16, 16>(), // 16: S=32,  512 cols/CTA (wide rows, 4 warps per scheduler)
-    dp2_variant<4, 16, 8, 16>(),  // 17: as 4, 16-row ring
-    // throughput (batch) candidates: low halo redundancy, one CTA per 1024-wide image
-    dp2_variant<8, 8, 5, 4>(),    // 18: S=240, 1200 cols/CTA (7% halo)
-    dp2_variant<4, 8, 10, 8>(),   // 19: S=112, 1120 cols/CTA (14% halo)
-    dp2_variant<8, 16, 5, 4>(),   // 20: S=224, 1120 cols/CTA (14% halo)
+    dp2_variant<2, 16, 4, 16>(),  // 0: S=32,  128 cols/CTA, one warp per scheduler (C1/C2/C5-wide rows)
+    dp2_variant<2, 16, 8, 16>(),  // 1: S=32,  256 cols/CTA (C3, up to 4096 columns)
+    dp2_variant<2, 16, 8, 8>(),   // 2: S=32,  256 cols/CTA, 8-row ring
+    dp2_variant<4, 16, 8, 8>(),   // 3: S=96,  768 cols/CTA (C4: 7680 columns in 10 CTAs)
+    dp2_variant<2, 8, 16, 8>(),   // 4: S=48,  768 cols/CTA
+    dp2_variant<4, 16, 4, 8>(),   // 5: S=96,  384 cols/CTA (batches)
+    dp2_variant<4, 16, 4, 16>(),  // 6: S=96,  384 cols/CTA, 16-row ring
+    dp2_variant<4, 32, 4, 8>(),   // 7: S=64,  256 cols/CTA
+    dp2_variant<2, 16, 4, 8>(),   // 8: S=32,  128 cols/CTA, 8-row ring
 };
 constexpr int kNumDp2Variants = int(sizeof(kDp2Variants) / sizeof(kDp2Variants[0]));
 
@@ -300,16 +287,19 @@ int env_int(const char* name, int dflt) {
     return s && *s ? std::atoi(s) : dflt;
 }
 
-// Preference order (measured on B200, tools/sweep_dp.py): the first variant
-// whose cluster fits wins. Narrow rows favour one C=2 warp per scheduler.
-const int kDp2Order[] = {12, 13, 0, 16, 17, 4, 14, 5, 2, 7, 15, 1, 3, 8, 9, 10, 6, 11, 18, 19, 20};
+// Preference orders (measured on B200: tools/sweep_dp.py, tools/sweep_batch.py;
+// profiles/r01_dp_variant_sweep.jsonl): the first variant whose cluster fits
+// wins. Single images are latency-bound and favour one C=2 warp per
+// scheduler; batches are throughput-bound and favour less halo redundancy.
+const int kDp2Order[] = {0, 1, 2, 3, 4, 6, 5, 7, 8};
+const int kDp2BatchOrder[] = {5, 6, 0, 1, 2, 3, 4, 7, 8};
 
-Dp2Plan dp2_plan(int W, int H) {
+Dp2Plan dp2_plan(int W, int H, bool batch = false) {
     const int nblk = H > 1 ? (H - 1 + LBLK - 1) / LBLK : 0;
     const int forced = env_int("CARVE_DP_VARIANT", -1);
     const int max_ncl = env_int("CARVE_DP_MAX_NCL", 16);
     for (int pass = 0; pass < 2; ++pass) {
-        for (int k : kDp2Order) {
+        for (int k : batch ? kDp2BatchOrder : kDp2Order) {
             if (forced >= 0 && k != forced) continue;
             const Dp2Variant& v = kDp2Variants[k];
             const int ncl = (W + v.cols() - 1) / v.cols();
@@ -468,7 +458,7 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
             int* seam = d_seams + seam_base + size_t(k) * H;
             unsigned long long* st = d_stamps ? d_stamps + size_t(stamp_seam0 + k) * 4 : nullptr;
             {
-                const Dp2Plan pl = dp2_plan(W, H);
+                const Dp2Plan pl = dp2_plan(W, H, nimg > 1);
                 Dp2Params q{};
                 q.e = e;
                 q.epitch = epitch;

@@ -26,7 +26,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
                       "compact_us": 1e3 * cp["ms_total"] / cp["launches"]}))
     sys.exit(0)
 names = sys.argv[1:] or ["c2"]
-variants = os.environ.get("VARIANTS", "0,1,2,3,4,5,6,7,8,9").split(",")
+variants = os.environ.get("VARIANTS", "0,1,2,3,4,5,6,7,8").split(",")
 for name in names:
     for v in variants:
         env = dict(os.environ, CARVE_DP_VARIANT=v, CARVE_DP_MAX_NCL="16")
