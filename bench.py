@@ -337,14 +337,24 @@ def measure(cfg_name, args, rk, distinct_max=None):
             "desc": desc, "n_local": n_local, "n_distinct": n_distinct}
 
 
-def roofline_of(kern):
+def measured_traffic(kernel, cfg_name):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu
+    --set full capture (profiles/r01_traffic.json), for the workload it was taken on."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
+        return t["bytes_per_launch"].get(kernel) if cfg_name == "c2" else None
+    except Exception:
+        return None
+
+
+def roofline_of(kern, cfg_name="c2"):
     peak, peak_src = peaks()
     dom = max(kern, key=lambda k: kern[k]["ms_total"]) if kern else None
     if not dom:
         return None
     kd = kern[dom]
     return {"kernel": dom, "bound": "hbm", "achieved": kd["gbs"], "peak": peak, "unit": "GB/s",
-            "frac": kd["gbs"] / peak, "traffic": None, "peak_source": peak_src,
+            "frac": kd["gbs"] / peak, "traffic": measured_traffic(dom, cfg_name), "peak_source": peak_src,
             "bytes_per_launch": kd["bytes_per_launch"], "avg_launch_us": kd["avg_us"], "share_of_step": kd["share"]}
 
 
@@ -369,7 +379,7 @@ def run_ours(args, cfg_name):
         "config": {"workload": m["desc"] + ("" if batch else " per GPU"), "images_per_gpu": m["n_local"],
                    "l2": "flushed between steps (256 MiB write)",
                    "parallelism": f"image-sharded x{world}, no collective"},
-        "e2e": m["e2e"], "gpu_launches": m["gpu_launches"], "roofline": roofline_of(m["kernels"]),
+        "e2e": m["e2e"], "gpu_launches": m["gpu_launches"], "roofline": roofline_of(m["kernels"], cfg_name),
         "kernels": m["kernels"], "verified_vs_golden": m["verified_vs_golden"], "clocks": m["clocks"],
     }
     if not batch and not args.no_batch:
@@ -380,7 +390,7 @@ def run_ours(args, cfg_name):
                          "images_per_gpu": b["n_local"],
                          "data": f"{b['n_distinct']} distinct make_test_image variants per GPU, tiled to "
                                  f"{b['n_local']} images", "verified_vs_golden": b["verified_vs_golden"],
-                         "roofline": roofline_of(b["kernels"]), "kernels": b["kernels"],
+                         "roofline": roofline_of(b["kernels"], "c5"), "kernels": b["kernels"],
                          "gpu_launches": b["gpu_launches"], "clocks": b["clocks"]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg_name)
