@@ -354,6 +354,17 @@ void launch_compact_inplace(const CompactParams& p, int nimg, cudaStream_t s) {
     LAUNCHED("k_compact_inplace");
 }
 
+template <int MODE>
+void launch_compact_transpose(const uint32_t* in, int ipitch, int W, int H, const int* seam, uint32_t* out,
+                              int opitch, uint8_t* packed, int nimg, long long in_is, long long out_is,
+                              long long seam_is, long long pk_is, unsigned long long* st, long long st_is,
+                              cudaStream_t s) {
+    dim3 grid((W - 1 + 31) / 32, (H + 31) / 32, nimg);
+    k_compact_transpose<MODE><<<grid, dim3(32, 8), 0, s>>>(in, ipitch, W, H, seam, out, opitch, packed, in_is, out_is,
+                                                           seam_is, pk_is, st, st_is);
+    LAUNCHED("k_compact_transpose");
+}
+
 void launch_compact(const CompactParams& p, int nimg, cudaStream_t s) {
     const int per_cta = CP_THREADS * CP_CHUNK;
     dim3 grid((p.W - 1 + per_cta - 1) / per_cta, p.H, nimg);
@@ -440,7 +451,11 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
     // single images keep the incremental energy plane. CARVE_FUSED=0/1 overrides.
     const int fused_env = env_int("CARVE_FUSED", -1);
     const bool fused = fused_env >= 0 ? fused_env != 0 : nimg > 1;
-    auto phase = [&](int W0, int H, int ntake, int pitch, int epitch, int seam_base, int stamp_seam0) {
+    // `finish`: what the phase's last removal writes (fused with K4, see k_compact_transpose):
+    // OUT_PLANE  the transposed RGBX plane for the height phase (rgb[cur ^ 1], pitch_b)
+    // OUT_PACKED the final image, transposed back, packed RGB into d_out
+    // OUT_ROWS   the final image, packed RGB into d_out
+    auto phase = [&](int W0, int H, int ntake, int pitch, int epitch, int seam_base, int stamp_seam0, int finish) {
         if (ntake <= 0) return;
         if (fused) {
             launch_rgb_edges(rgb[cur], pitch, W0, H, nimg, pis, s);
@@ -497,25 +512,38 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
             q.e_istride = eis;
             q.s_istride = (long long)seam_istride;
             q.st_istride = (long long)sw;
-            {
+            if (!last) {
                 // algorithmic: read W + write W-1 per row, 3 B RGB (+ 8 B FP64) per
                 // element, although the in-place kernel moves only the part right of the seam
-                Prof pr(c, s, KK_COMPACT, ((last || fused) ? 3.0 : 11.0) * H * (2.0 * W - 1) * nimg);
+                Prof pr(c, s, KK_COMPACT, (fused ? 3.0 : 11.0) * H * (2.0 * W - 1) * nimg);
                 launch_compact_inplace(q, nimg, s);
+            } else {
+                // the last removal writes the next layout directly (3 B RGB read + 3 B written per pixel)
+                Prof pr(c, s, KK_COMPACT, 3.0 * H * (2.0 * W - 1) * nimg);
+                unsigned long long* cst = st ? st + 2 : nullptr;
+                const long long ls = (long long)seam_istride, lst = (long long)sw;
+                if (finish == OUT_PLANE)
+                    launch_compact_transpose<OUT_PLANE>(rgb[cur], pitch, W, H, seam, rgb[cur ^ 1], g.pitch_b, nullptr,
+                                                        nimg, pis, pis, ls, 0, cst, lst, s);
+                else if (finish == OUT_PACKED)
+                    launch_compact_transpose<OUT_PACKED>(rgb[cur], pitch, W, H, seam, nullptr, 0, d_out, nimg, pis, 0,
+                                                         ls, out_is, cst, lst, s);
+                else
+                    launch_compact_transpose<OUT_ROWS>(rgb[cur], pitch, W, H, seam, nullptr, 0, d_out, nimg, pis, 0,
+                                                       ls, out_is, cst, lst, s);
             }
         }
     };
-    phase(g.w, g.h, g.w - g.tw, g.pitch_a, g.epitch_a, 0, 0);
-    if (g.th != g.h) {
-        {
+    const bool hphase = g.th != g.h, vphase = g.tw != g.w;
+    phase(g.w, g.h, g.w - g.tw, g.pitch_a, g.epitch_a, 0, 0, hphase ? OUT_PLANE : OUT_ROWS);
+    if (hphase) {
+        if (!vphase) {  // nothing removed vertically: plain transpose into the height-phase layout
             Prof pr(c, s, KK_TRANSPOSE, 8.0 * g.tw * g.h * nimg);
             launch_transpose(rgb[cur], g.pitch_a, g.tw, g.h, rgb[cur ^ 1], g.pitch_b, nimg, pis, pis, s);
         }
         cur ^= 1;
-        phase(g.h, g.tw, g.h - g.th, g.pitch_b, g.epitch_b, (g.w - g.tw) * g.h, g.w - g.tw);
-        Prof pr(c, s, KK_PACK, 7.0 * g.tw * g.th * nimg);
-        launch_pack(c, rgb[cur], g.pitch_b, g.tw, g.th, true, d_out, nimg, pis, out_is, s);
-    } else {
+        phase(g.h, g.tw, g.h - g.th, g.pitch_b, g.epitch_b, (g.w - g.tw) * g.h, g.w - g.tw, OUT_PACKED);
+    } else if (!vphase) {  // identity carve
         Prof pr(c, s, KK_PACK, 7.0 * g.tw * g.th * nimg);
         launch_pack(c, rgb[cur], g.pitch_a, g.tw, g.th, false, d_out, nimg, pis, out_is, s);
     }

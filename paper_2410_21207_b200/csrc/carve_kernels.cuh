@@ -467,4 +467,68 @@ __global__ void k_rgb_edges(uint32_t* __restrict__ rgb, int pitch, int W, int H,
     }
 }
 
+// K4, last removal of a phase, fused with the layout change that follows it
+// (carver.hpp:216-222 transpose sandwich; raster.hpp:73-79):
+//   OUT_PLANE : out(j, i) = in(i, j + [j >= s_i])  -> the transposed RGBX plane
+//               the height phase carves (j < W-1, i < H)
+//   OUT_PACKED: the final image in packed RGB, transposed back (height phase)
+//   OUT_ROWS  : the final image in packed RGB, not transposed (width-only carves)
+// A 32x32 tile goes through shared memory, so the row-major reads of the
+// shifted row and the transposed writes are both coalesced.
+enum { OUT_PLANE = 0, OUT_PACKED = 1, OUT_ROWS = 2 };
+
+template <int MODE>
+__global__ void k_compact_transpose(const uint32_t* __restrict__ in, int ipitch, int W, int H,
+                                    const int* __restrict__ seam, uint32_t* __restrict__ out, int opitch,
+                                    uint8_t* __restrict__ packed, long long in_is, long long out_is, long long seam_is,
+                                    long long pk_is, unsigned long long* stamps, long long st_is) {
+    __shared__ uint32_t tile[32][33];
+    const int img = blockIdx.z;
+    in += img * in_is;
+    seam += img * seam_is;
+    if (stamps && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && threadIdx.y == 0)
+        atomicCAS(&stamps[img * st_is + 0], 0ull, (unsigned long long)globaltimer());
+    const int Wn = W - 1;
+    const int bj = blockIdx.x * 32, bi = blockIdx.y * 32;  // output-column (j) and row (i) tile origins
+    if (MODE == OUT_ROWS) {
+        // no transpose: rows stay rows; one thread per output pixel, packed write
+        for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+            const int i = bi + r, j = bj + threadIdx.x;
+            if (i < H && j < Wn) {
+                const int sp = __ldg(seam + i);
+                const uint32_t v = in[(long long)i * ipitch + j + (j >= sp ? 1 : 0)];
+                uint8_t* o = packed + img * pk_is + ((long long)i * Wn + j) * 3;
+                o[0] = uint8_t(v);
+                o[1] = uint8_t(v >> 8);
+                o[2] = uint8_t(v >> 16);
+            }
+        }
+    } else {
+        for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+            const int i = bi + r, j = bj + threadIdx.x;
+            if (i < H && j < Wn) {
+                const int sp = __ldg(seam + i);
+                tile[r][threadIdx.x] = in[(long long)i * ipitch + j + (j >= sp ? 1 : 0)];
+            }
+        }
+        __syncthreads();
+        for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+            const int j = bj + r, i = bi + threadIdx.x;  // output row j, column i
+            if (i < H && j < Wn) {
+                const uint32_t v = tile[threadIdx.x][r];
+                if (MODE == OUT_PLANE) {
+                    out[img * out_is + (long long)j * opitch + i] = v;
+                } else {
+                    uint8_t* o = packed + img * pk_is + ((long long)j * H + i) * 3;
+                    o[0] = uint8_t(v);
+                    o[1] = uint8_t(v >> 8);
+                    o[2] = uint8_t(v >> 16);
+                }
+            }
+        }
+    }
+    if (stamps && threadIdx.x == 0 && threadIdx.y == 0)
+        atomicMax(&stamps[img * st_is + 1], (unsigned long long)globaltimer());
+}
+
 }  // namespace carve_dev

@@ -256,5 +256,5 @@ def test_batch_golden_sample(gold, dp_mode):
 def test_native_kernels_launched():
     cv.reset_launch_count()
     cv.carve(cv.make_test_image(64, 32), 60)
-    # unpack + energy + pad fill + 4 x (dp + in-place removal) + pack
-    assert cv.launch_count() == 12
+    # unpack + energy + pad fill + 4 x dp + 3 in-place removals + the last removal fused with the pack
+    assert cv.launch_count() == 11
