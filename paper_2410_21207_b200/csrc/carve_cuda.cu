@@ -232,6 +232,14 @@ int padded_epitch(int w) { return int(round_up(size_t(EPAD_L) + w + EPAD_R, 32))
 
 constexpr int kDpSmemBudget = 220 * 1024;
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("CARVE_PDL");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
 // ---- K2+K3 v2: cluster trapezoid DP (dp_cluster.cuh) ------------------------
 struct Dp2Variant {
     int C, K, NW, D;
@@ -326,19 +334,36 @@ void launch_dp2(Ctx& c, const Dp2Plan& pl, Dp2Params p, int nimg, cudaStream_t s
     cfg.blockDim = dim3(unsigned(v.NW * 32));
     cfg.dynamicSmemBytes = pl.smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = unsigned(pl.ncl);
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     void* args[] = {&p};
     ck(cudaLaunchKernelExC(&cfg, fn, args), "launch k_dp2");
     LAUNCHED("k_dp2");
 }
 
 void launch_compact_inplace(const CompactParams& p, int nimg, cudaStream_t s) {
+    if (env_int("CARVE_COMPACT", 2) == 2) {  // warp per row (default); 1 = CTA per row
+        constexpr int WPB = 8;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((p.H + WPB - 1) / WPB, nimg);
+        cfg.blockDim = dim3(WPB * 32);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl_enabled() ? 1 : 0;
+        ck(cudaLaunchKernelEx(&cfg, k_compact_warp<4>, p), "launch k_compact_warp");
+        LAUNCHED("k_compact_warp");
+        return;
+    }
     // one row per CTA: measured faster than batching 2-4 rows per CTA (C2 10.5 vs 11.3 us)
     const int W = p.W;
     auto grid = [&](int rpb) { return dim3((p.H + rpb - 1) / rpb, nimg); };

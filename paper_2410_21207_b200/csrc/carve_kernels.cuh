@@ -36,6 +36,13 @@ constexpr int EPAD_L = 128, EPAD_R = 2304, EPAD_B = 16;
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
 
+// Programmatic dependent launch: a seam's DP and removal kernels are launched
+// with programmatic stream serialization, so each is scheduled while its
+// predecessor drains; pdl_wait() blocks until the predecessor grid has
+// completed and its writes are visible (a no-op for ordinary launches).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ uint64_t globaltimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -529,6 +536,79 @@ __global__ void k_compact_transpose(const uint32_t* __restrict__ in, int ipitch,
     }
     if (stamps && threadIdx.x == 0 && threadIdx.y == 0)
         atomicMax(&stamps[img * st_is + 1], (unsigned long long)globaltimer());
+}
+
+// K4 in place, one warp per row: the warp walks the part of the row right of
+// the seam in batches of NB chunks per lane; all loads of a batch are issued
+// before its stores, and batch b+1's loads only touch elements at or beyond
+// the last element batch b read, so the left shift is race-free in program
+// order without any CTA barrier. Rows are independent.
+template <int NB>
+__global__ void __launch_bounds__(256) k_compact_warp(CompactParams p) {
+    const int img = blockIdx.y;
+    const int lane = threadIdx.x & 31;
+    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    pdl_wait();  // the DP that produced this seam has completed
+    pdl_launch_dependents();
+    if (p.stamps && blockIdx.x == 0 && threadIdx.x == 0)
+        atomicCAS(&p.stamps[img * p.st_istride + 0], 0ull, (unsigned long long)globaltimer());
+    if (i < p.H) {
+        const int W = p.W, Wn = W - 1;
+        const int s = __ldg(p.seam + img * p.s_istride + i);
+        uint32_t* rgb = p.rgb_out + img * p.p_istride + (long long)i * p.pitch;
+        double* e = p.e_out ? p.e_out + img * p.e_istride + (long long)i * p.epitch : nullptr;
+        // first 4-aligned chunk that changes
+        const int q0 = (s >> 2);
+        for (int qb = q0; qb * 4 < Wn; qb += 32 * NB) {
+            uint32_t o[NB][4];
+            double oe[NB][4];
+#pragma unroll
+            for (int u = 0; u < NB; ++u) {
+                const int base = (qb + u * 32 + lane) * 4;
+                if (base < Wn) {
+                    const uint4 v = *reinterpret_cast<const uint4*>(rgb + base);
+                    const uint32_t a[5] = {v.x, v.y, v.z, v.w, base + 4 < W ? rgb[base + 4] : 0u};
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) o[u][t] = (base + t >= s) ? a[t + 1] : a[t];
+                    if (e) {
+                        const double2 v0 = *reinterpret_cast<const double2*>(e + base);
+                        const double2 v1 = *reinterpret_cast<const double2*>(e + base + 2);
+                        const double b[5] = {v0.x, v0.y, v1.x, v1.y, base + 4 < W ? e[base + 4] : 0.0};
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) oe[u][t] = (base + t >= s) ? b[t + 1] : b[t];
+                    }
+                }
+            }
+            __syncwarp();  // every lane's loads of this batch precede any store of it
+#pragma unroll
+            for (int u = 0; u < NB; ++u) {
+                const int base = (qb + u * 32 + lane) * 4;
+                if (base + 4 <= Wn) {
+                    *reinterpret_cast<uint4*>(rgb + base) = make_uint4(o[u][0], o[u][1], o[u][2], o[u][3]);
+                    if (e) {
+                        *reinterpret_cast<double2*>(e + base) = make_double2(oe[u][0], oe[u][1]);
+                        *reinterpret_cast<double2*>(e + base + 2) = make_double2(oe[u][2], oe[u][3]);
+                    }
+                } else if (base < Wn) {
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        if (base + t < Wn) {
+                            rgb[base + t] = o[u][t];
+                            if (e) e[base + t] = oe[u][t];
+                        }
+                }
+            }
+            __syncwarp();  // this batch's stores precede the next batch's loads
+        }
+        if (lane == 0) {
+            if (e) e[Wn] = dinf();  // the vacated column joins the +inf pad
+            if (p.rgb_edges) {      // replica columns for the fused DP (raster.hpp:54-58)
+                rgb[-1] = rgb[0];
+                rgb[Wn] = rgb[Wn - 1];
+            }
+        }
+    }
+    if (p.stamps && threadIdx.x == 0) atomicMax(&p.stamps[img * p.st_istride + 1], (unsigned long long)globaltimer());
 }
 
 }  // namespace carve_dev

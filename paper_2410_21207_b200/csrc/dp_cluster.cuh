@@ -251,6 +251,8 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     // this lane's C doubles of stage u: ring_s[((warp * D + u) * 32 + lane) * C]
     const uint32_t ring_lane = smem_u32(ring_s + (size_t(warp) * D * 32 + lane) * C);
 
+    pdl_wait();  // the previous removal has completed (its planes and seam log are visible)
+    pdl_launch_dependents();
     if (p.stamps && cta == 0 && threadIdx.x == 0) p.stamps[img * p.st_istride + 0] = globaltimer();
 
     // K1 fix-up of the previous removal: rows are

@@ -192,4 +192,67 @@ int main2() {
     printf("status %s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
-int main() { main1(); return main2(); }
+
+// 6) lane-level halos: each lane keeps H extra columns per side, shuffles every H rows
+template <int C, int H>
+__global__ void k_row3(double* out, int n, long long* cyc) {
+    constexpr int T = C + 2 * H;  // columns held: [col0 - H, col0 + C + H)
+    const int lane = threadIdx.x & 31;
+    double m[T];
+    int lab[T];
+    double ev[T];
+#pragma unroll
+    for (int k = 0; k < T; ++k) { m[k] = out[lane * C + k]; lab[k] = k; ev[k] = 1.0 + k; }
+    uint64_t t0 = clk();
+    for (int i0 = 0; i0 < n; i0 += H) {
+#pragma unroll
+        for (int t = 0; t < H; ++t) {
+            // row t of the block: valid range shrinks by one per row: k in [t+1, T-1-t)
+            double nm[T];
+            int nl[T];
+#pragma unroll
+            for (int k = t + 1; k < T - 1 - t; ++k) {
+                double best = m[k - 1];
+                int bl = lab[k - 1];
+                if (m[k] < best) { best = m[k]; bl = lab[k]; }
+                if (m[k + 1] < best) { best = m[k + 1]; bl = lab[k + 1]; }
+                nm[k] = __dadd_rn(ev[k], best);
+                nl[k] = bl;
+            }
+#pragma unroll
+            for (int k = t + 1; k < T - 1 - t; ++k) { m[k] = nm[k]; lab[k] = nl[k]; }
+        }
+        // refresh halos: my left halo = left lane's columns [C, C+H) -> its core end; right halo likewise
+#pragma unroll
+        for (int k = 0; k < H; ++k) {
+            const double a = __shfl_up_sync(0xffffffffu, m[C + k], 1);       // left lane's core tail
+            const int al = __shfl_up_sync(0xffffffffu, lab[C + k], 1);
+            const double b = __shfl_down_sync(0xffffffffu, m[H + k], 1);     // right lane's core head
+            const int bl = __shfl_down_sync(0xffffffffu, lab[H + k], 1);
+            m[k] = a; lab[k] = al;
+            m[C + H + k] = b; lab[C + H + k] = bl;
+        }
+    }
+    uint64_t t1 = clk();
+#pragma unroll
+    for (int k = 0; k < T; ++k) out[lane * C + k] = m[k] + lab[k];
+    if (threadIdx.x == 0) cyc[0] = (long long)(t1 - t0);
+}
+
+int main3() {
+    double* buf;
+    cudaMalloc(&buf, 1 << 20);
+    cudaMemset(buf, 0, 1 << 20);
+    const int n = 4096;
+    run("row3 C=2 H=1", [&](int n, long long* d) { k_row3<2, 1><<<1, 32>>>(buf, n, d); }, n, 1);
+    run("row3 C=2 H=2", [&](int n, long long* d) { k_row3<2, 2><<<1, 32>>>(buf, n, d); }, n, 1);
+    run("row3 C=4 H=1", [&](int n, long long* d) { k_row3<4, 1><<<1, 32>>>(buf, n, d); }, n, 1);
+    run("row3 C=4 H=2", [&](int n, long long* d) { k_row3<4, 2><<<1, 32>>>(buf, n, d); }, n, 1);
+    run("row3 C=4 H=4", [&](int n, long long* d) { k_row3<4, 4><<<1, 32>>>(buf, n, d); }, n, 1);
+    run("row3 C=2 H=2 (4 warps)", [&](int n, long long* d) { k_row3<2, 2><<<1, 128>>>(buf, n, d); }, n, 1);
+    run("row3 C=4 H=2 (4 warps)", [&](int n, long long* d) { k_row3<4, 2><<<1, 128>>>(buf, n, d); }, n, 1);
+    printf("status %s\n", cudaGetErrorString(cudaGetLastError()));
+    return 0;
+}
+
+int main() { main1(); main2(); return main3(); }
