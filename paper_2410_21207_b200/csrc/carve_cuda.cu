@@ -288,6 +288,7 @@ struct Dp2Plan {
     const Dp2Variant* v;
     int ncl, nblk;
     size_t smem;
+    int gather;  // label table gathered into CTA 0 (fits in shared memory)
 };
 
 int env_int(const char* name, int dflt) {
@@ -315,7 +316,11 @@ Dp2Plan dp2_plan(int W, int H, bool batch = false) {
             if (ncl > (pass == 0 ? max_ncl : 16) || smem > size_t(kDpSmemBudget)) continue;
             // columns read past the image edge must stay inside the +inf pad
             if (ncl * v.cols() - W + v.K + 32 * v.C > EPAD_R) continue;
-            return Dp2Plan{&v, ncl, nblk, smem};
+            // gather the block-end labels into CTA 0 when the table is small
+            const size_t gbytes = round_up(size_t(nblk) * ncl * v.cols(), 16);
+            const bool gather = nblk > 0 && gbytes <= size_t(96) * 1024 && smem + gbytes <= size_t(kDpSmemBudget) &&
+                                env_int("CARVE_DP_GATHER", 1) != 0;
+            return Dp2Plan{&v, ncl, nblk, smem + (gather ? gbytes : 0), gather ? 1 : 0};
         }
     }
     fail(CARVE_E_IMAGE_TOO_LARGE, "no DP cluster configuration fits width " + std::to_string(W) + " x height " +
@@ -326,6 +331,7 @@ void launch_dp2(Ctx& c, const Dp2Plan& pl, Dp2Params p, int nimg, cudaStream_t s
     const Dp2Variant& v = *pl.v;
     p.G = pl.ncl * v.NW;
     p.nblk = pl.nblk;
+    p.gather = pl.gather;
     p.dbg = env_int("CARVE_DP_DBG", 0);
     const void* fn = fused ? v.fn_fused : p.m_out ? v.fn_tables : (p.prof ? v.fn_prof : v.fn);
     if (c.smem_set.find(fn) == c.smem_set.end()) fail(CARVE_E_CUDA, "DP kernel attributes not initialised");

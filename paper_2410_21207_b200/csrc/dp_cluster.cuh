@@ -74,6 +74,7 @@ struct Dp2Params {
     const uint32_t* rgb;   // RGBX plane (pitch rpitch), image stride rgb_istride
     int rpitch;
     long long rgb_istride;
+    int gather;  // 1: CTA 0 holds a gathered copy of every CTA's block-end labels (phase 1 stays local)
 };
 
 // smem layout (dynamic): labels int8 [nblk][NWARP*S] | mailbox | phase-2 dirs | reduce
@@ -85,7 +86,7 @@ struct Dp2Smem {
     static constexpr size_t mail_bytes = size_t(2) * NWARP * 2 * K * (8 + 4);
     static constexpr size_t p2_bytes = size_t(NWARP) * LBLK * P2_COLS;
     static constexpr size_t red_bytes = 64 * 16 + NWARP * 2 * 8;  // argmin scratch + halo mbarriers
-    static constexpr size_t ring_bytes(int D) { return size_t(NWARP) * D * 32 * C * 8; }
+    __host__ __device__ static constexpr size_t ring_bytes(int D) { return size_t(NWARP) * D * 32 * C * 8; }
     __host__ __device__ static size_t total(int nblk, int D) {
         return labels_bytes(nblk) + mail_bytes + p2_bytes + red_bytes + ring_bytes(D);
     }
@@ -520,6 +521,21 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     cp_async_wait<0>();  // the ring's trailing prefetches (rows past H-1) land before the region is reused
     long long pf_fwd = 0;
     if constexpr (PROF) pf_fwd = clock64();
+    // Small label tables are gathered into CTA 0 (plain DSMEM word stores, ordered
+    // by the cluster barrier below) so phase 1's block-to-block hops are local.
+    int8_t* gtab = reinterpret_cast<int8_t*>(reinterpret_cast<unsigned char*>(ring_s) + SM::ring_bytes(D));
+    const int GS = G * S;  // gathered row stride (bytes)
+    if (p.gather) {
+        __syncthreads();  // every warp of this CTA has stored its block-end labels
+        uint32_t* dst0 = reinterpret_cast<uint32_t*>(cluster.map_shared_rank(gtab, 0));
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(labels);
+        constexpr int WPR = SM::COLS / 4;  // words per label row of this CTA
+        for (int idx = threadIdx.x; idx < nblk * WPR; idx += NWARP * 32) {
+            const int b = idx / WPR, w = idx - b * WPR;
+            dst0[(b * GS + cta * SM::COLS) / 4 + w] = src[idx];
+        }
+    }
+
     // ---- K3a: argmin of the bottom row over useful columns (solvers.hpp:94-99)
     double bv = dinf();
     int bi = 0x7fffffff;
@@ -530,10 +546,13 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     for (int o = 16; o > 0; o >>= 1) argmin_combine(bv, bi, __shfl_xor_sync(FULL, bv, o), __shfl_xor_sync(FULL, bi, o));
     if (lane == 0) { red_v[warp] = bv; red_i[warp] = bi; }
     __syncthreads();
+    // per-CTA results go straight into CTA 0's slots (DSMEM stores, ordered by the barrier)
+    double* cl_v = red_v + 96;
+    int* cl_i = reinterpret_cast<int*>(red_v + 112);
     if (threadIdx.x == 0) {
         for (int w = 1; w < NWARP; ++w) argmin_combine(bv, bi, red_v[w], red_i[w]);
-        red_v[NWARP] = bv;  // this CTA's result
-        red_i[NWARP] = bi;
+        cluster.map_shared_rank(cl_v, 0)[cta] = bv;
+        cluster.map_shared_rank(cl_i, 0)[cta] = bi;
     }
     __threadfence();
     if (ncl > 1) cluster.sync();
@@ -541,18 +560,23 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
 
     // ---- K3b phase 1 (CTA 0, one thread): block-boundary columns through the labels
     if (cta == 0 && threadIdx.x == 0 && !(p.dbg & 2)) {
-        for (int r = 1; r < ncl; ++r) {
-            const double* rv = cluster.map_shared_rank(red_v, r);
-            const int* ri = cluster.map_shared_rank(red_i, r);
-            argmin_combine(bv, bi, rv[NWARP], ri[NWARP]);
-        }
+        bv = cl_v[0];
+        bi = cl_i[0];
+        for (int r = 1; r < ncl; ++r) argmin_combine(bv, bi, cl_v[r], cl_i[r]);
         int c = bi;
         seam[H - 1] = c;
-        for (int b = nblk - 1; b >= 0; --b) {
-            const int owner = (c / S) / NWARP;
-            const int8_t* lb = cluster.map_shared_rank(labels, owner);
-            c += lb[b * SM::COLS + (c - owner * SM::COLS)];
-            if (b > 0) seam[LBLK * b] = c;  // row 32b = last row of block b-1
+        if (p.gather) {
+            for (int b = nblk - 1; b >= 0; --b) {
+                c += gtab[b * GS + c];
+                if (b > 0) seam[LBLK * b] = c;  // row 32b = last row of block b-1
+            }
+        } else {
+            for (int b = nblk - 1; b >= 0; --b) {
+                const int owner = (c / S) / NWARP;
+                const int8_t* lb = cluster.map_shared_rank(labels, owner);
+                c += lb[b * SM::COLS + (c - owner * SM::COLS)];
+                if (b > 0) seam[LBLK * b] = c;  // row 32b = last row of block b-1
+            }
         }
         if (nblk > 0) seam[0] = c;
         __threadfence();
