@@ -432,15 +432,23 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
         (void)dbits;
         fetch(u);  // refill this stage with row i + D (own lane's bytes only: no cross-lane hazard)
     };
+    // block-end stores: shared-space label address and a running M-boundary
+    // pointer, both hoisted (the generic->shared conversion was per call)
+    const uint32_t lbl_s = smem_u32(labels + (col0 - cta_col0));
+    double* mb_row = mbound + p.mpitch + col0;  // M row 32*(blk+1), advanced per label block
     auto block_end = [&](int i, int blk) {  // last row of a label block: labels to smem, M to global
 #pragma unroll
         for (int k = 0; k < C; ++k)
-            if (useful >> k & 1) labels[blk * SM::COLS + (col0 + k - cta_col0)] = int8_t(lab[k] - (col0 + k));
+            if (useful >> k & 1)
+                asm volatile("st.shared.u8 [%0], %1;" ::"r"(lbl_s + uint32_t(blk * SM::COLS + k)),
+                             "r"(uint32_t(lab[k] - (col0 + k)))
+                             : "memory");
         if (i != H - 1) {
 #pragma unroll
             for (int k = 0; k < C; ++k)
-                if (useful >> k & 1) mbound[(long long)(blk + 1) * p.mpitch + col0 + k] = m[k];
+                if (useful >> k & 1) mb_row[k] = m[k];
         }
+        mb_row += p.mpitch;
     };
     auto reset_labels = [&]() {
 #pragma unroll
@@ -448,21 +456,37 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     };
     int par = 0;
     uint32_t phases = 0;  // bit p: phase parity of my mbarrier for mailbox parity p
+    // Per-lane exchange roles, hoisted out of the row loop. C divides K, so a
+    // lane's C columns are either all halo, all edge-of-segment, or neither.
+    const int wi0 = lane * C;  // my first column's index within the warp's 32*C
+    const bool sendL = gl >= 0 && wi0 >= K && wi0 < 2 * K;
+    const bool sendR = gr < G && wi0 >= 32 * C - 2 * K && wi0 < 32 * C - K;
+    const bool recvL = lane < KL, recvR = lane >= 32 - KL;
+    const uint32_t aLm = nl_m + uint32_t(wi0 - K) * 8, aLl = nl_l + uint32_t(wi0 - K) * 4;
+    const uint32_t aRm = nr_m + uint32_t(wi0 - (32 * C - 2 * K)) * 8, aRl = nr_l + uint32_t(wi0 - (32 * C - 2 * K)) * 4;
+    const double* rLm = my_m + wi0;                       // side 0 (+ parity*PSTRIDE)
+    const int* rLl = my_l + wi0;
+    const double* rRm = my_m + K + (wi0 - (32 * C - K));  // side 1
+    const int* rRl = my_l + K + (wi0 - (32 * C - K));
     auto exchange = [&]() {
         // send my K leftmost / rightmost useful columns straight into the
         // neighbours' halo mailboxes; each store completes bytes on the
         // neighbour's mbarrier (no cluster-wide barrier, no memory fence)
-        const uint32_t mo = uint32_t(par * PSTRIDE);
+        const uint32_t po8 = uint32_t(par * PSTRIDE * 8), po4 = uint32_t(par * PSTRIDE * 4);
+        if (sendL) {
+            const uint32_t mb = nl_b + par * 8;
 #pragma unroll
-        for (int k = 0; k < C; ++k) {
-            const int wi = lane * C + k;
-            if (wi >= K && wi < 2 * K && gl >= 0) {
-                st_async_b64(nl_m + (mo + wi - K) * 8, m[k], nl_b + par * 8);
-                st_async_b32(nl_l + (mo + wi - K) * 4, uint32_t(lab[k]), nl_b + par * 8);
+            for (int k = 0; k < C; ++k) {
+                st_async_b64(aLm + po8 + k * 8, m[k], mb);
+                st_async_b32(aLl + po4 + k * 4, uint32_t(lab[k]), mb);
             }
-            if (wi >= 32 * C - 2 * K && wi < 32 * C - K && gr < G) {
-                st_async_b64(nr_m + (mo + wi - (32 * C - 2 * K)) * 8, m[k], nr_b + par * 8);
-                st_async_b32(nr_l + (mo + wi - (32 * C - 2 * K)) * 4, uint32_t(lab[k]), nr_b + par * 8);
+        }
+        if (sendR) {
+            const uint32_t mb = nr_b + par * 8;
+#pragma unroll
+            for (int k = 0; k < C; ++k) {
+                st_async_b64(aRm + po8 + k * 8, m[k], mb);
+                st_async_b32(aRl + po4 + k * 4, uint32_t(lab[k]), mb);
             }
         }
         // wait until both neighbours' halos for this parity have landed here
@@ -473,20 +497,18 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
         }
         if constexpr (PROF) pf_wait += clock64() - w0;
         phases ^= 1u << par;
-        if (lane < KL) {
+        if (recvL) {
 #pragma unroll
             for (int k = 0; k < C; ++k) {
-                const int wi = lane * C + k;
-                m[k] = gl >= 0 ? my_m[par * PSTRIDE + wi] : dinf();
-                lab[k] = gl >= 0 ? my_l[par * PSTRIDE + wi] : 0;
+                m[k] = gl >= 0 ? rLm[par * PSTRIDE + k] : dinf();
+                lab[k] = rLl[par * PSTRIDE + k];
             }
         }
-        if (lane >= 32 - KL) {
+        if (recvR) {
 #pragma unroll
             for (int k = 0; k < C; ++k) {
-                const int wi = lane * C + k - (32 * C - K);
-                m[k] = gr < G ? my_m[par * PSTRIDE + K + wi] : dinf();
-                lab[k] = gr < G ? my_l[par * PSTRIDE + K + wi] : 0;
+                m[k] = gr < G ? rRm[par * PSTRIDE + k] : dinf();
+                lab[k] = rRl[par * PSTRIDE + k];
             }
         }
         par ^= 1;
