@@ -308,8 +308,11 @@ Dp2Plan dp2_plan(int W, int H, bool batch = false) {
     const int forced = env_int("CARVE_DP_VARIANT", -1);
     const int max_ncl = env_int("CARVE_DP_MAX_NCL", 16);
     for (int pass = 0; pass < 2; ++pass) {
-        for (int k : batch ? kDp2BatchOrder : kDp2Order) {
-            if (forced >= 0 && k != forced) continue;
+        std::vector<int> order;
+        if (forced >= 0 && forced < kNumDp2Variants) order.push_back(forced);
+        else if (batch) order.assign(std::begin(kDp2BatchOrder), std::end(kDp2BatchOrder));
+        else order.assign(std::begin(kDp2Order), std::end(kDp2Order));
+        for (int k : order) {
             const Dp2Variant& v = kDp2Variants[k];
             const int ncl = (W + v.cols() - 1) / v.cols();
             const size_t smem = v.smem(nblk, v.D);
@@ -366,7 +369,8 @@ void launch_compact_inplace(const CompactParams& p, int nimg, cudaStream_t s) {
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = pdl_enabled() ? 1 : 0;
-        ck(cudaLaunchKernelEx(&cfg, k_compact_warp<4>, p), "launch k_compact_warp");
+        if (p.e_out) ck(cudaLaunchKernelEx(&cfg, k_compact_warp<4, true>, p), "launch k_compact_warp");
+        else ck(cudaLaunchKernelEx(&cfg, k_compact_warp<4, false>, p), "launch k_compact_warp");
         LAUNCHED("k_compact_warp");
         return;
     }

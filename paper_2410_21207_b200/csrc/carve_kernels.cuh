@@ -543,7 +543,11 @@ __global__ void k_compact_transpose(const uint32_t* __restrict__ in, int ipitch,
 // before its stores, and batch b+1's loads only touch elements at or beyond
 // the last element batch b read, so the left shift is race-free in program
 // order without any CTA barrier. Rows are independent.
-template <int NB>
+// HAS_E: the FP64 energy plane moves too (single-image mode); without it the
+// kernel stays small enough for full occupancy (batches, RGBX only). The RGBX
+// replica columns -1 / W-1 the fused DP reads are written by the lanes that
+// store columns 0 / Wn-1 (no extra dependent load at the end of the row).
+template <int NB, bool HAS_E>
 __global__ void __launch_bounds__(256) k_compact_warp(CompactParams p) {
     const int img = blockIdx.y;
     const int lane = threadIdx.x & 31;
@@ -556,12 +560,13 @@ __global__ void __launch_bounds__(256) k_compact_warp(CompactParams p) {
         const int W = p.W, Wn = W - 1;
         const int s = __ldg(p.seam + img * p.s_istride + i);
         uint32_t* rgb = p.rgb_out + img * p.p_istride + (long long)i * p.pitch;
-        double* e = p.e_out ? p.e_out + img * p.e_istride + (long long)i * p.epitch : nullptr;
+        double* e = HAS_E ? p.e_out + img * p.e_istride + (long long)i * p.epitch : nullptr;
+        const bool edges = p.rgb_edges;
         // first 4-aligned chunk that changes
         const int q0 = (s >> 2);
         for (int qb = q0; qb * 4 < Wn; qb += 32 * NB) {
             uint32_t o[NB][4];
-            double oe[NB][4];
+            double oe[HAS_E ? NB : 1][4];
 #pragma unroll
             for (int u = 0; u < NB; ++u) {
                 const int base = (qb + u * 32 + lane) * 4;
@@ -570,7 +575,7 @@ __global__ void __launch_bounds__(256) k_compact_warp(CompactParams p) {
                     const uint32_t a[5] = {v.x, v.y, v.z, v.w, base + 4 < W ? rgb[base + 4] : 0u};
 #pragma unroll
                     for (int t = 0; t < 4; ++t) o[u][t] = (base + t >= s) ? a[t + 1] : a[t];
-                    if (e) {
+                    if constexpr (HAS_E) {
                         const double2 v0 = *reinterpret_cast<const double2*>(e + base);
                         const double2 v1 = *reinterpret_cast<const double2*>(e + base + 2);
                         const double b[5] = {v0.x, v0.y, v1.x, v1.y, base + 4 < W ? e[base + 4] : 0.0};
@@ -585,7 +590,7 @@ __global__ void __launch_bounds__(256) k_compact_warp(CompactParams p) {
                 const int base = (qb + u * 32 + lane) * 4;
                 if (base + 4 <= Wn) {
                     *reinterpret_cast<uint4*>(rgb + base) = make_uint4(o[u][0], o[u][1], o[u][2], o[u][3]);
-                    if (e) {
+                    if constexpr (HAS_E) {
                         *reinterpret_cast<double2*>(e + base) = make_double2(oe[u][0], oe[u][1]);
                         *reinterpret_cast<double2*>(e + base + 2) = make_double2(oe[u][2], oe[u][3]);
                     }
@@ -594,18 +599,22 @@ __global__ void __launch_bounds__(256) k_compact_warp(CompactParams p) {
                     for (int t = 0; t < 4; ++t)
                         if (base + t < Wn) {
                             rgb[base + t] = o[u][t];
-                            if (e) e[base + t] = oe[u][t];
+                            if constexpr (HAS_E) e[base + t] = oe[u][t];
                         }
+                }
+                if (edges && base < Wn) {  // replica columns (raster.hpp:54-58 clamping)
+                    if (base == 0 && s == 0) rgb[-1] = o[u][0];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        if (base + t == Wn - 1) rgb[Wn] = o[u][t];
                 }
             }
             __syncwarp();  // this batch's stores precede the next batch's loads
         }
-        if (lane == 0) {
-            if (e) e[Wn] = dinf();  // the vacated column joins the +inf pad
-            if (p.rgb_edges) {      // replica columns for the fused DP (raster.hpp:54-58)
-                rgb[-1] = rgb[0];
-                rgb[Wn] = rgb[Wn - 1];
-            }
+        // seam in the row's last chunk: nothing moved, but the right replica follows column Wn-1
+        if (edges && lane == 0 && q0 * 4 >= Wn) rgb[Wn] = rgb[Wn - 1];
+        if constexpr (HAS_E) {
+            if (lane == 0) e[Wn] = dinf();  // the vacated column joins the +inf pad
         }
     }
     if (p.stamps && threadIdx.x == 0) atomicMax(&p.stamps[img * p.st_istride + 1], (unsigned long long)globaltimer());
