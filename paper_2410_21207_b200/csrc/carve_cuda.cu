@@ -209,11 +209,33 @@ void launch_transpose(const uint32_t* in, int ipitch, int W, int H, uint32_t* ou
     LAUNCHED("k_transpose");
 }
 
+int env_int(const char* name, int dflt);
+
 void launch_energy(const uint32_t* rgb, int pitch, int W, int H, double* e, int epitch, int nimg, long long rgb_is,
                    long long e_is, cudaStream_t s) {
-    dim3 grid((W + K1_TW - 1) / K1_TW, (H + K1_TH - 1) / K1_TH, nimg);
-    k_energy_full<<<grid, 256, 0, s>>>(rgb, pitch, W, H, e, epitch, rgb_is, e_is);
-    LAUNCHED("k_energy_full");
+    if (env_int("CARVE_K1", 1) == 0) {  // shared-memory tile version (kept for A/B)
+        dim3 grid((W + K1_TW - 1) / K1_TW, (H + K1_TH - 1) / K1_TH, nimg);
+        k_energy_full<<<grid, 256, 0, s>>>(rgb, pitch, W, H, e, epitch, rgb_is, e_is);
+        LAUNCHED("k_energy_full");
+        return;
+    }
+    // Rows per warp: one full wave of resident warps over the whole job (no
+    // partial second wave), runs of at least 4 rows (vertical halo <= 50%).
+    static const long long resident_warps = [] {
+        int dev = 0, nsm = 0, per_sm = 0;
+        ck(cudaGetDevice(&dev), "cudaGetDevice");
+        ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "SM count");
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_energy_rows<1, 2>, 256, 0), "K1 occupancy");
+        return (long long)nsm * std::max(per_sm, 1) * 8;
+    }();
+    const int nstrips = (W + K1S_COLS - 1) / K1S_COLS;
+    const long long units = (long long)nstrips * H * nimg;  // warp-rows of work
+    int R = int(std::max<long long>(4, (units + resident_warps - 1) / resident_warps));
+    R = (R + 1) & ~1;
+    const long long warps = (long long)nstrips * ((H + R - 1) / R);
+    dim3 grid(unsigned((warps + 7) / 8), nimg);
+    k_energy_rows<1, 2><<<grid, 256, 0, s>>>(rgb, pitch, W, H, e, epitch, rgb_is, e_is, nstrips, R);
+    LAUNCHED("k_energy_rows");
 }
 
 void launch_fill_pads(double* e, int epitch, int W, int H, int nimg, long long e_is, cudaStream_t s) {

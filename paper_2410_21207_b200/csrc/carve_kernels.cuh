@@ -186,6 +186,98 @@ __global__ void __launch_bounds__(256) k_energy_full(const uint32_t* __restrict_
     k1_tile(rgb, pitch, W, H, e, epitch, blockIdx.y * K1_TH, blockIdx.x * K1_TW, L);
 }
 
+// K1, row-streaming form (the default): one warp owns a 128-column strip
+// (4 columns per lane) for a run of R rows. RGBX rows stream through registers
+// two rows ahead, the three luma rows (i-1, i, i+1) roll in registers, lane
+// neighbours come by shuffle and the strip's outer neighbours from one extra
+// pixel loaded by lanes 0 and 31, so every pixel's luma is computed about
+// once and there is no shared memory or barrier. Clamping follows at_clamped
+// (raster.hpp:54-58): rows outside [0, H) and columns outside [0, W) read the
+// nearest edge. Loads never leave [0, W) x [0, H), so unpadded planes work.
+constexpr int K1S_C = 4, K1S_COLS = 32 * K1S_C;
+template <int MINB, int PF>
+__global__ void __launch_bounds__(256, MINB) k_energy_rows(const uint32_t* __restrict__ rgb, int pitch, int W, int H,
+                                                     double* __restrict__ e, int epitch, long long rgb_istride,
+                                                     long long e_istride, int nstrips, int R) {
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int strip = gw % nstrips, i0 = (gw / nstrips) * R;
+    if (i0 >= H) return;
+    rgb += blockIdx.y * rgb_istride;
+    e += blockIdx.y * e_istride;
+    const int s0 = strip * K1S_COLS, col0 = s0 + lane * K1S_C;
+    const bool vec = col0 + K1S_C <= W;
+    uint32_t lcl = 0, rcl = 0, live = 0;
+#pragma unroll
+    for (int k = 0; k < K1S_C; ++k) {
+        if (col0 + k == 0) lcl |= 1u << k;
+        if (col0 + k == W - 1) rcl |= 1u << k;
+        if (col0 + k < W) live |= 1u << k;
+    }
+    // lanes 0 / 31: the column just outside the strip (clamped into the image)
+    const bool xl = lane == 0 || lane == 31;
+    const int xcol = lane == 0 ? max(s0 - 1, 0) : min(s0 + K1S_COLS, W - 1);
+    auto load = [&](int r, uint32_t (&px)[K1S_C], uint32_t& x) {
+        const uint32_t* row = rgb + (long long)min(max(r, 0), H - 1) * pitch;
+        if (vec) {
+            const uint4 v = *reinterpret_cast<const uint4*>(row + col0);
+            px[0] = v.x; px[1] = v.y; px[2] = v.z; px[3] = v.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < K1S_C; ++k) px[k] = row[min(col0 + k, W - 1)];
+        }
+        if (xl) x = row[xcol];
+    };
+    double Lp[K1S_C], Lc[K1S_C], Ln[K1S_C], xc = 0.0, xn = 0.0;
+    uint32_t pbuf[PF][K1S_C], xbuf[PF];
+    auto to_luma = [&](const uint32_t (&px)[K1S_C], uint32_t x, double (&L)[K1S_C], double& xlum) {
+#pragma unroll
+        for (int k = 0; k < K1S_C; ++k) L[k] = luma(px[k]);
+        if (xl) xlum = luma(x);
+    };
+    load(i0 - 1, pbuf[0], xbuf[0]);
+    to_luma(pbuf[0], xbuf[0], Lp, xc);
+    load(i0, pbuf[0], xbuf[0]);
+    to_luma(pbuf[0], xbuf[0], Lc, xc);
+    const int i1 = min(i0 + R, H);
+#pragma unroll
+    for (int u = 0; u < PF; ++u) load(i0 + 1 + u, pbuf[u], xbuf[u]);  // rows i+1 .. i+PF in flight at row i
+    auto row_step = [&](int i, uint32_t (&px)[K1S_C], uint32_t& x) {
+        to_luma(px, x, Ln, xn);
+        load(i + 1 + PF, px, x);  // refill this buffer (clamped past the bottom; unused there)
+        double lL = __shfl_up_sync(FULL, Lc[K1S_C - 1], 1);
+        double lR = __shfl_down_sync(FULL, Lc[0], 1);
+        if (lane == 0) lL = xc;
+        if (lane == 31) lR = xc;
+        double out[K1S_C];
+#pragma unroll
+        for (int k = 0; k < K1S_C; ++k) {
+            double left = k > 0 ? Lc[k - 1] : lL;
+            double right = k + 1 < K1S_C ? Lc[k + 1] : lR;
+            if (lcl >> k & 1) left = Lc[k];
+            if (rcl >> k & 1) right = Lc[k];
+            out[k] = e1(left, right, Lp[k], Ln[k]);
+        }
+        double* erow = e + (long long)i * epitch + col0;
+        if (live == (1u << K1S_C) - 1) {
+            *reinterpret_cast<double2*>(erow) = make_double2(out[0], out[1]);
+            *reinterpret_cast<double2*>(erow + 2) = make_double2(out[2], out[3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < K1S_C; ++k)
+                if (live >> k & 1) erow[k] = out[k];
+        }
+#pragma unroll
+        for (int k = 0; k < K1S_C; ++k) { Lp[k] = Lc[k]; Lc[k] = Ln[k]; }
+        xc = xn;
+    };
+    for (int i = i0; i < i1; i += PF) {
+#pragma unroll
+        for (int u = 0; u < PF; ++u)
+            if (i + u < i1) row_step(i + u, pbuf[u], xbuf[u]);
+    }
+}
+
 // +inf into the left/right pad columns of rows [0, H) (e points at logical column 0)
 __global__ void k_fill_pads(double* __restrict__ e, int epitch, int W, int H, long long e_istride) {
     e += blockIdx.y * e_istride;
