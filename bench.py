@@ -318,13 +318,19 @@ def measure(cfg_name, args, rk, distinct_max=None):
     # ---- end-to-end through the public host API (pinned host buffers) ---------------
     in_views = [pin_in[k].numpy() for k in range(n_local)]
     out_views = [pin_out[k].numpy() for k in range(n_local)]
-    rk.barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
+
+    def api_step():
         if batch:
             cv.carve_batch(in_views, TW, TH, devices=[local], out=out_views)
         else:
-            out_views[0][...] = cv.carve(in_views[0], TW, TH)
+            cv.carve(in_views[0], TW, TH, out=out_views[0])
+
+    for _ in range(args.warmup):  # same W untimed warm-up steps as the device-resident region
+        api_step()
+    rk.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        api_step()
     e2e_s = rk.max(time.perf_counter() - t0)
     unit = "images/s" if batch else "seams/s"
     e2e = {"value": units_total * args.steps / e2e_s, "unit": unit,
@@ -347,15 +353,30 @@ def measured_traffic(kernel, cfg_name):
         return None
 
 
-def roofline_of(kern, cfg_name="c2"):
+# DP rows per launch (the DP is a row-serial chain: its real bound is latency per row)
+DP_ROWS = {"c1": 512, "c2": 1080, "c3": (768 * 2160 + 432 * 3072) / 1200, "c4": 4320, "c5": 768}
+# one warp's dependent row step (2 shuffles + 2 compare/selects + DADD), measured on B200 by
+# tools/microbench.cu (profiles/r01_microbench_latency.txt)
+CHAIN_CYCLES_PER_ROW = 59.0
+
+
+def roofline_of(kern, cfg_name="c2", sm_mhz=None):
     peak, peak_src = peaks()
     dom = max(kern, key=lambda k: kern[k]["ms_total"]) if kern else None
     if not dom:
         return None
     kd = kern[dom]
-    return {"kernel": dom, "bound": "hbm", "achieved": kd["gbs"], "peak": peak, "unit": "GB/s",
-            "frac": kd["gbs"] / peak, "traffic": measured_traffic(dom, cfg_name), "peak_source": peak_src,
-            "bytes_per_launch": kd["bytes_per_launch"], "avg_launch_us": kd["avg_us"], "share_of_step": kd["share"]}
+    r = {"kernel": dom, "bound": "hbm", "achieved": kd["gbs"], "peak": peak, "unit": "GB/s",
+         "frac": kd["gbs"] / peak, "traffic": measured_traffic(dom, cfg_name), "peak_source": peak_src,
+         "bytes_per_launch": kd["bytes_per_launch"], "avg_launch_us": kd["avg_us"], "share_of_step": kd["share"],
+         # HBM fraction of every timed kernel (algorithmic bytes / event time / peak)
+         "hbm_frac_by_kernel": {k: round(v["gbs"] / peak, 4) for k, v in kern.items()}}
+    if dom == "k_dp_seam" and cfg_name in DP_ROWS and cfg_name != "c5":
+        ns_row = kd["avg_us"] * 1e3 / DP_ROWS[cfg_name]
+        floor = CHAIN_CYCLES_PER_ROW / ((sm_mhz or 1965.0) / 1e3)
+        r["latency"] = {"note": "the DP is latency-bound (row-serial chain), not HBM-bound",
+                        "ns_per_row": ns_row, "chain_floor_ns_per_row": floor, "frac_of_chain_floor": floor / ns_row}
+    return r
 
 
 def run_ours(args, cfg_name):
@@ -379,7 +400,7 @@ def run_ours(args, cfg_name):
         "config": {"workload": m["desc"] + ("" if batch else " per GPU"), "images_per_gpu": m["n_local"],
                    "l2": "flushed between steps (256 MiB write)",
                    "parallelism": f"image-sharded x{world}, no collective"},
-        "e2e": m["e2e"], "gpu_launches": m["gpu_launches"], "roofline": roofline_of(m["kernels"], cfg_name),
+        "e2e": m["e2e"], "gpu_launches": m["gpu_launches"], "roofline": roofline_of(m["kernels"], cfg_name, (m["clocks"] or {}).get("sm_mhz")),
         "kernels": m["kernels"], "verified_vs_golden": m["verified_vs_golden"], "clocks": m["clocks"],
     }
     if not batch and not args.no_batch:
@@ -390,7 +411,7 @@ def run_ours(args, cfg_name):
                          "images_per_gpu": b["n_local"],
                          "data": f"{b['n_distinct']} distinct make_test_image variants per GPU, tiled to "
                                  f"{b['n_local']} images", "verified_vs_golden": b["verified_vs_golden"],
-                         "roofline": roofline_of(b["kernels"], "c5"), "kernels": b["kernels"],
+                         "roofline": roofline_of(b["kernels"], "c5", (b["clocks"] or {}).get("sm_mhz")), "kernels": b["kernels"],
                          "gpu_launches": b["gpu_launches"], "clocks": b["clocks"]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg_name)

@@ -361,9 +361,11 @@ def _check_config(cfg: CarveConfig | None) -> None:
 
 
 def carve(img: np.ndarray, target_width: int, target_height: int | None = None, *, seams: bool = False,
-          timings: bool = False):
+          timings: bool = False, out: np.ndarray | None = None):
     """run_resize semantics (cli.hpp:249-256): carve_to_width then carve_to_height.
-    Returns the carved image, plus (seams, timings) lists when requested."""
+    Returns the carved image, plus (seams, timings) lists when requested. `out`
+    (optional, C-contiguous uint8 target_height x target_width x 3, e.g. pinned
+    memory) receives the image instead of a fresh array."""
     a = _img(img)
     h, w, _ = a.shape
     th = h if target_height is None else int(target_height)
@@ -372,7 +374,10 @@ def carve(img: np.ndarray, target_width: int, target_height: int | None = None, 
         raise CarveError(Errc.invalid_target, "target width must be in [1, width]")
     if th < 1 or th > h:
         raise CarveError(Errc.invalid_target, "target height must be in [1, height]")
-    out = np.empty((th, tw, 3), np.uint8)
+    if out is None:
+        out = np.empty((th, tw, 3), np.uint8)
+    elif out.shape != (th, tw, 3) or out.dtype != np.uint8 or not out.flags.c_contiguous:
+        raise CarveError(Errc.usage_error, "out must be a C-contiguous uint8 array of shape (th, tw, 3)")
     n_ints = (w - tw) * h + (h - th) * tw
     nseams = (w - tw) + (h - th)
     s = np.empty(max(n_ints, 1), np.int32)

@@ -381,18 +381,25 @@ void launch_dp2(Ctx& c, const Dp2Plan& pl, Dp2Params p, int nimg, cudaStream_t s
 
 void launch_compact_inplace(const CompactParams& p, int nimg, cudaStream_t s) {
     if (env_int("CARVE_COMPACT", 2) == 2) {  // warp per row (default); 1 = CTA per row
-        constexpr int WPB = 8;
+        // warps per CTA: small CTAs spread few rows over all SMs (single images)
+        const int wpb = env_int("CARVE_COMPACT_WPB", 8);
+        const int nb = env_int("CARVE_COMPACT_NB", 4);
         cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3((p.H + WPB - 1) / WPB, nimg);
-        cfg.blockDim = dim3(WPB * 32);
+        cfg.gridDim = dim3((p.H + wpb - 1) / wpb, nimg);
+        cfg.blockDim = dim3(wpb * 32);
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = pdl_enabled() ? 1 : 0;
-        if (p.e_out) ck(cudaLaunchKernelEx(&cfg, k_compact_warp<4, true>, p), "launch k_compact_warp");
-        else ck(cudaLaunchKernelEx(&cfg, k_compact_warp<4, false>, p), "launch k_compact_warp");
+        if (p.e_out) {
+            if (nb == 8) ck(cudaLaunchKernelEx(&cfg, k_compact_warp<8, true>, p), "launch k_compact_warp");
+            else if (nb == 2) ck(cudaLaunchKernelEx(&cfg, k_compact_warp<2, true>, p), "launch k_compact_warp");
+            else ck(cudaLaunchKernelEx(&cfg, k_compact_warp<4, true>, p), "launch k_compact_warp");
+        } else {
+            ck(cudaLaunchKernelEx(&cfg, k_compact_warp<4, false>, p), "launch k_compact_warp");
+        }
         LAUNCHED("k_compact_warp");
         return;
     }
