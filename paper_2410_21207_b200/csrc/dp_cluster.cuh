@@ -31,6 +31,7 @@
 #pragma once
 #include <cooperative_groups.h>
 #include <cstdint>
+#include <type_traits>
 #include <cstdio>
 
 namespace carve_dev {
@@ -468,7 +469,8 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     const int* rLl = my_l + wi0;
     const double* rRm = my_m + K + (wi0 - (32 * C - K));  // side 1
     const int* rRl = my_l + K + (wi0 - (32 * C - K));
-    auto exchange = [&]() {
+    // exchange, split in two so the block-end bookkeeping runs under the DSMEM latency:
+    auto send = [&]() {
         // send my K leftmost / rightmost useful columns straight into the
         // neighbours' halo mailboxes; each store completes bytes on the
         // neighbour's mbarrier (no cluster-wide barrier, no memory fence)
@@ -489,6 +491,8 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
                 st_async_b32(aRl + po4 + k * 4, uint32_t(lab[k]), mb);
             }
         }
+    };
+    auto recv = [&]() {
         // wait until both neighbours' halos for this parity have landed here
         if (lane == 0) mbar_arrive_expect_tx(my_b + par * 8, halo_tx);
         long long w0 = 0;
@@ -514,17 +518,39 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
         par ^= 1;
     };
 
-    static_assert(LBLK % K == 0 && K % D == 0, "K-blocks tile label blocks; the ring tiles K-blocks");
+    static_assert(LBLK % K == 0 && (D <= K ? K % D == 0 : D % K == 0),
+                  "K-blocks tile label blocks; ring and K-blocks tile each other");
+    // a ring deeper than a K-block (D = QB*K) cycles through QB block positions;
+    // each gets its own unrolled body so ring slots stay compile-time offsets
+    constexpr int QB = D > K ? D / K : 1;
+    auto kblock = [&](auto qq, int i0) {
+#pragma unroll
+        for (int t = 0; t < K; ++t) step((decltype(qq)::value * K + t) % D, i0 + t);
+    };
     const int nkb = (H - 1) / K;  // full K-row blocks
     for (int q = 0; q < nkb; ++q) {
         const int i0 = 1 + q * K;
         const int lpos = (q * K) % LBLK, blk = (q * K) / LBLK;
         if (lpos == 0) reset_labels();
-#pragma unroll
-        for (int t = 0; t < K; ++t) step(t % D, i0 + t);
-        // K divides LBLK, so label blocks end only on a K-block's last row
+        if constexpr (QB == 1) kblock(std::integral_constant<int, 0>{}, i0);
+        else if constexpr (QB == 2) {
+            if (q & 1) kblock(std::integral_constant<int, 1>{}, i0);
+            else kblock(std::integral_constant<int, 0>{}, i0);
+        } else {
+            static_assert(QB == 4, "ring depth must be K, 2K or 4K when deeper than a K-block");
+            switch (q & 3) {
+                case 0: kblock(std::integral_constant<int, 0>{}, i0); break;
+                case 1: kblock(std::integral_constant<int, 1>{}, i0); break;
+                case 2: kblock(std::integral_constant<int, 2>{}, i0); break;
+                default: kblock(std::integral_constant<int, 3>{}, i0); break;
+            }
+        }
+        // K divides LBLK, so label blocks end only on a K-block's last row. The halo
+        // lanes that recv() overwrites are never useful, so block_end may run in between.
+        const bool more = i0 + K < H;
+        if (more) send();
         if (lpos + K == LBLK || i0 + K - 1 == H - 1) block_end(i0 + K - 1, blk);
-        if (i0 + K < H) exchange();
+        if (more) recv();
     }
     {  // tail: the last (H-1) % K rows
         const int i0 = 1 + nkb * K;
@@ -534,7 +560,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
 #pragma unroll
             for (int t = 0; t < K; ++t) {
                 if (i0 + t >= H) break;
-                step(t % D, i0 + t);
+                step(((nkb % QB) * K + t) % D, i0 + t);
             }
             block_end(H - 1, blk);  // the tail always ends the image (and its label block)
         }
