@@ -5,6 +5,7 @@
 // per-seam timings come from device %globaltimer stamps.
 #pragma once
 
+#include <algorithm>
 #include <chrono>
 #include <utility>
 #include <vector>
@@ -115,14 +116,63 @@ inline std::vector<PixelGrid> carve_batch(const std::vector<PixelGrid>& imgs, in
     return outs;
 }
 
+/// carver.hpp:137-140: one pixel per row right of the seam, the rounded mean of
+/// its left and right neighbours (duplicating at the right border).
+inline PixelGrid insert_seam(const PixelGrid& grid, const Seam& seam) {
+    validate_seam(seam, grid.width, grid.height);
+    PixelGrid out(grid.width + 1, grid.height);
+    detail::check(carve_cuda_insert_seam_rgb(grid.bytes(), grid.width, grid.height, seam.data(), int(seam.size()),
+                                             out.bytes()));
+    return out;
+}
+
+/// carver.hpp:226-262: the removal loop on the device; seams reported in
+/// original-image coordinates.
+inline std::pair<std::vector<Seam>, CarveReport> record_seams(const PixelGrid& grid, int count,
+                                                              const CarveConfig& cfg = {}) {
+    if (count < 0 || count > grid.width - 1) fail(Errc::invalid_target, "cannot record more seams than width-1");
+    detail::check_config(cfg);
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<int32_t> flat(size_t(count) * grid.height);
+    std::vector<carve_seam_timing> tim(size_t(std::max(count, 1)));
+    detail::check(carve_cuda_record_seams(grid.bytes(), grid.width, grid.height, count, flat.data(), tim.data()));
+    std::vector<Seam> seams;
+    CarveReport rep;
+    for (int t = 0; t < count; ++t) {
+        seams.emplace_back(flat.begin() + size_t(t) * grid.height, flat.begin() + size_t(t + 1) * grid.height);
+        rep.per_seam.push_back({tim[t].energy_s, tim[t].solve_s, tim[t].remove_s});
+    }
+    rep.seam_count = count;
+    rep.seams = seams;
+    rep.total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return {std::move(seams), std::move(rep)};
+}
+
+/// carver.hpp:266-285: record target_width - width seams, then insert them
+/// (one device expansion pass, identical to the reference's ordered replay).
+inline std::pair<PixelGrid, CarveReport> enlarge_to_width(const PixelGrid& grid, int target_width,
+                                                          const CarveConfig& cfg = {}) {
+    const int k = target_width - grid.width;
+    if (k < 0) fail(Errc::invalid_target, "enlargement target is below the current width");
+    if (target_width > 2 * grid.width - 1)
+        fail(Errc::target_too_large, "single-pass enlargement is limited to 2*width-1");
+    detail::check_config(cfg);
+    const auto t0 = std::chrono::steady_clock::now();
+    PixelGrid out(target_width, grid.height);
+    std::vector<int32_t> flat(std::max<size_t>(size_t(k) * grid.height, 1));
+    detail::check(carve_cuda_enlarge(grid.bytes(), grid.width, grid.height, target_width, grid.height, out.bytes(),
+                                     flat.data()));
+    CarveReport rep;
+    for (int t = 0; t < k; ++t) {
+        rep.seams.emplace_back(flat.begin() + size_t(t) * grid.height, flat.begin() + size_t(t + 1) * grid.height);
+        rep.per_seam.push_back({0.0, 0.0, 0.0});
+    }
+    rep.seam_count = k;
+    rep.total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return {std::move(out), std::move(rep)};
+}
+
 // Paper-comparison / non-hot-path pipelines keep their declarations.
-inline PixelGrid insert_seam(const PixelGrid&, const Seam&) { detail::unsupported("insert_seam"); }
-inline std::pair<std::vector<Seam>, CarveReport> record_seams(const PixelGrid&, int, const CarveConfig& = {}) {
-    detail::unsupported("record_seams");
-}
-inline std::pair<PixelGrid, CarveReport> enlarge_to_width(const PixelGrid&, int, const CarveConfig& = {}) {
-    detail::unsupported("enlarge_to_width");
-}
 inline std::pair<PixelGrid, CarveReport> remove_object(const PixelGrid&, const RemovalMask&, const CarveConfig& = {},
                                                        bool = true) {
     detail::unsupported("remove_object");

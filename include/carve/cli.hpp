@@ -1,7 +1,10 @@
-// carve/cli.hpp — drop-in for the reference CLI's `resize` path
-// (/root/reference/proj/include/carve/cli.hpp:146-259, 368-379) without CLI11:
-//   carve resize --input X --output Y [--scale S | --width W] [--height H]
-//                [--solver dp|pardp] [--energy e1] [--forward]
+// carve/cli.hpp — drop-in for the reference CLI's `resize`, `enlarge` and
+// `seams` paths (/root/reference/proj/include/carve/cli.hpp:146-309, 368-379)
+// without CLI11:
+//   carve resize  --input X --output Y [--scale S | --width W] [--height H]
+//                 [--solver dp|pardp] [--energy e1] [--forward]
+//   carve enlarge --input X --output Y [--scale S | --width W] [--height H] [solver flags]
+//   carve seams   --input X --output Y --count N [solver flags]
 // Exit codes as the reference: 0 success, 1 usage error, 2 runtime error.
 // CARVE_WORKERS is validated like the reference (cli.hpp:109-126) but never
 // changes output. Other subcommands report usage_error (not on the B200 path).
@@ -24,7 +27,10 @@ struct ResizeCmd {
     std::optional<int> width, height;
     std::string solver = "pardp", energy = "e1";
     bool forward = false;
+    int count = 0;  // seams --count
 };
+using EnlargeCmd = ResizeCmd;  // same options (cli.hpp:34-39, 167-175)
+struct SeamsCmd : ResizeCmd {};  // --input --output --count + solver flags (cli.hpp:52-56, 189-193)
 
 namespace detail {
 
@@ -75,23 +81,32 @@ inline ResizeCmd parse_resize(const std::vector<std::string>& a) {
             if (c.energy != "e1" && c.energy != "e2" && c.energy != "hog" && c.energy != "entropy")
                 fail(Errc::usage_error, "--energy: unknown function " + c.energy);
         } else if (f == "--forward") c.forward = true;
+        else if (f == "--count" && a[0] == "seams") c.count = detail::parse_positive(f, val());
         else fail(Errc::usage_error, "unknown option " + f);
     }
     if (c.input.empty() || c.output.empty()) fail(Errc::usage_error, "--input and --output are required");
     if (c.scale && c.width) fail(Errc::usage_error, "--scale excludes --width");
+    if (a[0] == "seams" && (c.scale || c.width || c.height)) fail(Errc::usage_error, "seams takes --count, not a size");
+    if (a[0] == "seams" && c.count < 1) fail(Errc::usage_error, "--count is required");
     return c;
 }
 
-/// cli.hpp:242-259 run_resize: carve_to_width then carve_to_height, in one device-resident carve.
-inline int run_resize(const ResizeCmd& cmd) {
-    detail::check_env_workers();
-    PixelGrid img = load_image(cmd.input);
+namespace detail {
+inline CarveConfig config_of(const ResizeCmd& cmd) {
     CarveConfig cfg;
     cfg.solver = *parse_solver(cmd.solver);
     cfg.energy_fn = cmd.energy == "e1" ? EnergyFn::e1 : cmd.energy == "e2" ? EnergyFn::e2
                   : cmd.energy == "hog" ? EnergyFn::hog : EnergyFn::entropy;
     cfg.forward = cmd.forward;
-    ::carve::detail::check_config(cfg);
+    return cfg;
+}
+} // namespace detail
+
+/// cli.hpp:242-259 run_resize: carve_to_width then carve_to_height, in one device-resident carve.
+inline int run_resize(const ResizeCmd& cmd) {
+    detail::check_env_workers();
+    PixelGrid img = load_image(cmd.input);
+    ::carve::detail::check_config(detail::config_of(cmd));
     const int tw = cmd.scale ? int(std::lround(*cmd.scale * img.width)) : cmd.width.value_or(img.width);
     const int th = cmd.height.value_or(img.height);
     if (tw > img.width) fail(Errc::invalid_target, "resize cannot grow the width; use the enlarge command");
@@ -102,16 +117,51 @@ inline int run_resize(const ResizeCmd& cmd) {
     return 0;
 }
 
+/// cli.hpp:262-277 run_enlarge: enlarge_to_width, then enlarge_to_width of the
+/// transpose for the height — both phases in one device-resident call.
+inline int run_enlarge(const EnlargeCmd& cmd) {
+    detail::check_env_workers();
+    PixelGrid img = load_image(cmd.input);
+    ::carve::detail::check_config(detail::config_of(cmd));
+    const int tw = cmd.scale ? int(std::lround(*cmd.scale * img.width)) : cmd.width.value_or(img.width);
+    const int th = cmd.height.value_or(img.height);
+    PixelGrid out(tw, th);
+    ::carve::detail::check(carve_cuda_enlarge(img.bytes(), img.width, img.height, tw, th, out.bytes(), nullptr));
+    save_image(out, cmd.output);
+    return 0;
+}
+
+/// cli.hpp:301-309 run_seams: record the next --count seams and paint them red
+/// on the original image.
+inline int run_seams(const SeamsCmd& cmd) {
+    detail::check_env_workers();
+    PixelGrid img = load_image(cmd.input);
+    auto [recorded, report] = record_seams(img, cmd.count, detail::config_of(cmd));
+    for (const Seam& seam : recorded)
+        for (size_t i = 0; i < seam.size(); ++i) img.at(int(i), seam[i]) = Rgb{255, 0, 0};
+    save_image(img, cmd.output);
+    return 0;
+}
+
 inline int cli_main(int argc, char** argv) {
     try {
         const std::vector<std::string> args(argv + 1, argv + argc);
         if (args.empty() || args[0] == "--help" || args[0] == "-h") {
-            std::printf("usage: carve resize --input X --output Y [--scale S | --width W] [--height H]\n"
-                        "                    [--solver dp|pardp] [--energy e1]\n");
+            std::printf("usage: carve resize  --input X --output Y [--scale S | --width W] [--height H]\n"
+                        "                     [--solver dp|pardp] [--energy e1]\n"
+                        "       carve enlarge --input X --output Y [--scale S | --width W] [--height H]\n"
+                        "       carve seams   --input X --output Y --count N\n");
             return args.empty() ? 1 : 0;
         }
         if (args[0] == "resize") return run_resize(parse_resize(args));
-        fail(Errc::usage_error, "subcommand '" + args[0] + "' is not supported by the B200 engine (resize only)");
+        if (args[0] == "enlarge") return run_enlarge(parse_resize(args));
+        if (args[0] == "seams") {
+            SeamsCmd c;
+            static_cast<ResizeCmd&>(c) = parse_resize(args);
+            return run_seams(c);
+        }
+        fail(Errc::usage_error,
+             "subcommand '" + args[0] + "' is not supported by the B200 engine (resize, enlarge, seams)");
     } catch (const Error& err) {
         std::fprintf(stderr, "carve: %s\n", err.what());
         return err.code() == Errc::usage_error ? 1 : 2;

@@ -109,6 +109,24 @@ carve_status carve_cuda_dp_profile(const double* e, int w, int h, long long* cou
 /* replaces validate_seam (solvers.hpp:69-78); pure host check */
 carve_status carve_cuda_validate_seam(const int32_t* seam, int n, int w, int h);
 
+/* ---- seam recording and enlargement (carver.hpp:114-140, 226-285; cli.hpp:262-277, 301-309) */
+/* replaces insert_seam (carver.hpp:137-140: validate_seam + detail::insert_columns
+ * :117-130); out is (w+1)*h*3 bytes */
+carve_status carve_cuda_insert_seam_rgb(const uint8_t* rgb, int w, int h, const int32_t* seam, int n,
+                                        uint8_t* out);
+/* replaces record_seams (carver.hpp:226-262) with the default CarveConfig:
+ * seams_out receives count*h ints, seam t's column of row i at [t*h + i], in
+ * original-image coordinates. timings_out (nullable): count entries. */
+carve_status carve_cuda_record_seams(const uint8_t* rgb, int w, int h, int count, int32_t* seams_out,
+                                     carve_seam_timing* timings_out);
+/* replaces run_enlarge (cli.hpp:262-277): enlarge_to_width(target_w)
+ * (carver.hpp:266-285) if target_w != w, then enlarge_to_width of the
+ * transpose to target_h if target_h != h. rgb_out: target_w*target_h*3 bytes.
+ * seams_out (nullable): (target_w-w)*h + (target_h-h)*target_w ints — each
+ * phase's recorded seams (its CarveReport.seams), concatenated. */
+carve_status carve_cuda_enlarge(const uint8_t* rgb, int w, int h, int target_w, int target_h, uint8_t* rgb_out,
+                                int32_t* seams_out);
+
 /* ---- pipelines (carver.hpp:71-82, 191-222; cli.hpp:242-259) ----------- */
 /* replaces remove_seam(PixelGrid) (carver.hpp:71-82); out is (w-1)*h*3 bytes */
 carve_status carve_cuda_remove_seam_rgb(const uint8_t* rgb, int w, int h, const int32_t* seam, int n,

@@ -87,6 +87,35 @@ class _Checker:
         return out
 
 
+    def insert_seam(self, img: np.ndarray, seam) -> np.ndarray:
+        """carver.hpp:137-140"""
+        h, w, _ = img.shape
+        s = np.ascontiguousarray(seam, np.int32)
+        out = np.empty((h, w + 1, 3), np.uint8)
+        self._check(self._fn("insert_seam", _u8p, C.c_int, C.c_int, _i4p, C.c_int, _u8p)(
+            np.ascontiguousarray(img), w, h, s, len(s), out))
+        return out
+
+    def record_seams(self, img: np.ndarray, count: int) -> np.ndarray:
+        """carver.hpp:226-262: (count, h) original-coordinate columns."""
+        h, w, _ = img.shape
+        out = np.empty((max(count, 0), h), np.int32)
+        self._check(self._fn("record_seams", _u8p, C.c_int, C.c_int, C.c_int, C.c_void_p)(
+            np.ascontiguousarray(img), w, h, count, out.ctypes.data))
+        return out
+
+    def enlarge(self, img: np.ndarray, target_w: int, target_h: int | None = None, seams: bool = False):
+        """run_enlarge (cli.hpp:262-277): enlarge_to_width on the width, then on the transpose."""
+        h, w, _ = img.shape
+        th = h if target_h is None else target_h
+        out = np.empty((th, target_w, 3), np.uint8)
+        n = max(target_w - w, 0) * h + max(th - h, 0) * target_w
+        s = np.empty(max(n, 1), np.int32)
+        f = self._fn("enlarge", _u8p, C.c_int, C.c_int, C.c_int, C.c_int, _u8p, C.c_void_p)
+        self._check(f(np.ascontiguousarray(img), w, h, target_w, th, out, s.ctypes.data))
+        return (out, s[:n]) if seams else out
+
+
 class Port(_Checker):
     """The C restatement (carve_oracle.c)."""
 

@@ -27,6 +27,7 @@ enum {
     OR_EMPTY_IMAGE = 1 + 7,
     OR_WIDTH_TOO_SMALL = 1 + 8,
     OR_INVALID_TARGET = 1 + 9,
+    OR_TARGET_TOO_LARGE = 1 + 10,
     OR_NO_MEMORY = 100,
 };
 
@@ -210,6 +211,127 @@ int or_carve(const uint8_t* rgb, int w, int h, int target_w, int target_h, uint8
         st = carve_width_inplace(t, h, cw, target_h, &cursor);
         or_transpose(t, target_h, cw, work);
         free(t);
+    }
+    if (!st) memcpy(out, work, (size_t)cw * target_h * 3);
+    free(work);
+    return st;
+}
+
+/* carver.hpp:117-130 detail::insert_columns: one pixel per row right of
+ * column cols[i] (stride `cs` between rows' entries), the channel-wise rounded
+ * mean of its left and right neighbours, the right one clamped at the border. */
+static void insert_columns(const uint8_t* in, int w, int h, const int* cols, size_t cs, uint8_t* out) {
+    for (int i = 0; i < h; ++i) {
+        const int c = cols[(size_t)i * cs];
+        const uint8_t* src = in + (size_t)i * w * 3;
+        uint8_t* dst = out + (size_t)i * (w + 1) * 3;
+        memcpy(dst, src, (size_t)(c + 1) * 3);
+        const uint8_t* a = src + (size_t)c * 3;
+        const uint8_t* b = src + (size_t)(c + 1 < w ? c + 1 : w - 1) * 3;
+        for (int ch = 0; ch < 3; ++ch) dst[(size_t)(c + 1) * 3 + ch] = (uint8_t)((a[ch] + b[ch] + 1) / 2);
+        memcpy(dst + (size_t)(c + 2) * 3, src + (size_t)(c + 1) * 3, (size_t)(w - c - 1) * 3);
+    }
+}
+
+/* carver.hpp:137-140 insert_seam */
+int or_insert_seam(const uint8_t* in, int w, int h, const int* seam, int n, uint8_t* out) {
+    int st = or_validate_seam(seam, n, w, h);
+    if (st) return st;
+    insert_columns(in, w, h, seam, 1, out);
+    return OR_OK;
+}
+
+/* carver.hpp:226-262 record_seams (default config): the removal loop on a
+ * scratch copy, each seam mapped to original coordinates through per-row
+ * survivor lists (survivor[i][seam[i]], then erase). seams_out: count*h ints. */
+int or_record_seams(const uint8_t* rgb, int w, int h, int count, int* seams_out) {
+    if (w < 1 || h < 1) return OR_EMPTY_IMAGE;
+    if (count < 0 || count > w - 1) return OR_INVALID_TARGET;
+    uint8_t* work = (uint8_t*)malloc((size_t)w * h * 3);
+    int* cur = (int*)malloc(sizeof(int) * ((size_t)count * h + 1));
+    int* surv = (int*)malloc(sizeof(int) * (size_t)w * h);
+    if (!work || !cur || !surv) return OR_NO_MEMORY;
+    memcpy(work, rgb, (size_t)w * h * 3);
+    int* cursor = cur;
+    int st = carve_width_inplace(work, w, h, w - count, &cursor);
+    for (int i = 0; i < h && !st; ++i) {
+        int* row = surv + (size_t)i * w;
+        int len = w;
+        for (int j = 0; j < w; ++j) row[j] = j;
+        for (int t = 0; t < count; ++t) {
+            const int c = cur[(size_t)t * h + i];
+            seams_out[(size_t)t * h + i] = row[c];
+            memmove(row + c, row + c + 1, sizeof(int) * (size_t)(len - c - 1));
+            --len;
+        }
+    }
+    free(work);
+    free(cur);
+    free(surv);
+    return st;
+}
+
+/* carver.hpp:266-285 enlarge_to_width: record k seams, then replay them
+ * oldest-first through insert_columns, shifting every later recorded column
+ * right by one where it lands at-or-right-of the inserted column. `seams_out`
+ * (nullable) receives the recorded (unshifted) seams. */
+static int enlarge_width(const uint8_t* in, int w, int h, int target_w, uint8_t* out, int** seams_cursor) {
+    const int k = target_w - w;
+    if (k < 0) return OR_INVALID_TARGET;
+    if (target_w > 2 * w - 1) return OR_TARGET_TOO_LARGE;
+    int* seams = (int*)malloc(sizeof(int) * ((size_t)k * h + 1));
+    uint8_t* a = (uint8_t*)malloc((size_t)target_w * h * 3);
+    uint8_t* b = (uint8_t*)malloc((size_t)target_w * h * 3);
+    if (!seams || !a || !b) return OR_NO_MEMORY;
+    int st = or_record_seams(in, w, h, k, seams);
+    if (!st && seams_cursor && *seams_cursor) {
+        memcpy(*seams_cursor, seams, sizeof(int) * (size_t)k * h);
+        *seams_cursor += (size_t)k * h;
+    }
+    memcpy(a, in, (size_t)w * h * 3);
+    for (int t = 0; t < k && !st; ++t) {
+        insert_columns(a, w + t, h, seams + (size_t)t * h, 1, b);
+        memcpy(a, b, (size_t)(w + t + 1) * h * 3);
+        for (int u = t + 1; u < k; ++u)
+            for (int i = 0; i < h; ++i)
+                if (seams[(size_t)u * h + i] >= seams[(size_t)t * h + i]) ++seams[(size_t)u * h + i];
+    }
+    if (!st) memcpy(out, a, (size_t)target_w * h * 3);
+    free(seams);
+    free(a);
+    free(b);
+    return st;
+}
+
+/* run_enlarge (cli.hpp:262-277): enlarge_to_width on the width, then on the
+ * transpose for the height. */
+int or_enlarge(const uint8_t* rgb, int w, int h, int target_w, int target_h, uint8_t* out, int* seams_out) {
+    if (w < 1 || h < 1) return OR_EMPTY_IMAGE;
+    int* cursor = seams_out;
+    int cw = w, st = OR_OK;
+    uint8_t* work = (uint8_t*)malloc((size_t)(target_w > w ? target_w : w) * h * 3);
+    if (!work) return OR_NO_MEMORY;
+    if (target_w != w) {
+        st = enlarge_width(rgb, w, h, target_w, work, &cursor);
+        cw = target_w;
+    } else {
+        memcpy(work, rgb, (size_t)w * h * 3);
+    }
+    if (!st && target_h != h) {
+        const size_t big = (size_t)cw * (target_h > h ? target_h : h) * 3;
+        uint8_t* t = (uint8_t*)malloc(big);
+        uint8_t* t2 = (uint8_t*)malloc(big);
+        if (!t || !t2) return OR_NO_MEMORY;
+        or_transpose(work, cw, h, t);
+        st = enlarge_width(t, h, cw, target_h, t2, &cursor);
+        if (!st) {
+            free(work);
+            work = (uint8_t*)malloc(big);
+            if (!work) return OR_NO_MEMORY;
+            or_transpose(t2, target_h, cw, work);
+        }
+        free(t);
+        free(t2);
     }
     if (!st) memcpy(out, work, (size_t)cw * target_h * 3);
     free(work);

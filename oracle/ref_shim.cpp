@@ -179,6 +179,54 @@ int ref_carve(const std::uint8_t* rgb, int w, int h, int target_w, int target_h,
     });
 }
 
+// carver.hpp:117-140 insert_seam (validate_seam + insert_columns)
+int ref_insert_seam(const std::uint8_t* rgb, int w, int h, const int* seam, int n, std::uint8_t* out) {
+    return guarded([&] { grid_to(carve_ref::insert_seam(grid_from(rgb, w, h), carve_ref::Seam(seam, seam + n)), out); });
+}
+
+// carver.hpp:226-262 record_seams, default config: `count` seams in original
+// coordinates, concatenated (count * h ints).
+int ref_record_seams(const std::uint8_t* rgb, int w, int h, int count, int* seams_out) {
+    return guarded([&] {
+        auto [seams, report] = carve_ref::record_seams(grid_from(rgb, w, h), count, carve_ref::CarveConfig{});
+        size_t off = 0;
+        for (auto& s : seams) {
+            std::memcpy(seams_out + off, s.data(), s.size() * sizeof(int));
+            off += s.size();
+        }
+    });
+}
+
+// run_enlarge semantics (cli.hpp:262-277): enlarge_to_width (carver.hpp:266-285)
+// on the width, then on the transpose for the height. seams_out (nullable)
+// receives the recorded seams of both phases (original coordinates of the grid
+// each phase started from), concatenated.
+int ref_enlarge(const std::uint8_t* rgb, int w, int h, int target_w, int target_h, std::uint8_t* out,
+                int* seams_out) {
+    return guarded([&] {
+        carve_ref::PixelGrid img = grid_from(rgb, w, h);
+        size_t off = 0;
+        auto log = [&](const carve_ref::CarveReport& r) {
+            if (seams_out)
+                for (auto& s : r.seams) {
+                    std::memcpy(seams_out + off, s.data(), s.size() * sizeof(int));
+                    off += s.size();
+                }
+        };
+        if (target_w != img.width) {
+            auto [wider, report] = carve_ref::enlarge_to_width(img, target_w);
+            img = std::move(wider);
+            log(report);
+        }
+        if (target_h != img.height) {
+            auto [taller, report] = carve_ref::enlarge_to_width(carve_ref::transpose(img), target_h);
+            img = carve_ref::transpose(taller);
+            log(report);
+        }
+        grid_to(img, out);
+    });
+}
+
 // Batch driver for the C5 CPU baseline: the reference has no batch API but its
 // pipelines are reentrant, so `threads` host threads each run
 // carve_to_width over a static, strided share of the images.

@@ -25,6 +25,7 @@ __all__ = [
     "CarveReport", "CostTable", "SeamResult", "make_test_image", "to_grayscale", "energy_e1", "compute_energy",
     "energy_e1_rgb", "dp_seam", "parallel_dp_seam", "find_seam", "validate_seam", "remove_seam", "transpose",
     "carve_to_width", "carve_to_height", "carve", "carve_batch", "carve_device", "carve_batch_device",
+    "insert_seam", "record_seams", "enlarge_to_width", "enlarge",
     "library", "library_path", "device_count", "launch_count", "reset_launch_count",
 ]
 
@@ -170,6 +171,9 @@ def library() -> C.CDLL:
             "carve_cuda_dp_seam": ([vp, i, i, vp, vp, vp], i),
             "carve_cuda_validate_seam": ([vp, i, i, i], i),
             "carve_cuda_remove_seam_rgb": ([vp, i, i, vp, i, vp], i),
+            "carve_cuda_insert_seam_rgb": ([vp, i, i, vp, i, vp], i),
+            "carve_cuda_record_seams": ([vp, i, i, i, vp, vp], i),
+            "carve_cuda_enlarge": ([vp, i, i, i, i, vp, vp], i),
             "carve_cuda_carve": ([vp, i, i, i, i, vp, vp, vp], i),
             "carve_cuda_carve_batch": ([vp, i, i, i, i, i, vp, vp, i], i),
             "carve_cuda_carve_device": ([vp, i, i, i, i, vp, vp, vp], i),
@@ -414,6 +418,63 @@ def carve_to_width(img: np.ndarray, target_width: int, cfg: CarveConfig | None =
     t0 = time.perf_counter()
     out, seams, tims = carve(a, target_width, h, seams=True, timings=True)
     return out, _report(seams, tims, time.perf_counter() - t0)
+
+
+def insert_seam(img: np.ndarray, seam) -> np.ndarray:
+    """carver.hpp:137-140 — one pixel per row right of the seam, the rounded
+    mean of its neighbours (duplicating at the right border)."""
+    a = _img(img)
+    h, w, _ = a.shape
+    s = np.ascontiguousarray(seam, dtype=np.int32)
+    out = np.empty((h, w + 1, 3), np.uint8)
+    _check(library().carve_cuda_insert_seam_rgb(_ptr(a), w, h, _ptr(s), len(s), _ptr(out)))
+    return out
+
+
+def record_seams(img: np.ndarray, count: int, cfg: CarveConfig | None = None):
+    """carver.hpp:226-262 — the removal loop on a scratch copy; returns
+    (seams in original-image coordinates, CarveReport)."""
+    import time
+    a = _img(img)
+    h, w, _ = a.shape
+    _check_config(cfg)
+    count = int(count)
+    t0 = time.perf_counter()
+    s = np.empty((max(count, 0), h), np.int32)
+    t = (_Timing * max(count, 1))()
+    _check(library().carve_cuda_record_seams(_ptr(a), w, h, count, _ptr(s) if count > 0 else None,
+                                             C.cast(t, C.c_void_p)))
+    seams = [s[k].copy() for k in range(count)]
+    tims = [SeamTiming(t[k].energy_s, t[k].solve_s, t[k].remove_s) for k in range(count)]
+    return seams, _report(seams, tims, time.perf_counter() - t0)
+
+
+def enlarge(img: np.ndarray, target_width: int, target_height: int | None = None, *, seams: bool = False):
+    """run_enlarge (cli.hpp:262-277): enlarge_to_width on the width, then on the
+    transpose for the height. Returns the image (plus the recorded seams of both
+    phases, concatenated, when `seams`)."""
+    a = _img(img)
+    h, w, _ = a.shape
+    th = h if target_height is None else int(target_height)
+    tw = int(target_width)
+    n = max(tw - w, 0) * h + max(th - h, 0) * tw
+    out = np.empty((max(th, 0), max(tw, 0), 3), np.uint8)
+    s = np.empty(max(n, 1), np.int32)
+    _check(library().carve_cuda_enlarge(_ptr(a), w, h, tw, th, _ptr(out), _ptr(s)))
+    return (out, s[:n]) if seams else out
+
+
+def enlarge_to_width(img: np.ndarray, target_width: int, cfg: CarveConfig | None = None):
+    """carver.hpp:266-285 — returns (enlarged, CarveReport with the recorded seams)."""
+    import time
+    a = _img(img)
+    h, w, _ = a.shape
+    _check_config(cfg)
+    t0 = time.perf_counter()
+    out, flat = enlarge(a, target_width, h, seams=True)
+    k = int(target_width) - w
+    seams = [flat[t * h:(t + 1) * h].copy() for t in range(k)]
+    return out, _report(seams, [SeamTiming(0.0, 0.0, 0.0) for _ in range(k)], time.perf_counter() - t0)
 
 
 def carve_to_height(img: np.ndarray, target_height: int, cfg: CarveConfig | None = None):

@@ -99,6 +99,7 @@ struct Ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     DevBuf packed_in, packed_out, rgb[2], e[2], dir, seams, stamps, scratch_a, scratch_b, mbound;
+    DevBuf rec, enl[3];  // recorded seams (original coordinates), enlargement intermediates
     int max_smem_optin = 0;
     std::map<const void*, int> smem_set;  // kernel -> dynamic smem attribute set
     // kernel-event profiling mode (bench attribution): one event pair per launch
@@ -661,6 +662,62 @@ void validate_seam_host(const int32_t* seam, int n, int w, int h) {
     }
 }
 
+// stamps -> per-seam timings (energy is folded into the DP: reported as 0)
+void stamps_to_timings(const std::vector<unsigned long long>& st, int nseams, carve_seam_timing* timings) {
+    for (int k = 0; k < nseams; ++k) {
+        const unsigned long long* q = &st[size_t(k) * 4];
+        timings[k].energy_s = 0.0;
+        timings[k].solve_s = q[1] > q[0] ? double(q[1] - q[0]) * 1e-9 : 0.0;
+        timings[k].remove_s = q[3] > q[2] ? double(q[3] - q[2]) * 1e-9 : 0.0;
+    }
+}
+
+void launch_seams_to_original(const int* log, int count, int H, int* out, cudaStream_t s) {
+    const long long n = (long long)count * H;
+    if (n == 0) return;
+    k_seams_to_original<<<unsigned((n + 255) / 256), 256, 0, s>>>(log, count, H, out);
+    LAUNCHED("k_seams_to_original");
+}
+
+void launch_expand_rows(const uint8_t* in, int W, int H, const int* cols, int count, long long cstride, uint8_t* out,
+                        cudaStream_t s) {
+    constexpr int WPB = 4;
+    const size_t smem = size_t(WPB) * ((W + 31) / 32) * 4;
+    if (smem > 48 * 1024) {
+        ck(cudaFuncSetAttribute(k_expand_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+           "cudaFuncSetAttribute(k_expand_rows)");
+    }
+    k_expand_rows<<<unsigned((H + WPB - 1) / WPB), WPB * 32, smem, s>>>(in, W, H, cols, count, cstride, out);
+    LAUNCHED("k_expand_rows");
+}
+
+// record_seams (carver.hpp:226-262) on a packed device image: the ordinary
+// device carve loop to width w - count (its output is discarded), then the
+// logged seams mapped back to original coordinates. d_orig: count * h ints.
+void record_device(Ctx& c, const uint8_t* d_in, int w, int h, int count, int* d_orig, unsigned long long* d_st) {
+    if (count <= 0) return;
+    const CarveGeometry g = geometry(w, h, w - count, h);
+    ensure_carve_buffers(c, g, 1);
+    int* d_log = static_cast<int*>(c.seams.ensure(std::max<size_t>(g.seam_ints, 1) * 4));
+    uint8_t* d_scratch = static_cast<uint8_t*>(c.scratch_a.ensure(size_t(w - count) * h * 3));
+    run_carve(c, d_in, d_scratch, 1, g, d_log, g.seam_ints, d_st, c.stream);
+    launch_seams_to_original(d_log, count, h, d_orig, c.stream);
+}
+
+// packed w x h -> packed h x w (raster.hpp:73-79) through an RGBX plane
+void transpose_packed(Ctx& c, const uint8_t* d_in, int w, int h, uint8_t* d_out) {
+    const int pitch = int(round_up(w, 32));
+    uint32_t* plane = static_cast<uint32_t*>(c.rgb[0].ensure(size_t(pitch) * h * 4));
+    launch_unpack(c, d_in, w, h, plane, pitch, 1, 0, 0, c.stream);
+    launch_pack(c, plane, pitch, h, w, true, d_out, 1, 0, 0, c.stream);
+}
+
+// enlarge_to_width's target checks (carver.hpp:268-270)
+void check_enlarge(int w, int target) {
+    if (target < w) fail(CARVE_E_INVALID_TARGET, "enlargement target is below the current width");
+    if (target > 2 * w - 1) fail(CARVE_E_TARGET_TOO_LARGE, "single-pass enlargement is limited to 2*width-1");
+}
+
 void carve_one_host(Ctx& c, const uint8_t* rgb, int w, int h, int tw, int th, uint8_t* out, int32_t* seams_out,
                     carve_seam_timing* timings) {
     const CarveGeometry g = geometry(w, h, tw, th);
@@ -686,14 +743,7 @@ void carve_one_host(Ctx& c, const uint8_t* rgb, int w, int h, int tw, int th, ui
         ck(cudaMemcpyAsync(st.data(), d_st, st.size() * 8, cudaMemcpyDeviceToHost, s), "D2H stamps");
     }
     sync(c);
-    if (timings) {
-        for (int k = 0; k < g.nseams; ++k) {
-            const unsigned long long* q = &st[size_t(k) * 4];
-            timings[k].energy_s = 0.0;
-            timings[k].solve_s = q[1] > q[0] ? double(q[1] - q[0]) * 1e-9 : 0.0;
-            timings[k].remove_s = q[3] > q[2] ? double(q[3] - q[2]) * 1e-9 : 0.0;
-        }
-    }
+    if (timings) stamps_to_timings(st, g.nseams, timings);
 }
 
 }  // namespace
@@ -902,6 +952,87 @@ carve_status carve_cuda_dp_profile(const double* e, int w, int h, long long* cou
            "D2H prof");
         sync(c);
         *warps = G;
+    });
+}
+
+carve_status carve_cuda_insert_seam_rgb(const uint8_t* rgb, int w, int h, const int32_t* seam, int n, uint8_t* out) {
+    return guarded([&] {
+        validate_seam_host(seam, n, w, h);  // carver.hpp:138
+        Ctx& c = ctx();
+        uint8_t* d_in = static_cast<uint8_t*>(c.packed_in.ensure(size_t(w) * h * 3));
+        uint8_t* d_out = static_cast<uint8_t*>(c.packed_out.ensure(size_t(w + 1) * h * 3));
+        int* ds = static_cast<int*>(c.rec.ensure(size_t(h) * 4));
+        ck(cudaMemcpyAsync(d_in, rgb, size_t(w) * h * 3, cudaMemcpyHostToDevice, c.stream), "H2D");
+        ck(cudaMemcpyAsync(ds, seam, size_t(h) * 4, cudaMemcpyHostToDevice, c.stream), "H2D seam");
+        launch_expand_rows(d_in, w, h, ds, 1, h, d_out, c.stream);
+        ck(cudaMemcpyAsync(out, d_out, size_t(w + 1) * h * 3, cudaMemcpyDeviceToHost, c.stream), "D2H");
+        sync(c);
+    });
+}
+
+carve_status carve_cuda_record_seams(const uint8_t* rgb, int w, int h, int count, int32_t* seams_out,
+                                     carve_seam_timing* timings_out) {
+    return guarded([&] {
+        if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "PixelGrid dimensions must be >= 1");
+        if (count < 0 || count > w - 1) fail(CARVE_E_INVALID_TARGET, "cannot record more seams than width-1");
+        if (count == 0) return;
+        Ctx& c = ctx();
+        uint8_t* d_in = static_cast<uint8_t*>(c.packed_in.ensure(size_t(w) * h * 3));
+        int* d_orig = static_cast<int*>(c.rec.ensure(size_t(count) * h * 4));
+        const CarveGeometry g = geometry(w, h, w - count, h);
+        unsigned long long* d_st = nullptr;
+        if (timings_out) {
+            d_st = static_cast<unsigned long long*>(c.stamps.ensure(stamp_words(g) * 8));
+            ck(cudaMemsetAsync(d_st, 0, stamp_words(g) * 8, c.stream), "memset stamps");
+        }
+        ck(cudaMemcpyAsync(d_in, rgb, size_t(w) * h * 3, cudaMemcpyHostToDevice, c.stream), "H2D");
+        record_device(c, d_in, w, h, count, d_orig, d_st);
+        ck(cudaMemcpyAsync(seams_out, d_orig, size_t(count) * h * 4, cudaMemcpyDeviceToHost, c.stream), "D2H seams");
+        std::vector<unsigned long long> st;
+        if (timings_out) {
+            st.resize(stamp_words(g));
+            ck(cudaMemcpyAsync(st.data(), d_st, st.size() * 8, cudaMemcpyDeviceToHost, c.stream), "D2H stamps");
+        }
+        sync(c);
+        if (timings_out) stamps_to_timings(st, count, timings_out);
+    });
+}
+
+carve_status carve_cuda_enlarge(const uint8_t* rgb, int w, int h, int target_w, int target_h, uint8_t* rgb_out,
+                                int32_t* seams_out) {
+    return guarded([&] {
+        if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "PixelGrid dimensions must be >= 1");
+        if (target_w != w) check_enlarge(w, target_w);
+        if (target_h != h) check_enlarge(h, target_h);
+        Ctx& c = ctx();
+        const int kw = target_w - w, kh = target_h - h;
+        const size_t big = size_t(target_w) * target_h * 3;
+        uint8_t* d_in = static_cast<uint8_t*>(c.packed_in.ensure(size_t(w) * h * 3));
+        uint8_t* d_out = static_cast<uint8_t*>(c.packed_out.ensure(big));
+        uint8_t* e0 = static_cast<uint8_t*>(c.enl[0].ensure(big));
+        uint8_t* e1p = static_cast<uint8_t*>(c.enl[1].ensure(big));
+        uint8_t* e2 = static_cast<uint8_t*>(c.enl[2].ensure(big));
+        const size_t nrec = size_t(kw) * h + size_t(kh) * target_w;
+        int* d_orig = static_cast<int*>(c.rec.ensure(std::max<size_t>(nrec, 1) * 4));
+        ck(cudaMemcpyAsync(d_in, rgb, size_t(w) * h * 3, cudaMemcpyHostToDevice, c.stream), "H2D");
+        const uint8_t* cur = d_in;
+        if (kw > 0) {  // enlarge_to_width (carver.hpp:266-285)
+            record_device(c, d_in, w, h, kw, d_orig, nullptr);
+            launch_expand_rows(d_in, w, h, d_orig, kw, h, e0, c.stream);
+            cur = e0;
+        }
+        if (kh > 0) {  // the height: enlarge_to_width of the transpose (cli.hpp:271-274)
+            int* d_orig_h = d_orig + size_t(kw) * h;
+            transpose_packed(c, cur, target_w, h, e1p);  // h wide, target_w high
+            record_device(c, e1p, h, target_w, kh, d_orig_h, nullptr);
+            launch_expand_rows(e1p, h, target_w, d_orig_h, kh, target_w, e2, c.stream);
+            transpose_packed(c, e2, target_h, target_w, d_out);
+            cur = d_out;
+        }
+        ck(cudaMemcpyAsync(rgb_out, cur, big, cudaMemcpyDeviceToHost, c.stream), "D2H");
+        if (seams_out && nrec)
+            ck(cudaMemcpyAsync(seams_out, d_orig, nrec * 4, cudaMemcpyDeviceToHost, c.stream), "D2H seams");
+        sync(c);
     });
 }
 

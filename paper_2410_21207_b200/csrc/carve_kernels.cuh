@@ -712,4 +712,85 @@ __global__ void __launch_bounds__(256) k_compact_warp(CompactParams p) {
     if (p.stamps && threadIdx.x == 0) atomicMax(&p.stamps[img * p.st_istride + 1], (unsigned long long)globaltimer());
 }
 
+// ---------------------------------------------------------------------------
+// Seam recording and enlargement
+
+// record_seams (carver.hpp:226-262) reports each seam in original-image
+// coordinates via per-row survivor lists. The device carve loop logs seam t in
+// the coordinates of the grid it was found on; column x of grid u+1 is column
+// x + (x >= s_u) of grid u (remove_seam, carver.hpp:71-82), so walking back
+// through the row's earlier seams recovers the survivor index. One thread per
+// (seam, row); the log is read row-coalesced.
+__global__ void k_seams_to_original(const int* __restrict__ log, int count, int H, int* __restrict__ out) {
+    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (idx >= (long long)count * H) return;
+    const int t = int(idx / H), i = int(idx - (long long)t * H);
+    int x = log[idx];
+    for (int u = t - 1; u >= 0; --u) x += x >= log[(long long)u * H + i] ? 1 : 0;
+    out[idx] = x;
+}
+
+// enlarge_to_width's replay (carver.hpp:266-285) in closed form. Recorded
+// columns of one row are distinct original columns, and the replay's shift
+// rule keeps every later seam pointing at the same original pixel, so seam t
+// always inserts immediately right of original column o_t, whose right
+// neighbour at that moment is still original column o_t + 1 (nothing else has
+// been inserted after o_t; clamped at the border). The enlarged row is thus
+// the original row with insert_columns' rounded mean (carver.hpp:124-128) of
+// p[o] and p[min(o+1, W-1)] after every recorded column o — independent of the
+// replay order. One warp per row: the recorded columns become a bitmap in
+// shared memory; a warp scan of word popcounts gives every column's output
+// position; lanes walk the row with consecutive columns (coalesced reads).
+// cols[t * cstride + i] is row i's column of seam t. Packed RGB in and out.
+__global__ void k_expand_rows(const uint8_t* __restrict__ in, int W, int H, const int* __restrict__ cols, int count,
+                              long long cstride, uint8_t* __restrict__ out) {
+    extern __shared__ uint32_t bm_all[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int i = blockIdx.x * (blockDim.x >> 5) + wib;
+    const int nw = (W + 31) >> 5;
+    uint32_t* bm = bm_all + wib * nw;
+    if (i >= H) return;
+    for (int k = lane; k < nw; k += 32) bm[k] = 0u;
+    __syncwarp();
+    for (int t = lane; t < count; t += 32) {
+        const int o = cols[(long long)t * cstride + i];
+        atomicOr(&bm[o >> 5], 1u << (o & 31));
+    }
+    __syncwarp();
+    const uint8_t* src = in + (long long)i * W * 3;
+    uint8_t* dst = out + (long long)i * (W + count) * 3;
+    int running = 0;  // inserted pixels left of this group of 32 words
+    for (int wb = 0; wb < nw; wb += 32) {
+        const uint32_t word = wb + lane < nw ? bm[wb + lane] : 0u;
+        const int cnt = __popc(word);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int pre = running + incl - cnt;  // inserted pixels left of my word
+        for (int u = 0; u < 32 && wb + u < nw; ++u) {
+            const uint32_t wu = __shfl_sync(FULL, word, u);
+            const int pu = __shfl_sync(FULL, pre, u);
+            const int j = (wb + u) * 32 + lane;
+            if (j < W) {
+                const int pos = j + pu + __popc(wu & ((1u << lane) - 1u));
+                const uint8_t* a = src + 3 * j;
+                uint8_t* d = dst + 3 * pos;
+                d[0] = a[0];
+                d[1] = a[1];
+                d[2] = a[2];
+                if (wu >> lane & 1u) {
+                    const uint8_t* b = src + 3 * min(j + 1, W - 1);
+                    d[3] = uint8_t((a[0] + b[0] + 1) / 2);
+                    d[4] = uint8_t((a[1] + b[1] + 1) / 2);
+                    d[5] = uint8_t((a[2] + b[2] + 1) / 2);
+                }
+            }
+        }
+        running += __shfl_sync(FULL, incl, 31);
+    }
+}
+
 }  // namespace carve_dev

@@ -46,7 +46,10 @@ def test_cli_usage_errors_exit_1(tmp_path):
     assert run("resize", "--input", "a.ppm").returncode == 1  # missing --output
     assert run("resize", "--input", "a", "--output", "b", "--scale", "0").returncode == 1
     assert run("resize", "--input", "a", "--output", "b", "--scale", "0.5", "--width", "3").returncode == 1
-    assert run("enlarge", "--input", "a", "--output", "b").returncode == 1
+    assert run("enlarge", "--input", "a").returncode == 1  # missing --output
+    assert run("seams", "--input", "a", "--output", "b").returncode == 1  # --count is required
+    assert run("seams", "--input", "a", "--output", "b", "--count", "0").returncode == 1
+    assert run("remove-object", "--input", "a", "--output", "b").returncode == 1
     r = run("resize", "--input", "a", "--output", "b", "--solver", "quantum")
     assert r.returncode == 1 and "carve:" in r.stderr
 
@@ -99,3 +102,26 @@ def test_cli_resize_matches_oracle_and_is_worker_invariant(tmp_path):
     assert outs[0] == outs[1]
     want = oracle.port().carve(img, 90, 150)
     assert np.array_equal(read_ppm(tmp_path / "out1.ppm"), want)
+
+
+@pytest.mark.gpu
+def test_cli_enlarge_and_seams_match_oracle(tmp_path):
+    # cli.hpp:262-277 (enlarge) and :301-309 (seams); test_cli.cpp:185-188
+    port = oracle.port()
+    img = port.make_test_image(40, 30)
+    src = tmp_path / "in.ppm"
+    write_ppm(src, img)
+    r = run("enlarge", "--input", str(src), "--output", str(tmp_path / "e.ppm"), "--width", "55", "--height", "41")
+    assert r.returncode == 0, r.stderr
+    assert np.array_equal(read_ppm(tmp_path / "e.ppm"), port.enlarge(img, 55, 41))
+    r = run("enlarge", "--input", str(src), "--output", str(tmp_path / "e2.ppm"), "--scale", "1.25")
+    assert r.returncode == 0, r.stderr
+    assert np.array_equal(read_ppm(tmp_path / "e2.ppm"), port.enlarge(img, 50, 30))
+    r = run("enlarge", "--input", str(src), "--output", str(tmp_path / "e3.ppm"), "--width", "80")
+    assert r.returncode == 2 and "2*width-1" in r.stderr  # target_too_large is a runtime error
+    r = run("seams", "--input", str(src), "--output", str(tmp_path / "s.ppm"), "--count", "5")
+    assert r.returncode == 0, r.stderr
+    want = img.copy()
+    for seam in port.record_seams(img, 5):
+        want[np.arange(30), seam] = (255, 0, 0)
+    assert np.array_equal(read_ppm(tmp_path / "s.ppm"), want)

@@ -130,3 +130,58 @@ def test_reference_pardp_equals_dp():
     a = ref.dp_seam(e, 0)
     b = ref.dp_seam(e, 1, 4)
     assert all(np.array_equal(x, y) for x, y in zip(a, b))
+
+
+# -- seam recording and enlargement ---------------------------
+def test_enlarge_golden(port):
+    """The C restatement of record_seams / enlarge_to_width (replay with shifts) /
+    insert_seam against the reference-generated fixtures (make_golden_enlarge.py)."""
+    z = np.load(os.path.join(GOLD, "enlarge.npz"))
+    for k in range(int(z["n"])):
+        img = z[f"img{k}"]
+        cnt, tw, th = (int(v) for v in z[f"tgt{k}"])
+        assert np.array_equal(port.record_seams(img, cnt), z[f"rec{k}"]), k
+        out, seams = port.enlarge(img, tw, th, seams=True)
+        assert np.array_equal(out, z[f"enl{k}"]), k
+        assert np.array_equal(seams, z[f"enlseams{k}"][: seams.size]), k
+        assert np.array_equal(port.insert_seam(img, z[f"iseam{k}"]), z[f"ins{k}"]), k
+
+
+def test_enlarge_golden_config(port, gold):
+    c = gold["configs"]["ENLARGE"]
+    img = port.make_test_image(c["W"], c["H"])
+    assert f"{oracle.fnv1a64(img):016x}" == c["input"]
+    out, seams = port.enlarge(img, c["target_w"], c["target_h"], seams=True)
+    assert f"{oracle.fnv1a64(out):016x}" == c["output"]
+    assert f"{oracle.fnv1a64(seams):016x}" == c["seams"]
+    r = c["record"]
+    rec = port.record_seams(port.make_test_image(r["W"], r["H"]), r["count"])
+    assert f"{oracle.fnv1a64(rec):016x}" == r["seams"]
+
+
+def test_enlarge_errors(port):
+    # test_carver.cpp:247-253, :271-275
+    g = port.make_test_image(6, 4)
+    for (tw, th, st) in [(5, 4, 1 + 9), (12, 4, 1 + 10), (6, 3, 1 + 9), (6, 8, 1 + 10)]:
+        with pytest.raises(oracle.OracleError) as ei:
+            port.enlarge(g, tw, th)
+        assert ei.value.status == st
+    assert port.enlarge(g, 11, 4).shape == (4, 11, 3)
+    with pytest.raises(oracle.OracleError) as ei:
+        port.record_seams(np.zeros((4, 4, 3), np.uint8), 4)
+    assert ei.value.status == 1 + 9
+
+
+@need_ref
+def test_enlarge_port_vs_reference_random(port):
+    ref = oracle.reference()
+    rng = np.random.default_rng(21)
+    for _ in range(40):
+        h, w = (int(v) for v in rng.integers(1, 16, 2))
+        img = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+        cnt = int(rng.integers(0, w))
+        assert np.array_equal(port.record_seams(img, cnt), ref.record_seams(img, cnt))
+        tw, th = w + int(rng.integers(0, w)), h + int(rng.integers(0, h))
+        a, sa = port.enlarge(img, tw, th, seams=True)
+        b, sb = ref.enlarge(img, tw, th, seams=True)
+        assert np.array_equal(a, b) and np.array_equal(sa, sb)

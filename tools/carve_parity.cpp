@@ -84,6 +84,32 @@ static int selftest() {
     auto t = make_test_image(10, 8);
     EXPECT(carve_to_height(t, 5).first == transpose(carve_to_width(transpose(t), 5).first));
     EXPECT(transpose(transpose(t)) == t);
+    // insert_seam (test_carver.cpp:76-92)
+    PixelGrid one(1, 1, Rgb{9, 8, 7});
+    auto ins = insert_seam(one, {0});
+    EXPECT(ins.width == 2 && (ins.at(0, 0) == Rgb{9, 8, 7}) && (ins.at(0, 1) == Rgb{9, 8, 7}));
+    PixelGrid two(2, 1);
+    two.at(0, 0) = Rgb{0, 0, 0};
+    two.at(0, 1) = Rgb{100, 100, 100};
+    EXPECT((insert_seam(two, {0}).at(0, 1) == Rgb{50, 50, 50}));
+    // enlarge_to_width (test_carver.cpp:214-253)
+    PixelGrid pair(2, 1);
+    pair.at(0, 0) = Rgb{10, 20, 30};
+    pair.at(0, 1) = Rgb{30, 40, 50};
+    auto [wide, wrep] = enlarge_to_width(pair, 3);
+    EXPECT(wide.width == 3 && wrep.seam_count == 1 && (wrep.seams[0] == Seam{0}));
+    EXPECT((wide.at(0, 1) == Rgb{20, 30, 40}) && (wide.at(0, 2) == Rgb{30, 40, 50}));
+    auto six = make_test_image(6, 4);
+    EXPECT(thrown([&] { enlarge_to_width(six, 5); }) == Errc::invalid_target);
+    EXPECT(thrown([&] { enlarge_to_width(six, 12); }) == Errc::target_too_large);
+    EXPECT(enlarge_to_width(six, 11).first.width == 11);
+    // record_seams (test_carver.cpp:257-275)
+    auto [rec, rrep] = record_seams(make_test_image(15, 9), 6);
+    EXPECT(rec.size() == 6 && rrep.seam_count == 6 && rrep.per_seam.size() == 6);
+    for (int i = 0; i < 9; ++i)
+        for (size_t a = 0; a < rec.size(); ++a)
+            for (size_t b = a + 1; b < rec.size(); ++b) EXPECT(rec[a][i] != rec[b][i]);
+    EXPECT(thrown([] { record_seams(PixelGrid(4, 4), 4); }) == Errc::invalid_target);
     std::printf(failures ? "selftest FAILED (%d)\n" : "selftest ok\n", failures);
     return failures ? 1 : 0;
 }
