@@ -376,6 +376,15 @@ def roofline_of(kern, cfg_name="c2", sm_mhz=None):
         floor = CHAIN_CYCLES_PER_ROW / ((sm_mhz or 1965.0) / 1e3)
         r["latency"] = {"note": "the DP is latency-bound (row-serial chain), not HBM-bound",
                         "ns_per_row": ns_row, "chain_floor_ns_per_row": floor, "frac_of_chain_floor": floor / ns_row}
+        try:  # shared-memory fraction and barrier stalls of the committed C2 ncu capture
+            nm = json.load(open(os.path.join(ROOT, "profiles", "r01_dp_ncu_metrics.json")))
+            if cfg_name == "c2":
+                r["latency"].update(smem_frac_active_sms=nm["smem_wavefronts_frac_of_peak_active_sms"],
+                                    barrier_stall_share=nm["barrier_stall_share"],
+                                    halo_wait_stall_share=nm["stall_share"].get("long_scoreboard"),
+                                    ncu_source="profiles/r01_dp_ncu_metrics.json")
+        except Exception:
+            pass
     return r
 
 
