@@ -21,7 +21,7 @@ struct CarveConfig {
     SolverKind solver = SolverKind::ParallelDynamic;
     EnergyFn energy_fn = EnergyFn::e1;
     bool forward = false;
-    bool recompute = true;  // the engine always produces the recompute=true result
+    bool recompute = true;  // false: e1 once, then carved alongside (carver.hpp:176-188)
     SolverOptions solver_opts{};
 };
 
@@ -44,18 +44,25 @@ inline void check_config(const CarveConfig& cfg) {
     const bool dp = cfg.solver == SolverKind::Dynamic || cfg.solver == SolverKind::ParallelDynamic;
     if (cfg.forward && !dp) fail(Errc::usage_error, "forward energy requires the dp or pardp solver");
     if (!dp) unsupported(std::string("solver ") + to_string(cfg.solver));
-    if (cfg.energy_fn != EnergyFn::e1) unsupported(std::string("energy ") + to_string(cfg.energy_fn));
-    if (cfg.forward) unsupported("forward energy");
+    // forward mode solves on forward costs; energy_fn only matters for the backward form
+    if (!cfg.forward && cfg.energy_fn != EnergyFn::e1) unsupported(std::string("energy ") + to_string(cfg.energy_fn));
+}
+
+inline carve_cuda_config abi_config(const CarveConfig& cfg) {
+    return carve_cuda_config{cfg.forward ? 1 : 0, cfg.recompute ? 1 : 0};
 }
 
 // one device-resident carve: width phase then height phase (run_resize order)
-inline std::pair<PixelGrid, CarveReport> carve_device(const PixelGrid& grid, int tw, int th) {
+inline std::pair<PixelGrid, CarveReport> carve_device(const PixelGrid& grid, int tw, int th,
+                                                      const CarveConfig& cfg = {}) {
     const auto t0 = std::chrono::steady_clock::now();
     const int vs = grid.width - tw, hs = grid.height - th;
     PixelGrid out(tw, th);
     std::vector<int32_t> flat(size_t(vs) * grid.height + size_t(hs) * tw);
     std::vector<carve_seam_timing> tim(size_t(vs + hs));
-    check(carve_cuda_carve(grid.bytes(), grid.width, grid.height, tw, th, out.bytes(), flat.data(), tim.data()));
+    const carve_cuda_config c = abi_config(cfg);
+    check(carve_cuda_carve_cfg(grid.bytes(), grid.width, grid.height, tw, th, &c, out.bytes(), flat.data(),
+                               tim.data()));
     CarveReport rep;
     rep.seam_count = vs + hs;
     size_t off = 0;
@@ -85,7 +92,7 @@ inline std::pair<PixelGrid, CarveReport> carve_to_width(const PixelGrid& grid, i
     if (target_width < 1 || target_width > grid.width)
         fail(Errc::invalid_target, "target width must be in [1, width]");
     detail::check_config(cfg);
-    return detail::carve_device(grid, target_width, grid.height);
+    return detail::carve_device(grid, target_width, grid.height, cfg);
 }
 
 inline std::pair<PixelGrid, CarveReport> carve_to_height(const PixelGrid& grid, int target_height,
@@ -93,7 +100,7 @@ inline std::pair<PixelGrid, CarveReport> carve_to_height(const PixelGrid& grid, 
     if (target_height < 1 || target_height > grid.height)
         fail(Errc::invalid_target, "target height must be in [1, height]");
     detail::check_config(cfg);
-    return detail::carve_device(grid, grid.width, target_height);
+    return detail::carve_device(grid, grid.width, target_height, cfg);
 }
 
 /// Batch entry point (no reference equivalent): same-size images sharded by
@@ -135,7 +142,9 @@ inline std::pair<std::vector<Seam>, CarveReport> record_seams(const PixelGrid& g
     const auto t0 = std::chrono::steady_clock::now();
     std::vector<int32_t> flat(size_t(count) * grid.height);
     std::vector<carve_seam_timing> tim(size_t(std::max(count, 1)));
-    detail::check(carve_cuda_record_seams(grid.bytes(), grid.width, grid.height, count, flat.data(), tim.data()));
+    const carve_cuda_config c = detail::abi_config(cfg);
+    detail::check(
+        carve_cuda_record_seams(grid.bytes(), grid.width, grid.height, count, &c, flat.data(), tim.data()));
     std::vector<Seam> seams;
     CarveReport rep;
     for (int t = 0; t < count; ++t) {
@@ -160,8 +169,9 @@ inline std::pair<PixelGrid, CarveReport> enlarge_to_width(const PixelGrid& grid,
     const auto t0 = std::chrono::steady_clock::now();
     PixelGrid out(target_width, grid.height);
     std::vector<int32_t> flat(std::max<size_t>(size_t(k) * grid.height, 1));
-    detail::check(carve_cuda_enlarge(grid.bytes(), grid.width, grid.height, target_width, grid.height, out.bytes(),
-                                     flat.data()));
+    const carve_cuda_config c = detail::abi_config(cfg);
+    detail::check(carve_cuda_enlarge(grid.bytes(), grid.width, grid.height, target_width, grid.height, &c,
+                                     out.bytes(), flat.data()));
     CarveReport rep;
     for (int t = 0; t < k; ++t) {
         rep.seams.emplace_back(flat.begin() + size_t(t) * grid.height, flat.begin() + size_t(t + 1) * grid.height);

@@ -106,13 +106,14 @@ inline CarveConfig config_of(const ResizeCmd& cmd) {
 inline int run_resize(const ResizeCmd& cmd) {
     detail::check_env_workers();
     PixelGrid img = load_image(cmd.input);
-    ::carve::detail::check_config(detail::config_of(cmd));
+    const CarveConfig cfg = detail::config_of(cmd);
+    ::carve::detail::check_config(cfg);
     const int tw = cmd.scale ? int(std::lround(*cmd.scale * img.width)) : cmd.width.value_or(img.width);
     const int th = cmd.height.value_or(img.height);
     if (tw > img.width) fail(Errc::invalid_target, "resize cannot grow the width; use the enlarge command");
     if (tw < 1) fail(Errc::invalid_target, "target width must be in [1, width]");
     if (th < 1 || th > img.height) fail(Errc::invalid_target, "target height must be in [1, height]");
-    auto [out, report] = ::carve::detail::carve_device(img, tw, th);
+    auto [out, report] = ::carve::detail::carve_device(img, tw, th, cfg);
     save_image(out, cmd.output);
     return 0;
 }
@@ -122,11 +123,13 @@ inline int run_resize(const ResizeCmd& cmd) {
 inline int run_enlarge(const EnlargeCmd& cmd) {
     detail::check_env_workers();
     PixelGrid img = load_image(cmd.input);
-    ::carve::detail::check_config(detail::config_of(cmd));
+    const CarveConfig cfg = detail::config_of(cmd);
+    ::carve::detail::check_config(cfg);
     const int tw = cmd.scale ? int(std::lround(*cmd.scale * img.width)) : cmd.width.value_or(img.width);
     const int th = cmd.height.value_or(img.height);
     PixelGrid out(tw, th);
-    ::carve::detail::check(carve_cuda_enlarge(img.bytes(), img.width, img.height, tw, th, out.bytes(), nullptr));
+    const carve_cuda_config c = ::carve::detail::abi_config(cfg);
+    ::carve::detail::check(carve_cuda_enlarge(img.bytes(), img.width, img.height, tw, th, &c, out.bytes(), nullptr));
     save_image(out, cmd.output);
     return 0;
 }

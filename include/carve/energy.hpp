@@ -39,6 +39,10 @@ struct ForwardCosts {
     int width = 0;
     int height = 0;
     std::vector<double> cost_left, cost_up, cost_right;
+
+    double left(int row, int col) const { return cost_left[size_t(row) * width + col]; }
+    double up(int row, int col) const { return cost_up[size_t(row) * width + col]; }
+    double right(int row, int col) const { return cost_right[size_t(row) * width + col]; }
 };
 
 enum class EnergyFn { e1, e2, hog, entropy };
@@ -71,7 +75,19 @@ inline EnergyMap compute_energy(const LumaGrid& gray, EnergyFn fn) {
     return energy_e1(gray);
 }
 
-inline ForwardCosts forward_costs(const LumaGrid&) { detail::unsupported("forward energy"); }
+/// energy.hpp:196-216 forward transition costs, on the device.
+inline ForwardCosts forward_costs(const LumaGrid& gray) {
+    ForwardCosts fc;
+    fc.width = gray.width;
+    fc.height = gray.height;
+    const size_t n = gray.values.size();
+    fc.cost_left.resize(n);
+    fc.cost_up.resize(n);
+    fc.cost_right.resize(n);
+    detail::check(carve_cuda_forward_costs(gray.values.data(), gray.width, gray.height, fc.cost_left.data(),
+                                           fc.cost_up.data(), fc.cost_right.data()));
+    return fc;
+}
 inline EnergyMap apply_mask(const EnergyMap&, const RemovalMask&) { detail::unsupported("removal masks"); }
 
 } // namespace carve

@@ -60,6 +60,15 @@ enum {
 
 /* Per-seam timing, filled from device %globaltimer stamps
  * (replaces carver.hpp:23-27 SeamTiming laps). Seconds. */
+/* The CarveConfig fields that change results (carver.hpp:15-24); NULL = the
+ * reference defaults {forward = 0, recompute = 1}. solver/workers/energy_fn
+ * have no output effect on this path (dp == pardp; e1 only). */
+typedef struct carve_cuda_config {
+    int forward;   /* forward energy: dp_seam_forward on forward_costs(to_grayscale(current)) */
+    int recompute; /* 0: e1 once, then the map is carved alongside (carver.hpp:176-188);
+                      forward with recompute = 0 returns CARVE_E_USAGE_ERROR (not supported) */
+} carve_cuda_config;
+
 typedef struct carve_seam_timing {
     double energy_s; /* K1 full map for the first seam of a phase; 0 when the
                         incremental fix-up is fused into the removal kernel */
@@ -109,6 +118,14 @@ carve_status carve_cuda_dp_profile(const double* e, int w, int h, long long* cou
 /* replaces validate_seam (solvers.hpp:69-78); pure host check */
 carve_status carve_cuda_validate_seam(const int32_t* seam, int n, int w, int h);
 
+/* ---- forward energy (energy.hpp:196-216, solvers.hpp:294-326) ---------- */
+/* replaces forward_costs(const LumaGrid&); outputs w*h doubles each */
+carve_status carve_cuda_forward_costs(const double* luma, int w, int h, double* left, double* up, double* right);
+/* replaces dp_seam_forward(gray, forward_costs(gray)): table (nullable pair)
+ * and seam, bit-identical. */
+carve_status carve_cuda_dp_seam_forward(const double* luma, int w, int h, double* m_out, int32_t* b_out,
+                                        int32_t* seam_out);
+
 /* ---- seam recording and enlargement (carver.hpp:114-140, 226-285; cli.hpp:262-277, 301-309) */
 /* replaces insert_seam (carver.hpp:137-140: validate_seam + detail::insert_columns
  * :117-130); out is (w+1)*h*3 bytes */
@@ -117,15 +134,15 @@ carve_status carve_cuda_insert_seam_rgb(const uint8_t* rgb, int w, int h, const 
 /* replaces record_seams (carver.hpp:226-262) with the default CarveConfig:
  * seams_out receives count*h ints, seam t's column of row i at [t*h + i], in
  * original-image coordinates. timings_out (nullable): count entries. */
-carve_status carve_cuda_record_seams(const uint8_t* rgb, int w, int h, int count, int32_t* seams_out,
-                                     carve_seam_timing* timings_out);
+carve_status carve_cuda_record_seams(const uint8_t* rgb, int w, int h, int count, const carve_cuda_config* cfg,
+                                     int32_t* seams_out, carve_seam_timing* timings_out);
 /* replaces run_enlarge (cli.hpp:262-277): enlarge_to_width(target_w)
  * (carver.hpp:266-285) if target_w != w, then enlarge_to_width of the
  * transpose to target_h if target_h != h. rgb_out: target_w*target_h*3 bytes.
  * seams_out (nullable): (target_w-w)*h + (target_h-h)*target_w ints — each
  * phase's recorded seams (its CarveReport.seams), concatenated. */
-carve_status carve_cuda_enlarge(const uint8_t* rgb, int w, int h, int target_w, int target_h, uint8_t* rgb_out,
-                                int32_t* seams_out);
+carve_status carve_cuda_enlarge(const uint8_t* rgb, int w, int h, int target_w, int target_h,
+                                const carve_cuda_config* cfg, uint8_t* rgb_out, int32_t* seams_out);
 
 /* ---- pipelines (carver.hpp:71-82, 191-222; cli.hpp:242-259) ----------- */
 /* replaces remove_seam(PixelGrid) (carver.hpp:71-82); out is (w-1)*h*3 bytes */
@@ -138,6 +155,10 @@ carve_status carve_cuda_remove_seam_rgb(const uint8_t* rgb, int w, int h, const 
  *   seam in removal order, as CarveReport.seams holds them (carver.hpp:31).
  * timings_out (nullable): (w-target_w)+(h-target_h) entries.
  * The whole loop runs on the device; no host round trip per seam. */
+/* carve_cuda_carve with a CarveConfig (forward energy, recompute) */
+carve_status carve_cuda_carve_cfg(const uint8_t* rgb, int w, int h, int target_w, int target_h,
+                                  const carve_cuda_config* cfg, uint8_t* rgb_out, int32_t* seams_out,
+                                  carve_seam_timing* timings_out);
 carve_status carve_cuda_carve(const uint8_t* rgb, int w, int h, int target_w, int target_h, uint8_t* rgb_out,
                               int32_t* seams_out, carve_seam_timing* timings_out);
 

@@ -87,6 +87,36 @@ class _Checker:
         return out
 
 
+    def forward_costs(self, luma: np.ndarray):
+        """energy.hpp:196-216 -> (left, up, right)"""
+        h, w = luma.shape
+        outs = [np.empty((h, w), np.float64) for _ in range(3)]
+        self._check(self._fn("forward_costs", _f8p, C.c_int, C.c_int, _f8p, _f8p, _f8p)(
+            np.ascontiguousarray(luma, np.float64), w, h, *outs))
+        return tuple(outs)
+
+    def dp_seam_forward(self, luma: np.ndarray):
+        """solvers.hpp:294-326 with forward_costs(luma) -> (seam, m, b)"""
+        h, w = luma.shape
+        m = np.empty((h, w), np.float64)
+        b = np.empty((h, w), np.int32)
+        seam = np.empty(h, np.int32)
+        self._check(self._fn("dp_seam_forward", _f8p, C.c_int, C.c_int, _f8p, _i4p, _i4p)(
+            np.ascontiguousarray(luma, np.float64), w, h, m, b, seam))
+        return seam, m, b
+
+    def carve_cfg(self, img: np.ndarray, target_w: int, target_h: int | None = None, forward: bool = False,
+                  recompute: bool = True, seams: bool = False):
+        """run_resize with CarveConfig::forward / ::recompute"""
+        h, w, _ = img.shape
+        th = h if target_h is None else target_h
+        out = np.empty((th, target_w, 3), np.uint8)
+        n = (w - target_w) * h + (h - th) * target_w
+        s = np.empty(max(n, 1), np.int32)
+        f = self._fn("carve_cfg", _u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _u8p, C.c_void_p)
+        self._check(f(np.ascontiguousarray(img), w, h, target_w, th, int(forward), int(recompute), out, s.ctypes.data))
+        return (out, s[:n]) if seams else out
+
     def insert_seam(self, img: np.ndarray, seam) -> np.ndarray:
         """carver.hpp:137-140"""
         h, w, _ = img.shape

@@ -217,6 +217,145 @@ int or_carve(const uint8_t* rgb, int w, int h, int target_w, int target_h, uint8
     return st;
 }
 
+/* energy.hpp:196-216 forward_costs: at_clamped neighbours, cu = |right - left|,
+ * cl = cu + |above - left|, cr = cu + |above - right|. */
+int or_forward_costs(const double* g, int w, int h, double* left, double* up, double* right) {
+    if (w < 1 || h < 1) return OR_EMPTY_IMAGE;
+    for (int i = 0; i < h; ++i)
+        for (int j = 0; j < w; ++j) {
+            const double l = g[(size_t)i * w + clampi(j - 1, 0, w - 1)];
+            const double r = g[(size_t)i * w + clampi(j + 1, 0, w - 1)];
+            const double a = g[(size_t)clampi(i - 1, 0, h - 1) * w + j];
+            const size_t idx = (size_t)i * w + j;
+            const double cu = fabs(r - l);
+            up[idx] = cu;
+            left[idx] = cu + fabs(a - l);
+            right[idx] = cu + fabs(a - r);
+        }
+    return OR_OK;
+}
+
+/* solvers.hpp:294-326 dp_seam_forward(g, forward_costs(g)): candidates
+ * prev + transition cost in the order left, up, right, strict <. m/b nullable. */
+int or_dp_seam_forward(const double* g, int w, int h, double* m_out, int* b_out, int* seam) {
+    if (w < 1 || h < 1) return OR_EMPTY_IMAGE;
+    const size_t n = (size_t)w * h;
+    double* cl = (double*)malloc(n * 8);
+    double* cu = (double*)malloc(n * 8);
+    double* cr = (double*)malloc(n * 8);
+    double* m = m_out ? m_out : (double*)malloc(n * 8);
+    int* b = b_out ? b_out : (int*)malloc(n * 4);
+    if (!cl || !cu || !cr || !m || !b) return OR_NO_MEMORY;
+    or_forward_costs(g, w, h, cl, cu, cr);
+    for (int j = 0; j < w; ++j) {
+        m[j] = cu[j];
+        b[j] = j;
+    }
+    for (int i = 1; i < h; ++i) {
+        const double* prev = m + (size_t)(i - 1) * w;
+        for (int j = 0; j < w; ++j) {
+            const size_t idx = (size_t)i * w + j;
+            int from = -1;
+            double best = INFINITY;
+            if (j > 0 && prev[j - 1] + cl[idx] < best) {
+                best = prev[j - 1] + cl[idx];
+                from = j - 1;
+            }
+            if (prev[j] + cu[idx] < best) {
+                best = prev[j] + cu[idx];
+                from = j;
+            }
+            if (j < w - 1 && prev[j + 1] + cr[idx] < best) {
+                best = prev[j + 1] + cr[idx];
+                from = j + 1;
+            }
+            m[idx] = best;
+            b[idx] = from;
+        }
+    }
+    /* solvers.hpp:94-111 argmin (first index) + backtrack */
+    const double* last = m + (size_t)(h - 1) * w;
+    int c = 0;
+    for (int j = 1; j < w; ++j)
+        if (last[j] < last[c]) c = j;
+    seam[h - 1] = c;
+    for (int i = h - 1; i > 0; --i) seam[i - 1] = b[(size_t)i * w + seam[i]];
+    free(cl);
+    free(cu);
+    free(cr);
+    if (!m_out) free(m);
+    if (!b_out) free(b);
+    return OR_OK;
+}
+
+/* carver.hpp:191-214 carve_to_width with CarveConfig::forward / ::recompute
+ * (solve_step :153-173, carve_cached_state :176-188): forward solves
+ * dp_seam_forward on the current image's luma (recompute=true); recompute=false
+ * (backward) computes e1 once and then carves the map alongside the image. */
+static int carve_width_cfg(uint8_t* work, int w, int h, int target_w, int forward, int recompute,
+                           int** seams_cursor) {
+    double* e = (double*)malloc(sizeof(double) * (size_t)w * h);
+    double* e2 = (double*)malloc(sizeof(double) * (size_t)w * h);
+    uint8_t* tmp = (uint8_t*)malloc((size_t)w * h * 3);
+    int* seam = (int*)malloc(sizeof(int) * (size_t)h);
+    if (!e || !e2 || !tmp || !seam) return OR_NO_MEMORY;
+    if (!recompute && !forward) or_energy_e1_rgb(work, w, h, e);
+    for (int cw = w; cw > target_w; --cw) {
+        if (forward) {
+            or_to_grayscale(work, cw, h, e);
+            or_dp_seam_forward(e, cw, h, NULL, NULL, seam);
+        } else {
+            if (recompute) or_energy_e1_rgb(work, cw, h, e);
+            or_dp_seam(e, cw, h, NULL, NULL, seam);
+        }
+        or_remove_seam(work, cw, h, seam, h, tmp);
+        memcpy(work, tmp, (size_t)(cw - 1) * h * 3);
+        if (!recompute && !forward) { /* drop_columns (carver.hpp:57-67) on the cached map */
+            for (int i = 0; i < h; ++i) {
+                const double* src = e + (size_t)i * cw;
+                double* dst = e2 + (size_t)i * (cw - 1);
+                memcpy(dst, src, sizeof(double) * (size_t)seam[i]);
+                memcpy(dst + seam[i], src + seam[i] + 1, sizeof(double) * (size_t)(cw - seam[i] - 1));
+            }
+            memcpy(e, e2, sizeof(double) * (size_t)(cw - 1) * h);
+        }
+        if (seams_cursor && *seams_cursor) {
+            memcpy(*seams_cursor, seam, sizeof(int) * (size_t)h);
+            *seams_cursor += h;
+        }
+    }
+    free(e);
+    free(e2);
+    free(tmp);
+    free(seam);
+    return OR_OK;
+}
+
+/* run_resize (cli.hpp:242-259) with a CarveConfig (forward, recompute) */
+int or_carve_cfg(const uint8_t* rgb, int w, int h, int target_w, int target_h, int forward, int recompute,
+                 uint8_t* out, int* seams_out) {
+    if (w < 1 || h < 1) return OR_EMPTY_IMAGE;
+    if (target_w < 1 || target_w > w) return OR_INVALID_TARGET;
+    if (target_h < 1 || target_h > h) return OR_INVALID_TARGET;
+    uint8_t* work = (uint8_t*)malloc((size_t)w * h * 3);
+    if (!work) return OR_NO_MEMORY;
+    memcpy(work, rgb, (size_t)w * h * 3);
+    int* cursor = seams_out;
+    int st = carve_width_cfg(work, w, h, target_w, forward, recompute, &cursor);
+    const int cw = target_w;
+    if (!st && target_h != h) {
+        uint8_t* t = (uint8_t*)malloc((size_t)cw * h * 3);
+        if (!t) return OR_NO_MEMORY;
+        or_transpose(work, cw, h, t);
+        st = carve_width_cfg(t, h, cw, target_h, forward, recompute, &cursor);
+        or_transpose(t, target_h, cw, work);
+        free(t);
+    }
+    if (!st) memcpy(out, work, (size_t)cw * target_h * 3);
+    free(work);
+    return st;
+}
+
 /* carver.hpp:117-130 detail::insert_columns: one pixel per row right of
  * column cols[i] (stride `cs` between rows' entries), the channel-wise rounded
  * mean of its left and right neighbours, the right one clamped at the border. */

@@ -179,6 +179,67 @@ int ref_carve(const std::uint8_t* rgb, int w, int h, int target_w, int target_h,
     });
 }
 
+// energy.hpp:196-216 forward_costs on an arbitrary LumaGrid
+int ref_forward_costs(const double* luma, int w, int h, double* left, double* up, double* right) {
+    return guarded([&] {
+        carve_ref::LumaGrid g;
+        g.width = w;
+        g.height = h;
+        g.values.assign(luma, luma + size_t(w) * h);
+        auto fc = carve_ref::forward_costs(g);
+        std::memcpy(left, fc.cost_left.data(), fc.cost_left.size() * 8);
+        std::memcpy(up, fc.cost_up.data(), fc.cost_up.size() * 8);
+        std::memcpy(right, fc.cost_right.data(), fc.cost_right.size() * 8);
+    });
+}
+
+// solvers.hpp:294-326 dp_seam_forward(gray, forward_costs(gray))
+int ref_dp_seam_forward(const double* luma, int w, int h, double* m_out, int* b_out, int* seam_out) {
+    return guarded([&] {
+        carve_ref::LumaGrid g;
+        g.width = w;
+        g.height = h;
+        g.values.assign(luma, luma + size_t(w) * h);
+        auto r = carve_ref::dp_seam_forward(g, carve_ref::forward_costs(g));
+        std::memcpy(m_out, r.table.m.data(), r.table.m.size() * 8);
+        std::memcpy(b_out, r.table.b.data(), r.table.b.size() * 4);
+        std::memcpy(seam_out, r.seam.data(), r.seam.size() * 4);
+    });
+}
+
+// run_resize (cli.hpp:242-259) with CarveConfig::forward / ::recompute
+// (carver.hpp:15-24, 153-188); seams_out as ref_carve.
+int ref_carve_cfg(const std::uint8_t* rgb, int w, int h, int target_w, int target_h, int forward, int recompute,
+                  std::uint8_t* out, int* seams_out) {
+    return guarded([&] {
+        carve_ref::CarveConfig cfg;
+        cfg.forward = forward != 0;
+        cfg.recompute = recompute != 0;
+        carve_ref::PixelGrid img = grid_from(rgb, w, h);
+        size_t off = 0;
+        auto log = [&](const carve_ref::CarveReport& r) {
+            if (seams_out)
+                for (auto& s : r.seams) {
+                    std::memcpy(seams_out + off, s.data(), s.size() * sizeof(int));
+                    off += s.size();
+                }
+        };
+        if (target_w < 1 || target_w > img.width)
+            carve_ref::fail(carve_ref::Errc::invalid_target, "target width must be in [1, width]");
+        if (target_w < img.width) {
+            auto [carved, report] = carve_ref::carve_to_width(img, target_w, cfg);
+            img = std::move(carved);
+            log(report);
+        }
+        if (target_h != img.height) {
+            auto [carved, report] = carve_ref::carve_to_height(img, target_h, cfg);
+            img = std::move(carved);
+            log(report);
+        }
+        grid_to(img, out);
+    });
+}
+
 // carver.hpp:117-140 insert_seam (validate_seam + insert_columns)
 int ref_insert_seam(const std::uint8_t* rgb, int w, int h, const int* seam, int n, std::uint8_t* out) {
     return guarded([&] { grid_to(carve_ref::insert_seam(grid_from(rgb, w, h), carve_ref::Seam(seam, seam + n)), out); });

@@ -25,7 +25,7 @@ __all__ = [
     "CarveReport", "CostTable", "SeamResult", "make_test_image", "to_grayscale", "energy_e1", "compute_energy",
     "energy_e1_rgb", "dp_seam", "parallel_dp_seam", "find_seam", "validate_seam", "remove_seam", "transpose",
     "carve_to_width", "carve_to_height", "carve", "carve_batch", "carve_device", "carve_batch_device",
-    "insert_seam", "record_seams", "enlarge_to_width", "enlarge",
+    "insert_seam", "record_seams", "enlarge_to_width", "enlarge", "forward_costs", "dp_seam_forward",
     "library", "library_path", "device_count", "launch_count", "reset_launch_count",
 ]
 
@@ -172,9 +172,12 @@ def library() -> C.CDLL:
             "carve_cuda_validate_seam": ([vp, i, i, i], i),
             "carve_cuda_remove_seam_rgb": ([vp, i, i, vp, i, vp], i),
             "carve_cuda_insert_seam_rgb": ([vp, i, i, vp, i, vp], i),
-            "carve_cuda_record_seams": ([vp, i, i, i, vp, vp], i),
-            "carve_cuda_enlarge": ([vp, i, i, i, i, vp, vp], i),
+            "carve_cuda_record_seams": ([vp, i, i, i, vp, vp, vp], i),
+            "carve_cuda_enlarge": ([vp, i, i, i, i, vp, vp, vp], i),
             "carve_cuda_carve": ([vp, i, i, i, i, vp, vp, vp], i),
+            "carve_cuda_carve_cfg": ([vp, i, i, i, i, vp, vp, vp, vp], i),
+            "carve_cuda_forward_costs": ([vp, i, i, vp, vp, vp], i),
+            "carve_cuda_dp_seam_forward": ([vp, i, i, vp, vp, vp], i),
             "carve_cuda_carve_batch": ([vp, i, i, i, i, i, vp, vp, i], i),
             "carve_cuda_carve_device": ([vp, i, i, i, i, vp, vp, vp], i),
             "carve_cuda_carve_batch_device": ([vp, i, i, i, i, i, vp, vp], i),
@@ -356,16 +359,22 @@ def _check_config(cfg: CarveConfig | None) -> None:
         raise CarveError(Errc.usage_error, "forward energy requires the dp or pardp solver")  # carver.hpp:51-54
     if SolverKind(cfg.solver) not in (SolverKind.Dynamic, SolverKind.ParallelDynamic):
         _unsupported(f"solver {SolverKind(cfg.solver).value}")
-    if EnergyFn(cfg.energy_fn) is not EnergyFn.e1:
+    if not cfg.forward and EnergyFn(cfg.energy_fn) is not EnergyFn.e1:
         _unsupported(f"energy function {EnergyFn(cfg.energy_fn).value}")
-    if cfg.forward:
-        _unsupported("forward energy")
-    # cfg.recompute=False carves the stale map (carver.hpp:175-187) and is not the
-    # bit-exact default path; the engine always produces the recompute=True result.
+
+
+class _Config(C.Structure):  # carve_cuda_config
+    _fields_ = [("forward", C.c_int), ("recompute", C.c_int)]
+
+
+def _abi_config(cfg: CarveConfig | None = None, forward: bool = False, recompute: bool = True):
+    if cfg is not None:
+        forward, recompute = cfg.forward, cfg.recompute
+    return _Config(int(bool(forward)), int(bool(recompute)))
 
 
 def carve(img: np.ndarray, target_width: int, target_height: int | None = None, *, seams: bool = False,
-          timings: bool = False, out: np.ndarray | None = None):
+          timings: bool = False, out: np.ndarray | None = None, forward: bool = False, recompute: bool = True):
     """run_resize semantics (cli.hpp:249-256): carve_to_width then carve_to_height.
     Returns the carved image, plus (seams, timings) lists when requested. `out`
     (optional, C-contiguous uint8 target_height x target_width x 3, e.g. pinned
@@ -386,8 +395,13 @@ def carve(img: np.ndarray, target_width: int, target_height: int | None = None, 
     nseams = (w - tw) + (h - th)
     s = np.empty(max(n_ints, 1), np.int32)
     t = (_Timing * max(nseams, 1))()
-    _check(library().carve_cuda_carve(_ptr(a), w, h, tw, th, _ptr(out), _ptr(s) if seams else None,
-                                      C.cast(t, C.c_void_p) if timings else None))
+    if forward or not recompute:  # CarveConfig::forward / ::recompute (carver.hpp:15-24)
+        cfg = _abi_config(forward=forward, recompute=recompute)
+        _check(library().carve_cuda_carve_cfg(_ptr(a), w, h, tw, th, C.byref(cfg), _ptr(out),
+                                              _ptr(s) if seams else None, C.cast(t, C.c_void_p) if timings else None))
+    else:
+        _check(library().carve_cuda_carve(_ptr(a), w, h, tw, th, _ptr(out), _ptr(s) if seams else None,
+                                          C.cast(t, C.c_void_p) if timings else None))
     if not (seams or timings):
         return out
     seam_list = []
@@ -416,8 +430,37 @@ def carve_to_width(img: np.ndarray, target_width: int, cfg: CarveConfig | None =
         raise CarveError(Errc.invalid_target, "target width must be in [1, width]")
     _check_config(cfg)
     t0 = time.perf_counter()
-    out, seams, tims = carve(a, target_width, h, seams=True, timings=True)
+    c = cfg or CarveConfig()
+    out, seams, tims = carve(a, target_width, h, seams=True, timings=True, forward=c.forward, recompute=c.recompute)
     return out, _report(seams, tims, time.perf_counter() - t0)
+
+
+def forward_costs(luma: np.ndarray):
+    """energy.hpp:196-216 -> (cost_left, cost_up, cost_right), on the device."""
+    g = np.ascontiguousarray(luma, dtype=np.float64)
+    h, w = g.shape
+    outs = [np.empty((h, w), np.float64) for _ in range(3)]
+    _check(library().carve_cuda_forward_costs(_ptr(g), w, h, *[_ptr(o) for o in outs]))
+    return tuple(outs)
+
+
+def dp_seam_forward(luma: np.ndarray, costs=None) -> SeamResult:
+    """solvers.hpp:294-326 forward-energy DP. The device derives the transition
+    costs from `luma`; `costs` (if given) must equal forward_costs(luma)."""
+    g = np.ascontiguousarray(luma, dtype=np.float64)
+    if g.ndim != 2 or g.size == 0:
+        raise CarveError(Errc.empty_image, "image is empty")
+    h, w = g.shape
+    if costs is not None:
+        if any(np.shape(c) != (h, w) for c in costs):
+            raise CarveError(Errc.dimension_mismatch, "forward costs do not match image dimensions")
+        if not all(np.array_equal(a, b) for a, b in zip(costs, forward_costs(g))):
+            _unsupported("dp_seam_forward with costs other than forward_costs(gray)")
+    m = np.empty((h, w), np.float64)
+    b = np.empty((h, w), np.int32)
+    seam = np.empty(h, np.int32)
+    _check(library().carve_cuda_dp_seam_forward(_ptr(g), w, h, _ptr(m), _ptr(b), _ptr(seam)))
+    return SeamResult(seam, CostTable(w, h, m, b))
 
 
 def insert_seam(img: np.ndarray, seam) -> np.ndarray:
@@ -442,14 +485,16 @@ def record_seams(img: np.ndarray, count: int, cfg: CarveConfig | None = None):
     t0 = time.perf_counter()
     s = np.empty((max(count, 0), h), np.int32)
     t = (_Timing * max(count, 1))()
-    _check(library().carve_cuda_record_seams(_ptr(a), w, h, count, _ptr(s) if count > 0 else None,
+    c = _abi_config(cfg)
+    _check(library().carve_cuda_record_seams(_ptr(a), w, h, count, C.byref(c), _ptr(s) if count > 0 else None,
                                              C.cast(t, C.c_void_p)))
     seams = [s[k].copy() for k in range(count)]
     tims = [SeamTiming(t[k].energy_s, t[k].solve_s, t[k].remove_s) for k in range(count)]
     return seams, _report(seams, tims, time.perf_counter() - t0)
 
 
-def enlarge(img: np.ndarray, target_width: int, target_height: int | None = None, *, seams: bool = False):
+def enlarge(img: np.ndarray, target_width: int, target_height: int | None = None, *, seams: bool = False,
+            cfg: CarveConfig | None = None):
     """run_enlarge (cli.hpp:262-277): enlarge_to_width on the width, then on the
     transpose for the height. Returns the image (plus the recorded seams of both
     phases, concatenated, when `seams`)."""
@@ -460,7 +505,8 @@ def enlarge(img: np.ndarray, target_width: int, target_height: int | None = None
     n = max(tw - w, 0) * h + max(th - h, 0) * tw
     out = np.empty((max(th, 0), max(tw, 0), 3), np.uint8)
     s = np.empty(max(n, 1), np.int32)
-    _check(library().carve_cuda_enlarge(_ptr(a), w, h, tw, th, _ptr(out), _ptr(s)))
+    c = _abi_config(cfg)
+    _check(library().carve_cuda_enlarge(_ptr(a), w, h, tw, th, C.byref(c), _ptr(out), _ptr(s)))
     return (out, s[:n]) if seams else out
 
 
@@ -471,7 +517,7 @@ def enlarge_to_width(img: np.ndarray, target_width: int, cfg: CarveConfig | None
     h, w, _ = a.shape
     _check_config(cfg)
     t0 = time.perf_counter()
-    out, flat = enlarge(a, target_width, h, seams=True)
+    out, flat = enlarge(a, target_width, h, seams=True, cfg=cfg)
     k = int(target_width) - w
     seams = [flat[t * h:(t + 1) * h].copy() for t in range(k)]
     return out, _report(seams, [SeamTiming(0.0, 0.0, 0.0) for _ in range(k)], time.perf_counter() - t0)
@@ -486,7 +532,8 @@ def carve_to_height(img: np.ndarray, target_height: int, cfg: CarveConfig | None
         raise CarveError(Errc.invalid_target, "target height must be in [1, height]")
     _check_config(cfg)
     t0 = time.perf_counter()
-    out, seams, tims = carve(a, w, target_height, seams=True, timings=True)
+    c = cfg or CarveConfig()
+    out, seams, tims = carve(a, w, target_height, seams=True, timings=True, forward=c.forward, recompute=c.recompute)
     return out, _report(seams, tims, time.perf_counter() - t0)
 
 

@@ -270,6 +270,10 @@ struct Dp2Variant {
     const void* fn_tables; // parity-API kernel (writes the full cost / predecessor tables)
     const void* fn_prof;   // hot kernel + clock64 phase counters (tools)
     const void* fn_fused;  // hot kernel, energy recomputed from RGBX (batch mode)
+    const void* fn_fwd;    // forward energy from RGBX rows (fused), hot / with tables
+    const void* fn_fwd_tables;
+    const void* fn_fwdp;   // forward energy from an FP64 luma plane (dp_seam_forward API)
+    const void* fn_fwdp_tables;
     size_t (*smem)(int nblk, int D);
     int S() const { return 32 * C - 2 * K; }
     int cols() const { return NW * S(); }
@@ -279,6 +283,8 @@ template <int C, int K, int NW, int D>
 constexpr Dp2Variant dp2_variant() {
     return Dp2Variant{C, K, NW, D, (const void*)k_dp2<C, K, NW, D, 0>, (const void*)k_dp2<C, K, NW, D, 1>,
                       (const void*)k_dp2<C, K, NW, D, 2>, (const void*)k_dp2<C, K, NW, D, 0, true>,
+                      (const void*)k_dp2<C, K, NW, D, 0, true, true>, (const void*)k_dp2<C, K, NW, D, 1, true, true>,
+                      (const void*)k_dp2<C, K, NW, D, 0, false, true>, (const void*)k_dp2<C, K, NW, D, 1, false, true>,
                       &Dp2Smem<C, K, NW>::total};
 }
 
@@ -298,7 +304,8 @@ constexpr int kNumDp2Variants = int(sizeof(kDp2Variants) / sizeof(kDp2Variants[0
 
 void init_kernel_attributes(Ctx& c) {
     for (const Dp2Variant& v : kDp2Variants)
-        for (const void* fn : {v.fn, v.fn_tables, v.fn_prof, v.fn_fused}) {
+        for (const void* fn :
+             {v.fn, v.fn_tables, v.fn_prof, v.fn_fused, v.fn_fwd, v.fn_fwd_tables, v.fn_fwdp, v.fn_fwdp_tables}) {
             ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kDpSmemBudget),
                "cudaFuncSetAttribute(dp2 smem)");
             ck(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
@@ -353,13 +360,15 @@ Dp2Plan dp2_plan(int W, int H, bool batch = false) {
                                       std::to_string(H));
 }
 
-void launch_dp2(Ctx& c, const Dp2Plan& pl, Dp2Params p, int nimg, cudaStream_t s, bool fused = false) {
+void launch_dp2(Ctx& c, const Dp2Plan& pl, Dp2Params p, int nimg, cudaStream_t s, bool fused = false,
+                bool forward = false) {
     const Dp2Variant& v = *pl.v;
     p.G = pl.ncl * v.NW;
     p.nblk = pl.nblk;
     p.gather = pl.gather;
     p.dbg = env_int("CARVE_DP_DBG", 0);
-    const void* fn = fused ? v.fn_fused : p.m_out ? v.fn_tables : (p.prof ? v.fn_prof : v.fn);
+    const void* fn = forward ? (fused ? (p.m_out ? v.fn_fwd_tables : v.fn_fwd) : (p.m_out ? v.fn_fwdp_tables : v.fn_fwdp))
+                     : fused ? v.fn_fused : p.m_out ? v.fn_tables : (p.prof ? v.fn_prof : v.fn);
     if (c.smem_set.find(fn) == c.smem_set.end()) fail(CARVE_E_CUDA, "DP kernel attributes not initialised");
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(nimg * pl.ncl));
@@ -494,8 +503,25 @@ void check_targets(int w, int h, int tw, int th) {
 // [4: energy full start/end for phase A, phase B]
 size_t stamp_words(const CarveGeometry& g) { return size_t(g.nseams) * 4 + 4; }
 
+// CarveConfig fields that change the device loop (carver.hpp:15-24)
+struct CarveOpts {
+    bool forward = false;   // forward energy: dp_seam_forward on the current luma (fused DP, FWD cells)
+    bool recompute = true;  // false: e1 once per phase, then the map is only carved (no fix-up)
+};
+
+CarveOpts opts_of(const carve_cuda_config* cfg) {
+    CarveOpts o;
+    if (cfg) {
+        o.forward = cfg->forward != 0;
+        o.recompute = cfg->recompute != 0;
+    }
+    if (o.forward && !o.recompute)
+        fail(CARVE_E_USAGE_ERROR, "forward energy with recompute=false is not supported by the B200 engine");
+    return o;
+}
+
 void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const CarveGeometry& g, int* d_seams,
-               size_t seam_istride, unsigned long long* d_stamps, cudaStream_t s) {
+               size_t seam_istride, unsigned long long* d_stamps, cudaStream_t s, CarveOpts o = {}) {
     const long long in_is = (long long)g.w * g.h * 3, out_is = (long long)g.tw * g.th * 3;
     // logical column 0 of each padded RGBX plane ([1]: transpose target only)
     uint32_t* rgb[2] = {c.rgb[0].as<uint32_t>() + EPAD_L, c.rgb[1].p ? c.rgb[1].as<uint32_t>() + EPAD_L : nullptr};
@@ -514,8 +540,10 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
     // in-place removal. Nothing returns to the host between seams.
     // Batches run the fused DP (energy recomputed from RGBX, no energy plane);
     // single images keep the incremental energy plane. CARVE_FUSED=0/1 overrides.
+    // Forward energy always runs fused (transition costs from the RGBX rows);
+    // recompute=false needs the carried energy plane.
     const int fused_env = env_int("CARVE_FUSED", -1);
-    const bool fused = fused_env >= 0 ? fused_env != 0 : nimg > 1;
+    const bool fused = o.forward || (o.recompute && (fused_env >= 0 ? fused_env != 0 : nimg > 1));
     // `finish`: what the phase's last removal writes (fused with K4, see k_compact_transpose):
     // OUT_PLANE  the transposed RGBX plane for the height phase (rgb[cur ^ 1], pitch_b)
     // OUT_PACKED the final image, transposed back, packed RGB into d_out
@@ -556,11 +584,11 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
                 q.rpitch = pitch;
                 q.rgb_istride = pis;
                 // fix up the energy around the previous seam (removed from width W + 1)
-                if (k > 0 && !fused) q.prev_seam = seam - H;
+                if (k > 0 && !fused && o.recompute) q.prev_seam = seam - H;
                 // algorithmic: 8 B FP64 energy read per cell (no direction
                 // plane); fused: 4 B RGBX read per cell
                 Prof pr(c, s, KK_DP, (fused ? 4.0 : 8.0) * W * H * nimg);
-                launch_dp2(c, pl, q, nimg, s, fused);
+                launch_dp2(c, pl, q, nimg, s, fused, o.forward);
             }
             CompactParams q{};
             const bool last = (k + 1 == ntake);
@@ -694,13 +722,14 @@ void launch_expand_rows(const uint8_t* in, int W, int H, const int* cols, int co
 // record_seams (carver.hpp:226-262) on a packed device image: the ordinary
 // device carve loop to width w - count (its output is discarded), then the
 // logged seams mapped back to original coordinates. d_orig: count * h ints.
-void record_device(Ctx& c, const uint8_t* d_in, int w, int h, int count, int* d_orig, unsigned long long* d_st) {
+void record_device(Ctx& c, const uint8_t* d_in, int w, int h, int count, int* d_orig, unsigned long long* d_st,
+                   CarveOpts o = {}) {
     if (count <= 0) return;
     const CarveGeometry g = geometry(w, h, w - count, h);
     ensure_carve_buffers(c, g, 1);
     int* d_log = static_cast<int*>(c.seams.ensure(std::max<size_t>(g.seam_ints, 1) * 4));
     uint8_t* d_scratch = static_cast<uint8_t*>(c.scratch_a.ensure(size_t(w - count) * h * 3));
-    run_carve(c, d_in, d_scratch, 1, g, d_log, g.seam_ints, d_st, c.stream);
+    run_carve(c, d_in, d_scratch, 1, g, d_log, g.seam_ints, d_st, c.stream, o);
     launch_seams_to_original(d_log, count, h, d_orig, c.stream);
 }
 
@@ -719,7 +748,7 @@ void check_enlarge(int w, int target) {
 }
 
 void carve_one_host(Ctx& c, const uint8_t* rgb, int w, int h, int tw, int th, uint8_t* out, int32_t* seams_out,
-                    carve_seam_timing* timings) {
+                    carve_seam_timing* timings, CarveOpts o = {}) {
     const CarveGeometry g = geometry(w, h, tw, th);
     cudaStream_t s = c.stream;
     const size_t in_bytes = size_t(w) * h * 3, out_bytes = size_t(tw) * th * 3;
@@ -733,7 +762,7 @@ void carve_one_host(Ctx& c, const uint8_t* rgb, int w, int h, int tw, int th, ui
         ck(cudaMemsetAsync(d_st, 0, stamp_words(g) * 8, s), "memset stamps");
     }
     ck(cudaMemcpyAsync(d_in, rgb, in_bytes, cudaMemcpyHostToDevice, s), "H2D rgb");
-    run_carve(c, d_in, d_out, 1, g, d_seams, g.seam_ints, d_st, s);
+    run_carve(c, d_in, d_out, 1, g, d_seams, g.seam_ints, d_st, s, o);
     ck(cudaMemcpyAsync(out, d_out, out_bytes, cudaMemcpyDeviceToHost, s), "D2H rgb");
     if (seams_out && g.seam_ints)
         ck(cudaMemcpyAsync(seams_out, d_seams, g.seam_ints * 4, cudaMemcpyDeviceToHost, s), "D2H seams");
@@ -970,11 +999,12 @@ carve_status carve_cuda_insert_seam_rgb(const uint8_t* rgb, int w, int h, const 
     });
 }
 
-carve_status carve_cuda_record_seams(const uint8_t* rgb, int w, int h, int count, int32_t* seams_out,
-                                     carve_seam_timing* timings_out) {
+carve_status carve_cuda_record_seams(const uint8_t* rgb, int w, int h, int count, const carve_cuda_config* cfg,
+                                     int32_t* seams_out, carve_seam_timing* timings_out) {
     return guarded([&] {
         if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "PixelGrid dimensions must be >= 1");
         if (count < 0 || count > w - 1) fail(CARVE_E_INVALID_TARGET, "cannot record more seams than width-1");
+        const CarveOpts o = opts_of(cfg);
         if (count == 0) return;
         Ctx& c = ctx();
         uint8_t* d_in = static_cast<uint8_t*>(c.packed_in.ensure(size_t(w) * h * 3));
@@ -986,7 +1016,7 @@ carve_status carve_cuda_record_seams(const uint8_t* rgb, int w, int h, int count
             ck(cudaMemsetAsync(d_st, 0, stamp_words(g) * 8, c.stream), "memset stamps");
         }
         ck(cudaMemcpyAsync(d_in, rgb, size_t(w) * h * 3, cudaMemcpyHostToDevice, c.stream), "H2D");
-        record_device(c, d_in, w, h, count, d_orig, d_st);
+        record_device(c, d_in, w, h, count, d_orig, d_st, o);
         ck(cudaMemcpyAsync(seams_out, d_orig, size_t(count) * h * 4, cudaMemcpyDeviceToHost, c.stream), "D2H seams");
         std::vector<unsigned long long> st;
         if (timings_out) {
@@ -998,12 +1028,13 @@ carve_status carve_cuda_record_seams(const uint8_t* rgb, int w, int h, int count
     });
 }
 
-carve_status carve_cuda_enlarge(const uint8_t* rgb, int w, int h, int target_w, int target_h, uint8_t* rgb_out,
-                                int32_t* seams_out) {
+carve_status carve_cuda_enlarge(const uint8_t* rgb, int w, int h, int target_w, int target_h,
+                                const carve_cuda_config* cfg, uint8_t* rgb_out, int32_t* seams_out) {
     return guarded([&] {
         if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "PixelGrid dimensions must be >= 1");
         if (target_w != w) check_enlarge(w, target_w);
         if (target_h != h) check_enlarge(h, target_h);
+        const CarveOpts o = opts_of(cfg);
         Ctx& c = ctx();
         const int kw = target_w - w, kh = target_h - h;
         const size_t big = size_t(target_w) * target_h * 3;
@@ -1017,14 +1048,14 @@ carve_status carve_cuda_enlarge(const uint8_t* rgb, int w, int h, int target_w, 
         ck(cudaMemcpyAsync(d_in, rgb, size_t(w) * h * 3, cudaMemcpyHostToDevice, c.stream), "H2D");
         const uint8_t* cur = d_in;
         if (kw > 0) {  // enlarge_to_width (carver.hpp:266-285)
-            record_device(c, d_in, w, h, kw, d_orig, nullptr);
+            record_device(c, d_in, w, h, kw, d_orig, nullptr, o);
             launch_expand_rows(d_in, w, h, d_orig, kw, h, e0, c.stream);
             cur = e0;
         }
         if (kh > 0) {  // the height: enlarge_to_width of the transpose (cli.hpp:271-274)
             int* d_orig_h = d_orig + size_t(kw) * h;
             transpose_packed(c, cur, target_w, h, e1p);  // h wide, target_w high
-            record_device(c, e1p, h, target_w, kh, d_orig_h, nullptr);
+            record_device(c, e1p, h, target_w, kh, d_orig_h, nullptr, o);
             launch_expand_rows(e1p, h, target_w, d_orig_h, kh, target_w, e2, c.stream);
             transpose_packed(c, e2, target_h, target_w, d_out);
             cur = d_out;
@@ -1070,6 +1101,78 @@ carve_status carve_cuda_carve(const uint8_t* rgb, int w, int h, int target_w, in
         check_targets(w, h, target_w, target_h);
         Ctx& c = ctx();
         carve_one_host(c, rgb, w, h, target_w, target_h, rgb_out, seams_out, timings_out);
+    });
+}
+
+carve_status carve_cuda_carve_cfg(const uint8_t* rgb, int w, int h, int target_w, int target_h,
+                                  const carve_cuda_config* cfg, uint8_t* rgb_out, int32_t* seams_out,
+                                  carve_seam_timing* timings_out) {
+    return guarded([&] {
+        check_targets(w, h, target_w, target_h);
+        const CarveOpts o = opts_of(cfg);
+        Ctx& c = ctx();
+        carve_one_host(c, rgb, w, h, target_w, target_h, rgb_out, seams_out, timings_out, o);
+    });
+}
+
+carve_status carve_cuda_forward_costs(const double* luma, int w, int h, double* left, double* up, double* right) {
+    return guarded([&] {
+        if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "LumaGrid dimensions must be >= 1");
+        Ctx& c = ctx();
+        const size_t n = size_t(w) * h;
+        double* l = static_cast<double*>(c.scratch_a.ensure(n * 8 * 4));
+        ck(cudaMemcpyAsync(l, luma, n * 8, cudaMemcpyHostToDevice, c.stream), "H2D luma");
+        k_forward_costs<<<grid_for((long long)n, 256), 256, 0, c.stream>>>(l, w, h, l + n, l + 2 * n, l + 3 * n);
+        LAUNCHED("k_forward_costs");
+        ck(cudaMemcpyAsync(left, l + n, n * 8, cudaMemcpyDeviceToHost, c.stream), "D2H left");
+        ck(cudaMemcpyAsync(up, l + 2 * n, n * 8, cudaMemcpyDeviceToHost, c.stream), "D2H up");
+        ck(cudaMemcpyAsync(right, l + 3 * n, n * 8, cudaMemcpyDeviceToHost, c.stream), "D2H right");
+        sync(c);
+    });
+}
+
+carve_status carve_cuda_dp_seam_forward(const double* luma, int w, int h, double* m_out, int32_t* b_out,
+                                        int32_t* seam_out) {
+    return guarded([&] {
+        if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "image is empty");
+        if ((m_out == nullptr) != (b_out == nullptr)) fail(CARVE_E_USAGE_ERROR, "m_out and b_out go together");
+        Ctx& c = ctx();
+        const Dp2Plan pl = dp2_plan(w, h);
+        const int pitch = int(round_up(w, 32));
+        const int epitch = padded_epitch(w);
+        // the luma plane streams through the DP like an energy plane; its columns
+        // -1 and w replicate the edge columns (at_clamped, raster.hpp:54-58)
+        double* dl = static_cast<double*>(c.e[0].ensure(size_t(epitch) * (h + EPAD_B) * 8)) + EPAD_L;
+        double* mb = static_cast<double*>(c.mbound.ensure(size_t(pl.nblk + 1) * pitch * 8));
+        int* dseam = static_cast<int*>(c.seams.ensure(size_t(h) * 4));
+        double* dm = nullptr;
+        int* db = nullptr;
+        if (m_out) {
+            dm = static_cast<double*>(c.scratch_a.ensure(size_t(w) * h * 8));
+            db = static_cast<int*>(c.scratch_b.ensure(size_t(w) * h * 4));
+        }
+        ck(cudaMemcpy2DAsync(dl, size_t(epitch) * 8, luma, size_t(w) * 8, size_t(w) * 8, h, cudaMemcpyHostToDevice,
+                             c.stream),
+           "H2D luma");
+        k_edge_replicas_f64<<<grid_for(h, 256), 256, 0, c.stream>>>(dl, epitch, w, h);
+        LAUNCHED("k_edge_replicas_f64");
+        Dp2Params p{};
+        p.e = dl;
+        p.epitch = epitch;
+        p.W = w;
+        p.H = h;
+        p.mbound = mb;
+        p.mpitch = pitch;
+        p.seam = dseam;
+        p.m_out = dm;
+        p.b_out = db;
+        launch_dp2(c, pl, p, 1, c.stream, false, true);
+        ck(cudaMemcpyAsync(seam_out, dseam, size_t(h) * 4, cudaMemcpyDeviceToHost, c.stream), "D2H seam");
+        if (m_out) {
+            ck(cudaMemcpyAsync(m_out, dm, size_t(w) * h * 8, cudaMemcpyDeviceToHost, c.stream), "D2H m");
+            ck(cudaMemcpyAsync(b_out, db, size_t(w) * h * 4, cudaMemcpyDeviceToHost, c.stream), "D2H b");
+        }
+        sync(c);
     });
 }
 

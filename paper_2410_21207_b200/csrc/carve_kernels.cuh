@@ -713,6 +713,35 @@ __global__ void __launch_bounds__(256) k_compact_warp(CompactParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// Forward energy helpers
+
+// forward_costs (energy.hpp:196-216) of an arbitrary luma plane (the API entry;
+// the carve loop computes the same costs in registers inside the DP)
+__global__ void k_forward_costs(const double* __restrict__ g, int W, int H, double* __restrict__ left,
+                                double* __restrict__ up, double* __restrict__ right) {
+    const long long n = (long long)W * H;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const int i = int(k / W), j = int(k - (long long)i * W);
+        const double* row = g + (long long)i * W;
+        const double l = row[max(j - 1, 0)], r = row[min(j + 1, W - 1)];
+        const double a = g[(long long)max(i - 1, 0) * W + j];
+        const double cu = fabs(__dsub_rn(r, l));
+        up[k] = cu;
+        left[k] = __dadd_rn(cu, fabs(__dsub_rn(a, l)));
+        right[k] = __dadd_rn(cu, fabs(__dsub_rn(a, r)));
+    }
+}
+
+// columns -1 and W of a padded FP64 plane replicate columns 0 and W-1
+__global__ void k_edge_replicas_f64(double* __restrict__ e, int epitch, int W, int H) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < H; i += gridDim.x * blockDim.x) {
+        double* row = e + (long long)i * epitch;
+        row[-1] = row[0];
+        row[W] = row[W - 1];
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Seam recording and enlargement
 
 // record_seams (carver.hpp:226-262) reports each seam in original-image

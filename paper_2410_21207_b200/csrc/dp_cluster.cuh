@@ -125,6 +125,36 @@ __device__ __forceinline__ void dp_cell_left_last(double L, double M, double R, 
     d = left ? 0 : td;
 }
 
+// Forward-energy cell (dp_seam_forward, solvers.hpp:304-323): the candidates
+// are prev + transition cost, compared in the order left, up, right with strict
+// < (smallest column on ties). Out-of-image neighbours are +inf (pads), so
+// `best = left` first is the reference's `best = +inf` start.
+__device__ __forceinline__ void fwd_cell(double L, double M, double R, int lL, int lM, int lR, double cl, double cu,
+                                         double cr, double& out, int& lab, int& d) {
+    double best = __dadd_rn(L, cl);
+    int bl = lL;
+    d = 0;
+    const double mv = __dadd_rn(M, cu);
+    if (mv < best) { best = mv; bl = lM; d = 1; }
+    const double rv = __dadd_rn(R, cr);
+    if (rv < best) { best = rv; bl = lR; d = 2; }
+    out = best;
+    lab = bl;
+}
+// same cell with the shuffled left operand compared last (see dp_cell_left_last)
+__device__ __forceinline__ void fwd_cell_left_last(double L, double M, double R, int lL, int lM, int lR, double cl,
+                                                   double cu, double cr, double& out, int& lab, int& d) {
+    double t = __dadd_rn(M, cu);
+    int tl = lM, td = 1;
+    const double rv = __dadd_rn(R, cr);
+    if (rv < t) { t = rv; tl = lR; td = 2; }
+    const double lv = __dadd_rn(L, cl);
+    const bool left = lv <= t;
+    out = left ? lv : t;
+    lab = left ? lL : tl;
+    d = left ? 0 : td;
+}
+
 template <int C>
 __device__ __forceinline__ void load_row(const double* __restrict__ row, int col0, double (&v)[C]) {
 #pragma unroll
@@ -201,6 +231,30 @@ __device__ __forceinline__ void energy_cols(const double (&Lp)[C], const double 
     }
 }
 
+// forward_costs (energy.hpp:196-216) of a lane's C columns from the luma rows
+// above (Lp) and current (Lc): cu = |R - L|, cl = cu + |A - L|, cr = cu + |A - R|,
+// horizontal neighbours clamped through the RGBX replica columns; +inf outside.
+template <int C>
+__device__ __forceinline__ void fwd_cols(const double (&Lp)[C], const double (&Lc)[C], uint32_t oob, double (&cl)[C],
+                                         double (&cu)[C], double (&cr)[C]) {
+    const double lL = __shfl_up_sync(FULL, Lc[C - 1], 1);
+    const double lR = __shfl_down_sync(FULL, Lc[0], 1);
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+        const double left = k > 0 ? Lc[k - 1] : lL;
+        const double right = k + 1 < C ? Lc[k + 1] : lR;
+        const double up = fabs(__dsub_rn(right, left));
+        cu[k] = up;
+        cl[k] = __dadd_rn(up, fabs(__dsub_rn(Lp[k], left)));
+        cr[k] = __dadd_rn(up, fabs(__dsub_rn(Lp[k], right)));
+    }
+    if (oob) {
+#pragma unroll
+        for (int k = 0; k < C; ++k)
+            if (oob >> k & 1) cl[k] = cu[k] = cr[k] = dinf();
+    }
+}
+
 template <int C>
 __device__ __forceinline__ void luma_cols(const uint32_t* px, double (&L)[C]) {
 #pragma unroll
@@ -216,7 +270,12 @@ __device__ __forceinline__ void argmin_combine(double& v, int& i, double ov, int
 // FUSED: no energy plane — e1 is recomputed in registers from RGBX rows
 // streamed through the same ring (rolling three luma rows per lane). Used for
 // batches, where the energy plane's 16 B/px/seam of traffic bounds throughput.
-template <int C, int K, int NWARP, int D, int MODE, bool FUSED = false>
+// FWD: forward energy (CarveConfig::forward, carver.hpp:155-169): the cells take
+// dp_seam_forward's transition costs, computed in registers from the luma rows
+// above and current — from RGBX rows (FUSED) or, for the dp_seam_forward API,
+// from an FP64 luma plane streamed through the ring in place of the energy
+// plane (its columns -1 and W replicate the edge columns, like the RGBX planes).
+template <int C, int K, int NWARP, int D, int MODE, bool FUSED = false, bool FWD = false>
 __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     constexpr bool TABLES = MODE == 1;
     constexpr bool PROF = MODE == 2;
@@ -338,7 +397,19 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
         luma_cols<C>(px, Ln);
 #pragma unroll
         for (int k = 0; k < C; ++k) Lp[k] = Lc[k];
-        energy_cols<C>(Lp, Lc, Ln, oob, m);  // M[0] = e[0]
+        if constexpr (FWD) {  // M[0] = cost_up(0, j) (solvers.hpp:300-302)
+            double cl0[C], cr0[C];
+            fwd_cols<C>(Lc, Lc, oob, cl0, m, cr0);
+        } else {
+            energy_cols<C>(Lp, Lc, Ln, oob, m);  // M[0] = e[0]
+        }
+    } else if constexpr (FWD) {  // luma plane: row 0's luma, M[0] = cost_up(0, j)
+#pragma unroll
+        for (int k = 0; k < C; ++k)
+            if (col0 + k < 0 || col0 + k >= W) oob |= 1u << k;
+        load_row<C>(e, col0, Lc);
+        double cl0[C], cr0[C];
+        fwd_cols<C>(Lc, Lc, oob, cl0, m, cr0);
     } else {
         load_row<C>(e, col0, m);
     }
@@ -383,7 +454,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
 
     auto step = [&](int u, int i) {
         cp_async_wait<D - 1>();  // the oldest of the D groups in flight has landed
-        double ev[C];
+        double ev[C], fcl[C], fcu[C], fcr[C];  // energies, or forward transition costs (FWD)
         if constexpr (FUSED) {
             const uint32_t* src = reinterpret_cast<const uint32_t*>(ring_s + ((size_t(warp) * D + u) * 32 + lane) * C);
             uint32_t px[C];
@@ -392,7 +463,8 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
 #pragma unroll
             for (int k = 0; k < C; ++k) { Lp[k] = Lc[k]; Lc[k] = Ln[k]; }
             luma_cols<C>(px, Ln);  // row i+1 (clamped at the bottom)
-            energy_cols<C>(Lp, Lc, Ln, oob, ev);
+            if constexpr (FWD) fwd_cols<C>(Lp, Lc, oob, fcl, fcu, fcr);
+            else energy_cols<C>(Lp, Lc, Ln, oob, ev);
         } else {
             const double* src = ring_s + ((size_t(warp) * D + u) * 32 + lane) * C;
 #pragma unroll
@@ -400,6 +472,11 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
                 const double2 x = *reinterpret_cast<const double2*>(src + k);
                 ev[k] = x.x;
                 ev[k + 1] = x.y;
+            }
+            if constexpr (FWD) {  // the ring row is luma row i
+#pragma unroll
+                for (int k = 0; k < C; ++k) { Lp[k] = Lc[k]; Lc[k] = ev[k]; }
+                fwd_cols<C>(Lp, Lc, oob, fcl, fcu, fcr);
             }
         }
         const double lm = __shfl_up_sync(FULL, m[C - 1], 1);
@@ -416,8 +493,13 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
             const double nm = (k + 1 < C) ? m[k + 1] : rm;
             const int nl = (k + 1 < C) ? lab[k + 1] : rl;
             int d;
-            if (k == 0) dp_cell_left_last(pm, cm, nm, pl, cl, nl, ev[k], m[k], lab[k], d);
-            else dp_cell(pm, cm, nm, pl, cl, nl, ev[k], m[k], lab[k], d);
+            if constexpr (FWD) {
+                if (k == 0) fwd_cell_left_last(pm, cm, nm, pl, cl, nl, fcl[k], fcu[k], fcr[k], m[k], lab[k], d);
+                else fwd_cell(pm, cm, nm, pl, cl, nl, fcl[k], fcu[k], fcr[k], m[k], lab[k], d);
+            } else {
+                if (k == 0) dp_cell_left_last(pm, cm, nm, pl, cl, nl, ev[k], m[k], lab[k], d);
+                else dp_cell(pm, cm, nm, pl, cl, nl, ev[k], m[k], lab[k], d);
+            }
             dbits |= uint32_t(d) << (2 * k);
             pm = cm;
             pl = cl;
@@ -675,6 +757,12 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) px[k] = __ldg(rb + k);
                 luma_cols<4>(px, QLc);
+            } else if constexpr (FWD) {  // luma plane: the row above the block
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (wc0 + k < 0 || wc0 + k >= W) qoob |= 1u << k;
+                    QLp[k] = e[(long long)(r0 - 1) * p.epitch + wc0 + k];
+                }
             }
             auto p2fetch = [&](int r, int slot) {
                 const uint32_t dst = p2ring + uint32_t(slot * P2_COLS * 8);
@@ -692,12 +780,13 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
             for (int r = r0; r <= r1; ++r) {
                 const int slot = (r - r0) % P2D;
                 cp_async_wait<P2D - 1>();
-                double ec[4];
+                double ec[4], qcl[4], qcu[4], qcr[4];
                 if constexpr (FUSED) {
                     const uint4 q = *reinterpret_cast<const uint4*>(p2ring_ptr + slot * P2_COLS);
                     const uint32_t px[4] = {q.x, q.y, q.z, q.w};
                     luma_cols<4>(px, QLn);
-                    energy_cols<4>(QLp, QLc, QLn, qoob, ec);
+                    if constexpr (FWD) fwd_cols<4>(QLp, QLc, qoob, qcl, qcu, qcr);
+                    else energy_cols<4>(QLp, QLc, QLn, qoob, ec);
 #pragma unroll
                     for (int k = 0; k < 4; ++k) { QLp[k] = QLc[k]; QLc[k] = QLn[k]; }
                 } else {
@@ -705,6 +794,13 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
                     const double2 x0 = *reinterpret_cast<const double2*>(src);
                     const double2 x1 = *reinterpret_cast<const double2*>(src + 2);
                     ec[0] = x0.x; ec[1] = x0.y; ec[2] = x1.x; ec[3] = x1.y;
+                    if constexpr (FWD) {  // luma row r
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) QLc[k] = ec[k];
+                        fwd_cols<4>(QLp, QLc, qoob, qcl, qcu, qcr);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) QLp[k] = QLc[k];
+                    }
                 }
                 p2fetch(r + P2D, slot);
                 const double lm = __shfl_up_sync(FULL, mm[3], 1);
@@ -717,7 +813,8 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
                     const double cm = mm[k];
                     const double nm = (k + 1 < 4) ? mm[k + 1] : rr;
                     int d, dummy;
-                    dp_cell(pm, cm, nm, 0, 0, 0, ec[k], mm[k], dummy, d);
+                    if constexpr (FWD) fwd_cell(pm, cm, nm, 0, 0, 0, qcl[k], qcu[k], qcr[k], mm[k], dummy, d);
+                    else dp_cell(pm, cm, nm, 0, 0, 0, ec[k], mm[k], dummy, d);
                     db |= uint32_t(d) << (8 * k);
                     pm = cm;
                 }

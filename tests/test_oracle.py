@@ -185,3 +185,54 @@ def test_enlarge_port_vs_reference_random(port):
         a, sa = port.enlarge(img, tw, th, seams=True)
         b, sb = ref.enlarge(img, tw, th, seams=True)
         assert np.array_equal(a, b) and np.array_equal(sa, sb)
+
+
+# -- forward energy and recompute=false ---------------------------
+def fbits(a):
+    return np.ascontiguousarray(a, np.float64).view(np.uint64)
+
+
+def test_forward_golden(port):
+    """The C restatement of forward_costs / dp_seam_forward / the forward and
+    recompute=false carve loops against the reference-generated fixtures."""
+    z = np.load(os.path.join(GOLD, "forward.npz"))
+    for k in range(int(z["nmaps"])):
+        g = z[f"g{k}"]
+        for got, key in zip(port.forward_costs(g), ("cl", "cu", "cr")):
+            assert np.array_equal(fbits(got), fbits(z[f"{key}{k}"])), (k, key)
+        seam, m, b = port.dp_seam_forward(g)
+        assert np.array_equal(seam, z[f"seam{k}"]) and np.array_equal(b, z[f"b{k}"]), k
+        assert np.array_equal(fbits(m), fbits(z[f"m{k}"])), k
+    for k in range(int(z["nimgs"])):
+        img = z[f"img{k}"]
+        tw, th = (int(v) for v in z[f"tgt{k}"])
+        o, s = port.carve_cfg(img, tw, th, forward=True, seams=True)
+        assert np.array_equal(o, z[f"fwd{k}"]) and np.array_equal(s, z[f"fwdseams{k}"][: s.size]), k
+        o, s = port.carve_cfg(img, tw, th, recompute=False, seams=True)
+        assert np.array_equal(o, z[f"norec{k}"]) and np.array_equal(s, z[f"norecseams{k}"][: s.size]), k
+
+
+def test_forward_reference_cases(port):
+    # test_solvers.cpp:222-249: constant image -> leftmost seam; diagonal edge
+    assert port.dp_seam_forward(np.full((3, 4), 55.0))[0].tolist() == [0, 0, 0]
+    g = np.array([0, 200, 200, 200, 0, 0, 200, 200, 200, 0, 0, 200, 200, 200, 0, 0], float).reshape(4, 4)
+    assert port.dp_seam_forward(g)[0].tolist() == [2, 3, 3, 3]
+    # test_energy.cpp:178-190: hand-evaluated 2x3 costs
+    cl, cu, cr = port.forward_costs(np.array([[10, 50, 20], [80, 40, 90]], float))
+    assert cu.tolist() == [[40, 10, 30], [40, 10, 50]]
+    assert cl.tolist() == [[40, 50, 60], [110, 40, 70]]
+    assert cr.tolist() == [[80, 40, 30], [70, 50, 120]]
+
+
+@need_ref
+def test_forward_port_vs_reference_random(port):
+    ref = oracle.reference()
+    rng = np.random.default_rng(44)
+    for t in range(30):
+        h, w = (int(v) for v in rng.integers(1, 20, 2))
+        img = rng.integers(0, 256, (h, w, 3), dtype=np.uint8) if t % 2 else port.make_test_image(w, h)
+        tw, th = int(rng.integers(1, w + 1)), int(rng.integers(1, h + 1))
+        for fwd, rec in ((True, True), (False, False)):
+            a, sa = port.carve_cfg(img, tw, th, fwd, rec, seams=True)
+            b, sb = ref.carve_cfg(img, tw, th, fwd, rec, seams=True)
+            assert np.array_equal(a, b) and np.array_equal(sa, sb)
