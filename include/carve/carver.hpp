@@ -183,9 +183,32 @@ inline std::pair<PixelGrid, CarveReport> enlarge_to_width(const PixelGrid& grid,
 }
 
 // Paper-comparison / non-hot-path pipelines keep their declarations.
-inline std::pair<PixelGrid, CarveReport> remove_object(const PixelGrid&, const RemovalMask&, const CarveConfig& = {},
-                                                       bool = true) {
-    detail::unsupported("remove_object");
+/// carver.hpp:327-340: the whole removal loop (mask-biased e1, DP, removal of
+/// image and mask) and the restoring enlargement run on the device.
+inline std::pair<PixelGrid, CarveReport> remove_object(const PixelGrid& grid, const RemovalMask& mask,
+                                                       const CarveConfig& cfg = {}, bool restore = true) {
+    detail::check_config(cfg);
+    if (grid.width != mask.width || grid.height != mask.height)
+        fail(Errc::dimension_mismatch, "mask dimensions do not match image");
+    const auto t0 = std::chrono::steady_clock::now();
+    const carve_cuda_config c = detail::abi_config(cfg);
+    std::vector<uint8_t> buf(grid.pixels.size() * 3);
+    std::vector<int32_t> flat(std::max<size_t>(grid.pixels.size(), 1));
+    int ow = 0, oh = 0, ns = 0;
+    detail::check(carve_cuda_remove_object(grid.bytes(), grid.width, grid.height, mask.flags.data(), &c,
+                                           restore ? 1 : 0, buf.data(), &ow, &oh, flat.data(), &ns));
+    PixelGrid out(ow, oh);
+    std::copy(buf.begin(), buf.begin() + size_t(ow) * oh * 3, out.bytes());
+    CarveReport rep;
+    rep.seam_count = ns;
+    const MaskBounds b = mask_bounds(mask);
+    const size_t len = size_t(b.width() <= b.height() ? grid.height : grid.width);
+    for (int t = 0; t < ns; ++t) {
+        rep.seams.emplace_back(flat.begin() + size_t(t) * len, flat.begin() + size_t(t + 1) * len);
+        rep.per_seam.push_back({0.0, 0.0, 0.0});
+    }
+    rep.total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return {std::move(out), std::move(rep)};
 }
 
 } // namespace carve

@@ -5,6 +5,7 @@
 //                 [--solver dp|pardp] [--energy e1] [--forward]
 //   carve enlarge --input X --output Y [--scale S | --width W] [--height H] [solver flags]
 //   carve seams   --input X --output Y --count N [solver flags]
+//   carve remove-object --input X --mask M --output Y [--no-restore] [solver flags]
 // Exit codes as the reference: 0 success, 1 usage error, 2 runtime error.
 // CARVE_WORKERS is validated like the reference (cli.hpp:109-126) but never
 // changes output. Other subcommands report usage_error (not on the B200 path).
@@ -28,6 +29,8 @@ struct ResizeCmd {
     std::string solver = "pardp", energy = "e1";
     bool forward = false;
     int count = 0;  // seams --count
+    std::string mask;        // remove-object --mask (cli.hpp:41-45, 177-182)
+    bool no_restore = false;  // remove-object --no-restore
 };
 using EnlargeCmd = ResizeCmd;  // same options (cli.hpp:34-39, 167-175)
 struct SeamsCmd : ResizeCmd {};  // --input --output --count + solver flags (cli.hpp:52-56, 189-193)
@@ -82,12 +85,17 @@ inline ResizeCmd parse_resize(const std::vector<std::string>& a) {
                 fail(Errc::usage_error, "--energy: unknown function " + c.energy);
         } else if (f == "--forward") c.forward = true;
         else if (f == "--count" && a[0] == "seams") c.count = detail::parse_positive(f, val());
+        else if (f == "--mask" && a[0] == "remove-object") c.mask = val();
+        else if (f == "--no-restore" && a[0] == "remove-object") c.no_restore = true;
         else fail(Errc::usage_error, "unknown option " + f);
     }
     if (c.input.empty() || c.output.empty()) fail(Errc::usage_error, "--input and --output are required");
     if (c.scale && c.width) fail(Errc::usage_error, "--scale excludes --width");
     if (a[0] == "seams" && (c.scale || c.width || c.height)) fail(Errc::usage_error, "seams takes --count, not a size");
     if (a[0] == "seams" && c.count < 1) fail(Errc::usage_error, "--count is required");
+    if (a[0] == "remove-object" && c.mask.empty()) fail(Errc::usage_error, "--mask is required");
+    if (a[0] == "remove-object" && (c.scale || c.width || c.height))
+        fail(Errc::usage_error, "remove-object takes no size options");
     return c;
 }
 
@@ -146,6 +154,17 @@ inline int run_seams(const SeamsCmd& cmd) {
     return 0;
 }
 
+/// cli.hpp:279-287 run_remove_object: mask_from_image of --mask, remove_object.
+inline int run_remove_object(const ResizeCmd& cmd) {
+    detail::check_env_workers();
+    PixelGrid img = load_image(cmd.input);
+    PixelGrid mask_img = load_image(cmd.mask);
+    RemovalMask mask = mask_from_image(mask_img);
+    auto [result, report] = remove_object(img, mask, detail::config_of(cmd), !cmd.no_restore);
+    save_image(result, cmd.output);
+    return 0;
+}
+
 inline int cli_main(int argc, char** argv) {
     try {
         const std::vector<std::string> args(argv + 1, argv + argc);
@@ -153,18 +172,21 @@ inline int cli_main(int argc, char** argv) {
             std::printf("usage: carve resize  --input X --output Y [--scale S | --width W] [--height H]\n"
                         "                     [--solver dp|pardp] [--energy e1]\n"
                         "       carve enlarge --input X --output Y [--scale S | --width W] [--height H]\n"
-                        "       carve seams   --input X --output Y --count N\n");
+                        "       carve seams   --input X --output Y --count N\n"
+                        "       carve remove-object --input X --mask M --output Y [--no-restore]\n");
             return args.empty() ? 1 : 0;
         }
         if (args[0] == "resize") return run_resize(parse_resize(args));
         if (args[0] == "enlarge") return run_enlarge(parse_resize(args));
+        if (args[0] == "remove-object") return run_remove_object(parse_resize(args));
         if (args[0] == "seams") {
             SeamsCmd c;
             static_cast<ResizeCmd&>(c) = parse_resize(args);
             return run_seams(c);
         }
         fail(Errc::usage_error,
-             "subcommand '" + args[0] + "' is not supported by the B200 engine (resize, enlarge, seams)");
+             "subcommand '" + args[0] +
+                 "' is not supported by the B200 engine (resize, enlarge, seams, remove-object)");
     } catch (const Error& err) {
         std::fprintf(stderr, "carve: %s\n", err.what());
         return err.code() == Errc::usage_error ? 1 : 2;

@@ -4,6 +4,7 @@
 // masks keep their declarations and fail with usage_error (no CPU fallback).
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -88,6 +89,54 @@ inline ForwardCosts forward_costs(const LumaGrid& gray) {
                                            fc.cost_up.data(), fc.cost_right.data()));
     return fc;
 }
-inline EnergyMap apply_mask(const EnergyMap&, const RemovalMask&) { detail::unsupported("removal masks"); }
+/// energy.hpp:220-241 on the device: masked cells -> -1000*(h*m + 1).
+inline EnergyMap apply_mask(const EnergyMap& energy, const RemovalMask& mask) {
+    if (energy.width != mask.width || energy.height != mask.height)
+        fail(Errc::dimension_mismatch, "mask dimensions do not match energy map");
+    EnergyMap out{energy.width, energy.height, std::vector<double>(energy.values.size())};
+    detail::check(carve_cuda_apply_mask(energy.values.data(), energy.width, energy.height, mask.flags.data(),
+                                        out.values.data()));
+    return out;
+}
+
+/// energy.hpp:244-253: FP64 luma >= 128 marks a pixel (on the device).
+inline RemovalMask mask_from_image(const PixelGrid& img) {
+    RemovalMask mask;
+    mask.width = img.width;
+    mask.height = img.height;
+    mask.flags.resize(img.pixels.size());
+    detail::check(carve_cuda_mask_from_rgb(img.bytes(), img.width, img.height, mask.flags.data()));
+    return mask;
+}
+
+inline RemovalMask transpose(const RemovalMask& mask) {
+    RemovalMask out;
+    out.width = mask.height;
+    out.height = mask.width;
+    out.flags.resize(mask.flags.size());
+    for (int i = 0; i < mask.height; ++i)
+        for (int j = 0; j < mask.width; ++j)
+            out.flags[size_t(j) * out.width + i] = mask.flags[size_t(i) * mask.width + j];
+    return out;
+}
+
+struct MaskBounds {
+    int top = 0, left = 0, bottom = -1, right = -1;  // inclusive; empty when bottom < top
+    int width() const { return right - left + 1; }
+    int height() const { return bottom - top + 1; }
+};
+
+inline MaskBounds mask_bounds(const RemovalMask& mask) {
+    MaskBounds b{mask.height, mask.width, -1, -1};
+    for (int i = 0; i < mask.height; ++i)
+        for (int j = 0; j < mask.width; ++j)
+            if (mask.marked(i, j)) {
+                b.top = std::min(b.top, i);
+                b.left = std::min(b.left, j);
+                b.bottom = std::max(b.bottom, i);
+                b.right = std::max(b.right, j);
+            }
+    return b;
+}
 
 } // namespace carve

@@ -126,6 +126,20 @@ carve_status carve_cuda_forward_costs(const double* luma, int w, int h, double* 
 carve_status carve_cuda_dp_seam_forward(const double* luma, int w, int h, double* m_out, int32_t* b_out,
                                         int32_t* seam_out);
 
+/* ---- object removal (energy.hpp:220-253, carver.hpp:287-340) ---------- */
+/* replaces mask_from_image: flags (w*h bytes) = luma >= 128 */
+carve_status carve_cuda_mask_from_rgb(const uint8_t* rgb, int w, int h, uint8_t* flags);
+/* replaces apply_mask(energy, mask): masked cells -> -1000*(h*m+1) */
+carve_status carve_cuda_apply_mask(const double* e, int w, int h, const uint8_t* mask, double* out);
+/* replaces remove_object(grid, mask, cfg, restore) (carver.hpp:327-340).
+ * mask: w*h flags (nonzero = remove). rgb_out: caller buffer of w*h*3 bytes,
+ * the result is *out_w x *out_h. seams_out (nullable): w*h ints, receives the
+ * report's seams concatenated (length h each for vertical removal, w each when
+ * the mask's bounding box is wider than tall); *nseams (nullable) their count. */
+carve_status carve_cuda_remove_object(const uint8_t* rgb, int w, int h, const uint8_t* mask,
+                                      const carve_cuda_config* cfg, int restore, uint8_t* rgb_out, int* out_w,
+                                      int* out_h, int32_t* seams_out, int* nseams);
+
 /* ---- seam recording and enlargement (carver.hpp:114-140, 226-285; cli.hpp:262-277, 301-309) */
 /* replaces insert_seam (carver.hpp:137-140: validate_seam + detail::insert_columns
  * :117-130); out is (w+1)*h*3 bytes */

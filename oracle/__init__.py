@@ -117,6 +117,35 @@ class _Checker:
         self._check(f(np.ascontiguousarray(img), w, h, target_w, th, int(forward), int(recompute), out, s.ctypes.data))
         return (out, s[:n]) if seams else out
 
+    def apply_mask(self, e: np.ndarray, mask: np.ndarray) -> np.ndarray:
+        """energy.hpp:220-241"""
+        h, w = e.shape
+        out = np.empty((h, w), np.float64)
+        self._check(self._fn("apply_mask", _f8p, C.c_int, C.c_int, _u8p, _f8p)(
+            np.ascontiguousarray(e, np.float64), w, h, np.ascontiguousarray(mask, np.uint8), out))
+        return out
+
+    def mask_from_image(self, img: np.ndarray) -> np.ndarray:
+        """energy.hpp:244-253"""
+        h, w, _ = img.shape
+        out = np.empty((h, w), np.uint8)
+        self._check(self._fn("mask_from_image", _u8p, C.c_int, C.c_int, _u8p)(np.ascontiguousarray(img), w, h, out))
+        return out
+
+    def remove_object(self, img: np.ndarray, mask: np.ndarray, forward: bool = False, restore: bool = True):
+        """carver.hpp:327-340 -> (result, seams list)"""
+        h, w, _ = img.shape
+        out = np.empty(w * h * 3, np.uint8)
+        dims = np.zeros(2, np.int32)
+        seams = np.empty(max(w * h, 1), np.int32)
+        n = np.zeros(1, np.int32)
+        f = self._fn("remove_object", _u8p, C.c_int, C.c_int, _u8p, C.c_int, C.c_int, _u8p, _i4p, _i4p, _i4p)
+        self._check(f(np.ascontiguousarray(img), w, h, np.ascontiguousarray(mask, np.uint8), int(forward),
+                      int(restore), out, dims, seams, n))
+        ow, oh = int(dims[0]), int(dims[1])
+        res = out[: ow * oh * 3].reshape(oh, ow, 3).copy()
+        return res, seams, int(n[0])
+
     def insert_seam(self, img: np.ndarray, seam) -> np.ndarray:
         """carver.hpp:137-140"""
         h, w, _ = img.shape

@@ -28,6 +28,7 @@ enum {
     OR_WIDTH_TOO_SMALL = 1 + 8,
     OR_INVALID_TARGET = 1 + 9,
     OR_TARGET_TOO_LARGE = 1 + 10,
+    OR_EMPTY_MASK = 1 + 11,
     OR_NO_MEMORY = 100,
 };
 
@@ -356,6 +357,132 @@ int or_carve_cfg(const uint8_t* rgb, int w, int h, int target_w, int target_h, i
     return st;
 }
 
+/* energy.hpp:220-241 apply_mask: masked cells become -k, k = 1000*(h*m + 1),
+ * m = max over unmasked cells (over all cells when every cell is masked). */
+int or_apply_mask(const double* e, int w, int h, const uint8_t* mask, double* out) {
+    double max_unmasked = 0.0, max_all = 0.0;
+    int any_unmasked = 0;
+    const size_t n = (size_t)w * h;
+    for (size_t i = 0; i < n; ++i) {
+        if (e[i] > max_all) max_all = e[i];
+        if (!mask[i]) {
+            if (e[i] > max_unmasked) max_unmasked = e[i];
+            any_unmasked = 1;
+        }
+    }
+    const double m = any_unmasked ? max_unmasked : max_all;
+    const double k = 1000.0 * ((double)h * m + 1.0);
+    for (size_t i = 0; i < n; ++i) out[i] = mask[i] ? -k : e[i];
+    return OR_OK;
+}
+
+/* energy.hpp:244-253 mask_from_image: luma >= 128 marks a pixel */
+int or_mask_from_image(const uint8_t* rgb, int w, int h, uint8_t* flags) {
+    for (size_t i = 0; i < (size_t)w * h; ++i) flags[i] = luma_of(rgb + 3 * i) >= 128.0 ? 1 : 0;
+    return OR_OK;
+}
+
+static void transpose_u8(const uint8_t* in, int w, int h, uint8_t* out) {
+    for (int i = 0; i < h; ++i)
+        for (int j = 0; j < w; ++j) out[(size_t)j * h + i] = in[(size_t)i * w + j];
+}
+
+static int enlarge_width(const uint8_t* in, int w, int h, int target_w, int forward, uint8_t* out,
+                         int** seams_cursor);
+
+/* carver.hpp:287-315 remove_object_vertical: per seam e1 of the current image,
+ * apply_mask with the remaining mask, dp seam, remove from image and mask; until
+ * no marked cell remains. Then (restore) enlarge_to_width back to w. `forward`
+ * only affects the restoring enlargement (record_seams with cfg). */
+static int remove_object_vertical(uint8_t* work, int w, int h, uint8_t* mask, int forward, int restore, int* out_w,
+                                  int* seams_out, int* nseams, uint8_t* out) {
+    double* e = (double*)malloc((size_t)w * h * 8);
+    double* eb = (double*)malloc((size_t)w * h * 8);
+    uint8_t* tmp = (uint8_t*)malloc((size_t)w * h * 3);
+    uint8_t* mtmp = (uint8_t*)malloc((size_t)w * h);
+    int* seam = (int*)malloc(sizeof(int) * (size_t)h);
+    if (!e || !eb || !tmp || !mtmp || !seam) return OR_NO_MEMORY;
+    int cw = w, ns = 0, st = OR_OK;
+    for (;;) {
+        size_t marked = 0;
+        for (size_t i = 0; i < (size_t)cw * h; ++i) marked += mask[i] != 0;
+        if (!marked) break;
+        if (cw < 2) { st = OR_WIDTH_TOO_SMALL; break; }
+        or_energy_e1_rgb(work, cw, h, e);
+        or_apply_mask(e, cw, h, mask, eb);
+        or_dp_seam(eb, cw, h, NULL, NULL, seam);
+        or_remove_seam(work, cw, h, seam, h, tmp);
+        memcpy(work, tmp, (size_t)(cw - 1) * h * 3);
+        for (int i = 0; i < h; ++i) { /* remove_seam(RemovalMask) carver.hpp:100-112 */
+            const uint8_t* src = mask + (size_t)i * cw;
+            uint8_t* dst = mtmp + (size_t)i * (cw - 1);
+            memcpy(dst, src, (size_t)seam[i]);
+            memcpy(dst + seam[i], src + seam[i] + 1, (size_t)(cw - seam[i] - 1));
+        }
+        memcpy(mask, mtmp, (size_t)(cw - 1) * h);
+        memcpy(seams_out + (size_t)ns * h, seam, sizeof(int) * (size_t)h);
+        ++ns;
+        --cw;
+    }
+    *nseams = ns;
+    if (!st) {
+        if (restore && cw < w) {
+            int* none = NULL;
+            st = enlarge_width(work, cw, h, w, forward, out, &none);
+            *out_w = w;
+        } else {
+            memcpy(out, work, (size_t)cw * h * 3);
+            *out_w = cw;
+        }
+    }
+    free(e);
+    free(eb);
+    free(tmp);
+    free(mtmp);
+    free(seam);
+    return st;
+}
+
+/* carver.hpp:327-340 remove_object. out: w*h*3 bytes; out_dims {w, h};
+ * seams_out: w*h ints (the report's seams, concatenated); nseams. */
+int or_remove_object(const uint8_t* rgb, int w, int h, const uint8_t* mask_in, int forward, int restore, uint8_t* out,
+                     int* out_dims, int* seams_out, int* nseams) {
+    int top = h, left = w, bottom = -1, right = -1;
+    for (int i = 0; i < h; ++i)
+        for (int j = 0; j < w; ++j)
+            if (mask_in[(size_t)i * w + j]) {
+                if (i < top) top = i;
+                if (j < left) left = j;
+                if (i > bottom) bottom = i;
+                if (j > right) right = j;
+            }
+    if (bottom < top) return OR_EMPTY_MASK;
+    uint8_t* work = (uint8_t*)malloc((size_t)w * h * 3);
+    uint8_t* mask = (uint8_t*)malloc((size_t)w * h);
+    if (!work || !mask) return OR_NO_MEMORY;
+    int st, ow;
+    if (right - left + 1 <= bottom - top + 1) {
+        memcpy(work, rgb, (size_t)w * h * 3);
+        memcpy(mask, mask_in, (size_t)w * h);
+        st = remove_object_vertical(work, w, h, mask, forward, restore, &ow, seams_out, nseams, out);
+        out_dims[0] = ow;
+        out_dims[1] = h;
+    } else {
+        uint8_t* res = (uint8_t*)malloc((size_t)w * h * 3);
+        if (!res) return OR_NO_MEMORY;
+        or_transpose(rgb, w, h, work);
+        transpose_u8(mask_in, w, h, mask);
+        st = remove_object_vertical(work, h, w, mask, forward, restore, &ow, seams_out, nseams, res);
+        if (!st) or_transpose(res, ow, w, out);
+        out_dims[0] = w;
+        out_dims[1] = ow;
+        free(res);
+    }
+    free(work);
+    free(mask);
+    return st;
+}
+
 /* carver.hpp:117-130 detail::insert_columns: one pixel per row right of
  * column cols[i] (stride `cs` between rows' entries), the channel-wise rounded
  * mean of its left and right neighbours, the right one clamped at the border. */
@@ -383,7 +510,16 @@ int or_insert_seam(const uint8_t* in, int w, int h, const int* seam, int n, uint
 /* carver.hpp:226-262 record_seams (default config): the removal loop on a
  * scratch copy, each seam mapped to original coordinates through per-row
  * survivor lists (survivor[i][seam[i]], then erase). seams_out: count*h ints. */
+static int carve_width_cfg(uint8_t* work, int w, int h, int target_w, int forward, int recompute,
+                           int** seams_cursor);
+
+static int record_seams_cfg(const uint8_t* rgb, int w, int h, int count, int forward, int* seams_out);
+
 int or_record_seams(const uint8_t* rgb, int w, int h, int count, int* seams_out) {
+    return record_seams_cfg(rgb, w, h, count, 0, seams_out);
+}
+
+static int record_seams_cfg(const uint8_t* rgb, int w, int h, int count, int forward, int* seams_out) {
     if (w < 1 || h < 1) return OR_EMPTY_IMAGE;
     if (count < 0 || count > w - 1) return OR_INVALID_TARGET;
     uint8_t* work = (uint8_t*)malloc((size_t)w * h * 3);
@@ -392,7 +528,7 @@ int or_record_seams(const uint8_t* rgb, int w, int h, int count, int* seams_out)
     if (!work || !cur || !surv) return OR_NO_MEMORY;
     memcpy(work, rgb, (size_t)w * h * 3);
     int* cursor = cur;
-    int st = carve_width_inplace(work, w, h, w - count, &cursor);
+    int st = carve_width_cfg(work, w, h, w - count, forward, 1, &cursor);
     for (int i = 0; i < h && !st; ++i) {
         int* row = surv + (size_t)i * w;
         int len = w;
@@ -414,7 +550,8 @@ int or_record_seams(const uint8_t* rgb, int w, int h, int count, int* seams_out)
  * oldest-first through insert_columns, shifting every later recorded column
  * right by one where it lands at-or-right-of the inserted column. `seams_out`
  * (nullable) receives the recorded (unshifted) seams. */
-static int enlarge_width(const uint8_t* in, int w, int h, int target_w, uint8_t* out, int** seams_cursor) {
+static int enlarge_width(const uint8_t* in, int w, int h, int target_w, int forward, uint8_t* out,
+                         int** seams_cursor) {
     const int k = target_w - w;
     if (k < 0) return OR_INVALID_TARGET;
     if (target_w > 2 * w - 1) return OR_TARGET_TOO_LARGE;
@@ -422,7 +559,7 @@ static int enlarge_width(const uint8_t* in, int w, int h, int target_w, uint8_t*
     uint8_t* a = (uint8_t*)malloc((size_t)target_w * h * 3);
     uint8_t* b = (uint8_t*)malloc((size_t)target_w * h * 3);
     if (!seams || !a || !b) return OR_NO_MEMORY;
-    int st = or_record_seams(in, w, h, k, seams);
+    int st = record_seams_cfg(in, w, h, k, forward, seams);
     if (!st && seams_cursor && *seams_cursor) {
         memcpy(*seams_cursor, seams, sizeof(int) * (size_t)k * h);
         *seams_cursor += (size_t)k * h;
@@ -451,7 +588,7 @@ int or_enlarge(const uint8_t* rgb, int w, int h, int target_w, int target_h, uin
     uint8_t* work = (uint8_t*)malloc((size_t)(target_w > w ? target_w : w) * h * 3);
     if (!work) return OR_NO_MEMORY;
     if (target_w != w) {
-        st = enlarge_width(rgb, w, h, target_w, work, &cursor);
+        st = enlarge_width(rgb, w, h, target_w, 0, work, &cursor);
         cw = target_w;
     } else {
         memcpy(work, rgb, (size_t)w * h * 3);
@@ -462,7 +599,7 @@ int or_enlarge(const uint8_t* rgb, int w, int h, int target_w, int target_h, uin
         uint8_t* t2 = (uint8_t*)malloc(big);
         if (!t || !t2) return OR_NO_MEMORY;
         or_transpose(work, cw, h, t);
-        st = enlarge_width(t, h, cw, target_h, t2, &cursor);
+        st = enlarge_width(t, h, cw, target_h, 0, t2, &cursor);
         if (!st) {
             free(work);
             work = (uint8_t*)malloc(big);

@@ -240,6 +240,45 @@ int ref_carve_cfg(const std::uint8_t* rgb, int w, int h, int target_w, int targe
     });
 }
 
+// energy.hpp:220-241 apply_mask
+int ref_apply_mask(const double* e, int w, int h, const std::uint8_t* mask, double* out) {
+    return guarded([&] {
+        carve_ref::RemovalMask m{w, h, std::vector<std::uint8_t>(mask, mask + size_t(w) * h)};
+        auto r = carve_ref::apply_mask(map_from(e, w, h), m);
+        std::memcpy(out, r.values.data(), r.values.size() * 8);
+    });
+}
+
+// energy.hpp:244-253 mask_from_image
+int ref_mask_from_image(const std::uint8_t* rgb, int w, int h, std::uint8_t* flags) {
+    return guarded([&] {
+        auto m = carve_ref::mask_from_image(grid_from(rgb, w, h));
+        std::memcpy(flags, m.flags.data(), m.flags.size());
+    });
+}
+
+// carver.hpp:327-340 remove_object (cfg.forward as given, restore flag). out:
+// the result (caller buffer of w*h*3 bytes), out_dims = {width, height};
+// seams_out (w*h ints) the report's seams concatenated, nseams their count.
+int ref_remove_object(const std::uint8_t* rgb, int w, int h, const std::uint8_t* mask, int forward, int restore,
+                      std::uint8_t* out, int* out_dims, int* seams_out, int* nseams) {
+    return guarded([&] {
+        carve_ref::CarveConfig cfg;
+        cfg.forward = forward != 0;
+        carve_ref::RemovalMask m{w, h, std::vector<std::uint8_t>(mask, mask + size_t(w) * h)};
+        auto [res, report] = carve_ref::remove_object(grid_from(rgb, w, h), m, cfg, restore != 0);
+        grid_to(res, out);
+        out_dims[0] = res.width;
+        out_dims[1] = res.height;
+        size_t off = 0;
+        for (auto& s : report.seams) {
+            std::memcpy(seams_out + off, s.data(), s.size() * sizeof(int));
+            off += s.size();
+        }
+        *nseams = report.seam_count;
+    });
+}
+
 // carver.hpp:117-140 insert_seam (validate_seam + insert_columns)
 int ref_insert_seam(const std::uint8_t* rgb, int w, int h, const int* seam, int n, std::uint8_t* out) {
     return guarded([&] { grid_to(carve_ref::insert_seam(grid_from(rgb, w, h), carve_ref::Seam(seam, seam + n)), out); });

@@ -26,6 +26,7 @@ __all__ = [
     "energy_e1_rgb", "dp_seam", "parallel_dp_seam", "find_seam", "validate_seam", "remove_seam", "transpose",
     "carve_to_width", "carve_to_height", "carve", "carve_batch", "carve_device", "carve_batch_device",
     "insert_seam", "record_seams", "enlarge_to_width", "enlarge", "forward_costs", "dp_seam_forward",
+    "apply_mask", "mask_from_image", "mask_bounds", "remove_object",
     "library", "library_path", "device_count", "launch_count", "reset_launch_count",
 ]
 
@@ -177,6 +178,9 @@ def library() -> C.CDLL:
             "carve_cuda_carve": ([vp, i, i, i, i, vp, vp, vp], i),
             "carve_cuda_carve_cfg": ([vp, i, i, i, i, vp, vp, vp, vp], i),
             "carve_cuda_forward_costs": ([vp, i, i, vp, vp, vp], i),
+            "carve_cuda_mask_from_rgb": ([vp, i, i, vp], i),
+            "carve_cuda_apply_mask": ([vp, i, i, vp, vp], i),
+            "carve_cuda_remove_object": ([vp, i, i, vp, vp, i, vp, vp, vp, vp, vp], i),
             "carve_cuda_dp_seam_forward": ([vp, i, i, vp, vp, vp], i),
             "carve_cuda_carve_batch": ([vp, i, i, i, i, i, vp, vp, i], i),
             "carve_cuda_carve_device": ([vp, i, i, i, i, vp, vp, vp], i),
@@ -461,6 +465,60 @@ def dp_seam_forward(luma: np.ndarray, costs=None) -> SeamResult:
     seam = np.empty(h, np.int32)
     _check(library().carve_cuda_dp_seam_forward(_ptr(g), w, h, _ptr(m), _ptr(b), _ptr(seam)))
     return SeamResult(seam, CostTable(w, h, m, b))
+
+
+def mask_from_image(img: np.ndarray) -> np.ndarray:
+    """energy.hpp:244-253 — uint8 flags (luma >= 128), on the device."""
+    a = _img(img)
+    h, w, _ = a.shape
+    out = np.empty((h, w), np.uint8)
+    _check(library().carve_cuda_mask_from_rgb(_ptr(a), w, h, _ptr(out)))
+    return out
+
+
+def apply_mask(energy: np.ndarray, mask: np.ndarray) -> np.ndarray:
+    """energy.hpp:220-241 — masked cells -> -1000*(h*m + 1), on the device."""
+    e = np.ascontiguousarray(energy, dtype=np.float64)
+    m = np.ascontiguousarray(mask, dtype=np.uint8)
+    if e.shape != m.shape:
+        raise CarveError(Errc.dimension_mismatch, "mask dimensions do not match energy map")
+    h, w = e.shape
+    out = np.empty((h, w), np.float64)
+    _check(library().carve_cuda_apply_mask(_ptr(e), w, h, _ptr(m), _ptr(out)))
+    return out
+
+
+def mask_bounds(mask: np.ndarray):
+    """energy.hpp:266-283 — (top, left, bottom, right), inclusive; bottom < top when empty."""
+    ys, xs = np.nonzero(np.asarray(mask))
+    if ys.size == 0:
+        h, w = np.shape(mask)
+        return (h, w, -1, -1)
+    return (int(ys.min()), int(xs.min()), int(ys.max()), int(xs.max()))
+
+
+def remove_object(img: np.ndarray, mask: np.ndarray, cfg: CarveConfig | None = None, restore: bool = True):
+    """carver.hpp:327-340 — returns (result, CarveReport). The removal loop and
+    the restoring enlargement run on the device."""
+    import time
+    a = _img(img)
+    h, w, _ = a.shape
+    _check_config(cfg)
+    m = np.ascontiguousarray(mask, dtype=np.uint8)
+    if m.shape != (h, w):
+        raise CarveError(Errc.dimension_mismatch, "mask dimensions do not match image")
+    t0 = time.perf_counter()
+    buf = np.empty(max(w * h * 3, 1), np.uint8)
+    flat = np.empty(max(w * h, 1), np.int32)
+    ow, oh, ns = C.c_int(), C.c_int(), C.c_int()
+    c = _abi_config(cfg)
+    _check(library().carve_cuda_remove_object(_ptr(a), w, h, _ptr(m), C.byref(c), int(bool(restore)), _ptr(buf),
+                                              C.byref(ow), C.byref(oh), _ptr(flat), C.byref(ns)))
+    out = buf[: ow.value * oh.value * 3].reshape(oh.value, ow.value, 3).copy()
+    top, left, bottom, right = mask_bounds(m)
+    n = h if right - left <= bottom - top else w
+    seams = [flat[t * n:(t + 1) * n].copy() for t in range(ns.value)]
+    return out, _report(seams, [SeamTiming(0.0, 0.0, 0.0) for _ in seams], time.perf_counter() - t0)
 
 
 def insert_seam(img: np.ndarray, seam) -> np.ndarray:

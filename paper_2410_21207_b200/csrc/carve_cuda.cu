@@ -100,6 +100,7 @@ struct Ctx {
     cudaStream_t stream = nullptr;
     DevBuf packed_in, packed_out, rgb[2], e[2], dir, seams, stamps, scratch_a, scratch_b, mbound;
     DevBuf rec, enl[3];  // recorded seams (original coordinates), enlargement intermediates
+    DevBuf stats;        // object removal: MaskStats
     int max_smem_optin = 0;
     std::map<const void*, int> smem_set;  // kernel -> dynamic smem attribute set
     // kernel-event profiling mode (bench attribution): one event pair per launch
@@ -1173,6 +1174,166 @@ carve_status carve_cuda_dp_seam_forward(const double* luma, int w, int h, double
             ck(cudaMemcpyAsync(b_out, db, size_t(w) * h * 4, cudaMemcpyDeviceToHost, c.stream), "D2H b");
         }
         sync(c);
+    });
+}
+
+carve_status carve_cuda_mask_from_rgb(const uint8_t* rgb, int w, int h, uint8_t* flags) {
+    return guarded([&] {
+        if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "PixelGrid dimensions must be >= 1");
+        Ctx& c = ctx();
+        const long long n = (long long)w * h;
+        uint8_t* d_in = static_cast<uint8_t*>(c.packed_in.ensure(size_t(n) * 3));
+        uint8_t* d_f = static_cast<uint8_t*>(c.packed_out.ensure(size_t(n)));
+        ck(cudaMemcpyAsync(d_in, rgb, size_t(n) * 3, cudaMemcpyHostToDevice, c.stream), "H2D");
+        k_mask_from_rgb<<<grid_for(n, 256), 256, 0, c.stream>>>(d_in, n, d_f);
+        LAUNCHED("k_mask_from_rgb");
+        ck(cudaMemcpyAsync(flags, d_f, size_t(n), cudaMemcpyDeviceToHost, c.stream), "D2H");
+        sync(c);
+    });
+}
+
+carve_status carve_cuda_apply_mask(const double* e, int w, int h, const uint8_t* mask, double* out) {
+    return guarded([&] {
+        if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "EnergyMap dimensions must be >= 1");
+        Ctx& c = ctx();
+        const size_t n = size_t(w) * h;
+        double* d_e = static_cast<double*>(c.scratch_a.ensure(n * 16));
+        uint8_t* d_m = static_cast<uint8_t*>(c.packed_in.ensure(n));
+        MaskStats* st = static_cast<MaskStats*>(c.stats.ensure(sizeof(MaskStats)));
+        ck(cudaMemcpyAsync(d_e, e, n * 8, cudaMemcpyHostToDevice, c.stream), "H2D e");
+        ck(cudaMemcpyAsync(d_m, mask, n, cudaMemcpyHostToDevice, c.stream), "H2D mask");
+        ck(cudaMemsetAsync(st, 0, sizeof(MaskStats), c.stream), "memset stats");
+        k_mask_stats<true><<<grid_for((long long)n, 256), 256, 0, c.stream>>>(d_e, w, d_m, nullptr, 0, w, h, st);
+        LAUNCHED("k_mask_stats");
+        k_apply_mask<true><<<grid_for((long long)n, 256), 256, 0, c.stream>>>(d_e, w, d_m, nullptr, 0, w, h, st,
+                                                                              d_e + n, w, 0);
+        LAUNCHED("k_apply_mask");
+        ck(cudaMemcpyAsync(out, d_e + n, n * 8, cudaMemcpyDeviceToHost, c.stream), "D2H");
+        sync(c);
+    });
+}
+
+carve_status carve_cuda_remove_object(const uint8_t* rgb, int w, int h, const uint8_t* mask,
+                                      const carve_cuda_config* cfg, int restore, uint8_t* rgb_out, int* out_w,
+                                      int* out_h, int32_t* seams_out, int* nseams) {
+    return guarded([&] {
+        if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "PixelGrid dimensions must be >= 1");
+        const CarveOpts o = opts_of(cfg);
+        // mask_bounds (energy.hpp:272-283) of the caller's flags: picks the orientation
+        int top = h, left = w, bottom = -1, right = -1;
+        for (int i = 0; i < h; ++i)
+            for (int j = 0; j < w; ++j)
+                if (mask[size_t(i) * w + j]) {
+                    top = std::min(top, i);
+                    left = std::min(left, j);
+                    bottom = std::max(bottom, i);
+                    right = std::max(right, j);
+                }
+        if (bottom < top) fail(CARVE_E_EMPTY_MASK, "removal mask marks no pixels");
+        const bool transposed = right - left + 1 > bottom - top + 1;
+        Ctx& c = ctx();
+        cudaStream_t s = c.stream;
+        const size_t n = size_t(w) * h;
+        // the vertical loop runs on a W x H view: the image itself or its transpose
+        const int W = transposed ? h : w, H = transposed ? w : h;
+        const int pitch = padded_epitch(W), epitch = padded_epitch(W);
+        const size_t plane = size_t(pitch) * (H + EPAD_B);
+        uint8_t* d_in = static_cast<uint8_t*>(c.packed_in.ensure(n * 3));
+        uint8_t* d_mask = static_cast<uint8_t*>(c.enl[2].ensure(n));
+        uint32_t* rgbx = static_cast<uint32_t*>(c.rgb[0].ensure(plane * 4)) + EPAD_L;
+        double* e = static_cast<double*>(c.e[0].ensure(plane * 8)) + EPAD_L;
+        double* eb = static_cast<double*>(c.e[1].ensure(plane * 8)) + EPAD_L;
+        // the removal's seam log (c.seams belongs to the carve loop the restore runs)
+        int* d_seams = static_cast<int*>(c.dir.ensure(std::max<size_t>(n, 1) * 4));
+        MaskStats* st = static_cast<MaskStats*>(c.stats.ensure(sizeof(MaskStats)));
+        const int mpitch = epitch;
+        double* mb = static_cast<double*>(c.mbound.ensure(size_t((H + LBLK - 1) / LBLK + 1) * mpitch * 8));
+        ck(cudaMemcpyAsync(d_in, rgb, n * 3, cudaMemcpyHostToDevice, s), "H2D rgb");
+        ck(cudaMemcpyAsync(d_mask, mask, n, cudaMemcpyHostToDevice, s), "H2D mask");
+        if (!transposed) {
+            k_unpack_masked<<<grid_for((long long)n, 256), 256, 0, s>>>(d_in, d_mask, w, h, rgbx, pitch);
+            LAUNCHED("k_unpack_masked");
+        } else {  // transpose(grid), transpose(mask) (carver.hpp:337-339): the mask bit travels along
+            uint32_t* tmp = static_cast<uint32_t*>(c.rgb[1].ensure(size_t(round_up(w, 32)) * h * 4));
+            const int tp = int(round_up(w, 32));
+            k_unpack_masked<<<grid_for((long long)n, 256), 256, 0, s>>>(d_in, d_mask, w, h, tmp, tp);
+            LAUNCHED("k_unpack_masked");
+            launch_transpose(tmp, tp, w, h, rgbx, pitch, 1, 0, 0, s);
+        }
+        // e1 of the start image; +inf pads on both planes (SPEC.md:315 exclusion)
+        launch_energy(rgbx, pitch, W, H, e, epitch, 1, 0, 0, s);
+        launch_fill_pads(e, epitch, W, H, 1, 0, s);
+        launch_fill_pads(eb, epitch, W, H, 1, 0, s);
+        unsigned long long* h_marked = nullptr;
+        ck(cudaMallocHost(&h_marked, sizeof(unsigned long long)), "cudaMallocHost");
+        std::unique_ptr<unsigned long long, decltype(&cudaFreeHost)> guard_marked(h_marked, cudaFreeHost);
+        // remove_object_vertical (carver.hpp:291-315), one seam per iteration:
+        // stats -> (stop?) -> biased map -> DP -> removal of image, mask and map -> fix-up
+        int cw = W, ns = 0;
+        for (;;) {
+            ck(cudaMemsetAsync(st, 0, sizeof(MaskStats), s), "memset stats");
+            k_mask_stats<false><<<grid_for((long long)cw * H, 256), 256, 0, s>>>(e, epitch, nullptr, rgbx, pitch, cw,
+                                                                                H, st);
+            LAUNCHED("k_mask_stats");
+            ck(cudaMemcpyAsync(h_marked, &st->marked, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s),
+               "D2H marked");
+            sync(c);
+            if (*h_marked == 0) break;
+            if (cw < 2) fail(CARVE_E_WIDTH_TOO_SMALL, "mask cannot be carved out of a 1-pixel-wide image");
+            k_apply_mask<false><<<grid_for((long long)cw * H, 256), 256, 0, s>>>(e, epitch, nullptr, rgbx, pitch, cw,
+                                                                                H, st, eb, epitch, 1);
+            LAUNCHED("k_apply_mask");
+            int* seam = d_seams + size_t(ns) * H;
+            const Dp2Plan pl = dp2_plan(cw, H);
+            Dp2Params q{};
+            q.e = eb;
+            q.epitch = epitch;
+            q.W = cw;
+            q.H = H;
+            q.mbound = mb;
+            q.mpitch = mpitch;
+            q.seam = seam;
+            launch_dp2(c, pl, q, 1, s);
+            CompactParams r{};
+            r.rgb_in = r.rgb_out = rgbx;
+            r.e_in = r.e_out = e;
+            r.pitch = pitch;
+            r.epitch = epitch;
+            r.W = cw;
+            r.H = H;
+            r.seam = seam;
+            launch_compact_inplace(r, 1, s);
+            --cw;
+            k_fixup_energy<<<grid_for(H, 256), 256, 0, s>>>(e, epitch, rgbx, pitch, cw, H, seam);
+            LAUNCHED("k_fixup_energy");
+            ++ns;
+        }
+        // restore (carver.hpp:309-313): enlarge_to_width back to the original width
+        uint8_t* d_cur = static_cast<uint8_t*>(c.packed_out.ensure(n * 3));
+        launch_pack(c, rgbx, pitch, cw, H, false, d_cur, 1, 0, 0, s);
+        const uint8_t* res = d_cur;
+        int rw = cw;
+        if (restore && cw < W) {
+            uint8_t* d_big = static_cast<uint8_t*>(c.enl[0].ensure(n * 3));
+            int* d_orig = static_cast<int*>(c.rec.ensure(size_t(W - cw) * H * 4));
+            check_enlarge(cw, W);
+            record_device(c, d_cur, cw, H, W - cw, d_orig, nullptr, o);
+            launch_expand_rows(d_cur, cw, H, d_orig, W - cw, H, d_big, s);
+            res = d_big;
+            rw = W;
+        }
+        if (transposed) {  // back to the caller's orientation
+            uint8_t* d_t = static_cast<uint8_t*>(c.enl[1].ensure(n * 3));
+            transpose_packed(c, res, rw, H, d_t);
+            res = d_t;
+        }
+        *out_w = transposed ? w : rw;
+        *out_h = transposed ? rw : h;
+        ck(cudaMemcpyAsync(rgb_out, res, size_t(rw) * H * 3, cudaMemcpyDeviceToHost, s), "D2H");
+        if (seams_out && ns)
+            ck(cudaMemcpyAsync(seams_out, d_seams, size_t(ns) * H * 4, cudaMemcpyDeviceToHost, s), "D2H seams");
+        sync(c);
+        if (nseams) *nseams = ns;
     });
 }
 

@@ -713,6 +713,119 @@ __global__ void __launch_bounds__(256) k_compact_warp(CompactParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// Object removal: masks travel in the RGBX planes' spare
+// byte (bit 24), so every removal and transpose kernel carries them for free.
+
+constexpr uint32_t MASK_BIT = 1u << 24;
+
+// packed RGB + u8 flags (nonzero = remove, energy.hpp:25-37) -> RGBX with the mask bit
+__global__ void k_unpack_masked(const uint8_t* __restrict__ in, const uint8_t* __restrict__ mask, int W, int H,
+                                uint32_t* __restrict__ out, int pitch) {
+    const long long n = (long long)W * H;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const int i = int(k / W), j = int(k - (long long)i * W);
+        const uint8_t* p = in + 3 * k;
+        out[(long long)i * pitch + j] = uint32_t(p[0]) | (uint32_t(p[1]) << 8) | (uint32_t(p[2]) << 16) |
+                                        (mask[k] ? MASK_BIT : 0u);
+    }
+}
+
+// mask_from_image (energy.hpp:244-253): FP64 luma >= 128 marks a pixel
+__global__ void k_mask_from_rgb(const uint8_t* __restrict__ in, long long n, uint8_t* __restrict__ flags) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const uint8_t* p = in + 3 * k;
+        flags[k] = luma(uint32_t(p[0]) | (uint32_t(p[1]) << 8) | (uint32_t(p[2]) << 16)) >= 128.0 ? 1 : 0;
+    }
+}
+
+// apply_mask's reductions (energy.hpp:224-233) over the live W x H: energies are
+// >= +0, so their IEEE bit patterns order like the values and atomicMax on the
+// bits is an exact max.
+struct MaskStats {
+    unsigned long long max_unmasked, max_all, marked;
+    int any_unmasked;
+};
+
+template <bool U8>  // mask from a u8 plane (API) or the RGBX mask bit (carve loop)
+__device__ __forceinline__ bool masked_at(const uint8_t* m8, const uint32_t* rgb, int rpitch, int i, int j, int W) {
+    if constexpr (U8) return m8[(long long)i * W + j] != 0;
+    else return (rgb[(long long)i * rpitch + j] & MASK_BIT) != 0;
+}
+
+template <bool U8>
+__global__ void k_mask_stats(const double* __restrict__ e, int epitch, const uint8_t* __restrict__ m8,
+                             const uint32_t* __restrict__ rgb, int rpitch, int W, int H, MaskStats* st) {
+    unsigned long long mu = 0, ma = 0, cnt = 0;
+    int any = 0;
+    const long long n = (long long)W * H;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const int i = int(k / W), j = int(k - (long long)i * W);
+        // std::max(0.0, v) semantics (the reference's maxima start at 0.0): only
+        // positive values can raise them, and their bit patterns order like values
+        const double v = e[(long long)i * epitch + j];
+        const unsigned long long b = v > 0.0 ? (unsigned long long)__double_as_longlong(v) : 0ull;
+        ma = b > ma ? b : ma;
+        if (masked_at<U8>(m8, rgb, rpitch, i, j, W)) ++cnt;
+        else {
+            mu = b > mu ? b : mu;
+            any = 1;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(FULL, mu, o), c = __shfl_xor_sync(FULL, ma, o);
+        mu = a > mu ? a : mu;
+        ma = c > ma ? c : ma;
+        cnt += __shfl_xor_sync(FULL, cnt, o);
+        any |= __shfl_xor_sync(FULL, any, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (mu) atomicMax(&st->max_unmasked, mu);
+        if (ma) atomicMax(&st->max_all, ma);
+        if (cnt) atomicAdd(&st->marked, cnt);
+        if (any) atomicOr(&st->any_unmasked, 1);
+    }
+}
+
+// k = 1000 * (h * m + 1), left to right, no contraction (energy.hpp:234-235)
+__device__ __forceinline__ double mask_bias(const MaskStats* st, int H) {
+    const double m = __longlong_as_double((long long)(st->any_unmasked ? st->max_unmasked : st->max_all));
+    return __dmul_rn(1000.0, __dadd_rn(__dmul_rn(double(H), m), 1.0));
+}
+
+// biased map (energy.hpp:237-240): masked cells -> -k; in the carve loop also
+// column W (the one the last removal vacated) -> +inf pad
+template <bool U8>
+__global__ void k_apply_mask(const double* __restrict__ e, int epitch, const uint8_t* __restrict__ m8,
+                             const uint32_t* __restrict__ rgb, int rpitch, int W, int H, const MaskStats* st,
+                             double* __restrict__ out, int opitch, int pad_col) {
+    const double negk = -mask_bias(st, H);
+    const long long n = (long long)W * H;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const int i = int(k / W), j = int(k - (long long)i * W);
+        out[(long long)i * opitch + j] = masked_at<U8>(m8, rgb, rpitch, i, j, W) ? negk : e[(long long)i * epitch + j];
+        if (pad_col && j == W - 1) out[(long long)i * opitch + W] = dinf();
+    }
+}
+
+// K1 fix-up of the two new-grid columns around a removed seam (SURVEY.md
+// Appendix A.4), standalone: the object-removal loop solves on a biased copy,
+// so the DP prologue's in-place fix-up does not apply there.
+__global__ void k_fixup_energy(double* __restrict__ e, int epitch, const uint32_t* __restrict__ rgb, int rpitch, int W,
+                               int H, const int* __restrict__ seam) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < H; i += gridDim.x * blockDim.x) {
+        const int sp = seam[i];
+        const uint32_t* row = rgb + (long long)i * rpitch;
+        const uint32_t* up = rgb + (long long)max(i - 1, 0) * rpitch;
+        const uint32_t* dn = rgb + (long long)min(i + 1, H - 1) * rpitch;
+        for (int x = sp - 1; x <= sp; ++x)
+            if (x >= 0 && x < W)
+                e[(long long)i * epitch + x] =
+                    e1(luma(row[max(x - 1, 0)]), luma(row[min(x + 1, W - 1)]), luma(up[x]), luma(dn[x]));
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Forward energy helpers
 
 // forward_costs (energy.hpp:196-216) of an arbitrary luma plane (the API entry;

@@ -125,3 +125,21 @@ def test_cli_enlarge_and_seams_match_oracle(tmp_path):
     for seam in port.record_seams(img, 5):
         want[np.arange(30), seam] = (255, 0, 0)
     assert np.array_equal(read_ppm(tmp_path / "s.ppm"), want)
+
+
+@pytest.mark.gpu
+def test_cli_remove_object_matches_oracle(tmp_path):
+    # cli.hpp:279-287: mask_from_image of --mask, remove_object, optional --no-restore
+    port = oracle.port()
+    img = port.make_test_image(48, 36)
+    mimg = np.zeros((36, 48, 3), np.uint8)
+    mimg[10:20, 20:26] = 255
+    write_ppm(tmp_path / "in.ppm", img)
+    write_ppm(tmp_path / "m.ppm", mimg)
+    mask = port.mask_from_image(mimg)
+    for extra, restore in (([], True), (["--no-restore"], False)):
+        out = tmp_path / f"o{int(restore)}.ppm"
+        r = run("remove-object", "--input", str(tmp_path / "in.ppm"), "--mask", str(tmp_path / "m.ppm"),
+                "--output", str(out), *extra)
+        assert r.returncode == 0, r.stderr
+        assert np.array_equal(read_ppm(out), port.remove_object(img, mask, False, restore)[0])

@@ -236,3 +236,29 @@ def test_forward_port_vs_reference_random(port):
             a, sa = port.carve_cfg(img, tw, th, fwd, rec, seams=True)
             b, sb = ref.carve_cfg(img, tw, th, fwd, rec, seams=True)
             assert np.array_equal(a, b) and np.array_equal(sa, sb)
+
+
+# -- object removal ------------------------------------------------
+def _seam_len(mask):
+    ys, xs = np.nonzero(mask)
+    h, w = mask.shape
+    return h if xs.max() - xs.min() <= ys.max() - ys.min() else w
+
+
+def test_masks_golden(port):
+    z = np.load(os.path.join(GOLD, "masks.npz"))
+    for k in range(int(z["n"])):
+        img, mask = z[f"img{k}"], z[f"mask{k}"]
+        assert np.array_equal(fbits(port.apply_mask(z[f"e{k}"], mask)), fbits(z[f"biased{k}"])), k
+        assert np.array_equal(port.mask_from_image(img), z[f"mfi{k}"]), k
+        fwd, restore = (int(v) for v in z[f"flags{k}"])
+        n = int(z[f"n{k}"])
+        if n < 0:
+            with pytest.raises(oracle.OracleError) as ei:
+                port.remove_object(img, mask, fwd, restore)
+            assert ei.value.status == -n, k
+            continue
+        res, seams, got_n = port.remove_object(img, mask, fwd, restore)
+        L = n * _seam_len(mask)
+        assert got_n == n and np.array_equal(res, z[f"res{k}"]), k
+        assert np.array_equal(seams[:L], z[f"seams{k}"][:L]), k

@@ -110,6 +110,21 @@ static int selftest() {
         for (size_t a = 0; a < rec.size(); ++a)
             for (size_t b = a + 1; b < rec.size(); ++b) EXPECT(rec[a][i] != rec[b][i]);
     EXPECT(thrown([] { record_seams(PixelGrid(4, 4), 4); }) == Errc::invalid_target);
+    // apply_mask / remove_object (test_energy.cpp:209-216, test_carver.cpp:279-287, :335-344)
+    EnergyMap unit{3, 3, std::vector<double>(9, 1.0)};
+    for (double v : apply_mask(unit, RemovalMask{3, 3, std::vector<uint8_t>(9, 1)}).values) EXPECT(v == -4000.0);
+    PixelGrid gc(5, 5);
+    const uint8_t gv[5] = {50, 120, 60, 70, 80};
+    for (int i = 0; i < 5; ++i)
+        for (int j = 0; j < 5; ++j) gc.at(i, j) = Rgb{gv[j], gv[j], gv[j]};
+    RemovalMask col{5, 5, std::vector<uint8_t>(25, 0)};
+    for (int i = 0; i < 5; ++i) col.set(i, 1, true);
+    auto [ro, rrep2] = remove_object(gc, col);
+    EXPECT(rrep2.seam_count == 1 && (rrep2.seams[0] == Seam{1, 1, 1, 1, 1}) && ro.width == 5 && ro.height == 5);
+    EXPECT(thrown([] { remove_object(PixelGrid(4, 4), RemovalMask{4, 4, std::vector<uint8_t>(16, 0)}); }) ==
+           Errc::empty_mask);
+    EXPECT(thrown([] { remove_object(PixelGrid(4, 4), RemovalMask{3, 4, std::vector<uint8_t>(12, 1)}); }) ==
+           Errc::dimension_mismatch);
     std::printf(failures ? "selftest FAILED (%d)\n" : "selftest ok\n", failures);
     return failures ? 1 : 0;
 }
