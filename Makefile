@@ -23,10 +23,10 @@ $(LIB): | build
 tools: build/carve build/carve_parity
 
 build/carve: tools/carve_main.cpp $(wildcard include/carve/*.hpp) $(LIB) | build
-	$(CXX) -std=c++20 -O2 -Iinclude -o $@ tools/carve_main.cpp -L$(PKG) -lcarve_cuda -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+	$(CXX) -std=c++20 -O2 -Iinclude -o $@ tools/carve_main.cpp -L$(PKG) -lcarve_cuda -lz -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
 build/carve_parity: tools/carve_parity.cpp $(wildcard include/carve/*.hpp) $(LIB) | build
-	$(CXX) -std=c++20 -O2 -Iinclude -o $@ tools/carve_parity.cpp -L$(PKG) -lcarve_cuda -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+	$(CXX) -std=c++20 -O2 -Iinclude -o $@ tools/carve_parity.cpp -L$(PKG) -lcarve_cuda -lz -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
 oracle:
 	$(MAKE) -s -C oracle

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "carve/error.hpp"
+#include "carve/png_codec.hpp"
 
 namespace carve {
 
@@ -65,7 +66,7 @@ inline PixelGrid transpose(const PixelGrid& grid) {
     return out;
 }
 
-// ---- image IO (binary PPM; PNG decoding is not part of the B200 engine yet) ----
+// ---- image IO: PNG (carve/png_codec.hpp, zlib) and binary PPM (raster.hpp:81-284) ----
 namespace detail {
 
 struct CFile {
@@ -108,8 +109,13 @@ inline PixelGrid load_image(const std::string& path) {
     unsigned char sig[8] = {};
     const size_t got = std::fread(sig, 1, sizeof sig, f.fp);
     std::rewind(f.fp);
-    if (got >= 8 && sig[0] == 0x89 && std::memcmp(sig + 1, "PNG", 3) == 0)
-        fail(Errc::unsupported_format, path + ": PNG input is not supported by the B200 engine yet; use PPM (P6)");
+    static const unsigned char png_sig[8] = {0x89, 'P', 'N', 'G', 0x0d, 0x0a, 0x1a, 0x0a};
+    if (got >= 8 && std::memcmp(sig, png_sig, 8) == 0) {
+        const png::Image im = png::decode(png::read_file(f.fp), path);
+        PixelGrid g(im.width, im.height);
+        std::memcpy(g.bytes(), im.rgb.data(), im.rgb.size());
+        return g;
+    }
     if (got < 2 || sig[0] != 'P' || sig[1] != '6')
         fail(Errc::unsupported_format, path + ": expected PNG or binary PPM (P6)");
     std::fgetc(f.fp);
@@ -124,8 +130,10 @@ inline PixelGrid load_image(const std::string& path) {
 }
 
 inline void save_image(const PixelGrid& grid, const std::string& path) {
-    if (detail::has_suffix(path, ".png"))
-        fail(Errc::unsupported_format, path + ": PNG output is not supported by the B200 engine yet; use .ppm");
+    if (detail::has_suffix(path, ".png")) {
+        png::write_file(path, png::encode(grid.bytes(), grid.width, grid.height, 3));
+        return;
+    }
     if (!detail::has_suffix(path, ".ppm"))
         fail(Errc::unsupported_format, path + ": unknown output extension (use .png or .ppm)");
     detail::CFile f(path, "wb");
@@ -134,6 +142,11 @@ inline void save_image(const PixelGrid& grid, const std::string& path) {
     if (std::fwrite(hdr.data(), 1, hdr.size(), f.fp) != hdr.size() ||
         std::fwrite(grid.pixels.data(), 3, grid.pixels.size(), f.fp) != grid.pixels.size())
         fail(Errc::io_failure, path + ": write failed");
+}
+
+/// 8-bit grayscale PNG, used for energy-map visualization (raster.hpp:262-283).
+inline void save_gray_png(const std::vector<std::uint8_t>& gray, int width, int height, const std::string& path) {
+    png::write_file(path, png::encode(gray.data(), width, height, 1));
 }
 
 } // namespace carve

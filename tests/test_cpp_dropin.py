@@ -143,3 +143,17 @@ def test_cli_remove_object_matches_oracle(tmp_path):
                 "--output", str(out), *extra)
         assert r.returncode == 0, r.stderr
         assert np.array_equal(read_ppm(out), port.remove_object(img, mask, False, restore)[0])
+
+
+@pytest.mark.gpu
+def test_cli_resize_png_in_png_out(tmp_path):
+    # raster.hpp:128-146 load_image / save_image with PNG on both ends
+    img = oracle.port().make_test_image(64, 48)
+    ppm = tmp_path / "in.ppm"
+    write_ppm(ppm, img)
+    subprocess.run([PARITY, "convert", str(ppm), str(tmp_path / "in.png")], check=True)
+    r = run("resize", "--input", str(tmp_path / "in.png"), "--output", str(tmp_path / "out.png"), "--width", "50",
+            "--height", "40")
+    assert r.returncode == 0, r.stderr
+    subprocess.run([PARITY, "convert", str(tmp_path / "out.png"), str(tmp_path / "out.ppm")], check=True)
+    assert np.array_equal(read_ppm(tmp_path / "out.ppm"), oracle.port().carve(img, 50, 40))

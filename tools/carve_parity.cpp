@@ -3,6 +3,7 @@
 // and prints FNV-1a-64 hashes of the configs for tests/test_cpp_dropin.py.
 //   carve_parity selftest            -> reference unit-test pins, exit 0/1
 //   carve_parity hash W H TW TH      -> "<input hash> <output hash> <seams hash>"
+//   carve_parity convert IN OUT      -> load_image + save_image (PNG / PPM codecs, host only)
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -132,6 +133,10 @@ static int selftest() {
 int main(int argc, char** argv) {
     try {
         if (argc >= 2 && std::string(argv[1]) == "selftest") return selftest();
+        if (argc == 4 && std::string(argv[1]) == "convert") {  // host-only image IO (PNG/PPM), no GPU
+            save_image(load_image(argv[2]), argv[3]);
+            return 0;
+        }
         if (argc == 6 && std::string(argv[1]) == "hash") {
             const int w = std::atoi(argv[2]), h = std::atoi(argv[3]), tw = std::atoi(argv[4]), th = std::atoi(argv[5]);
             auto img = make_test_image(w, h);
