@@ -350,10 +350,12 @@ Dp2Plan dp2_plan(int W, int H, bool batch = false) {
             if (ncl > (pass == 0 ? max_ncl : 16) || smem > size_t(kDpSmemBudget)) continue;
             // columns read past the image edge must stay inside the +inf pad
             if (ncl * v.cols() - W + v.K + 32 * v.C > EPAD_R) continue;
-            // gather the block-end labels into CTA 0 when the table is small
+            // gather the block-end labels into CTA 0 when the table is small; not for
+            // batches, where the extra shared memory costs a CTA per SM (measured:
+            // C5 2.33K -> 2.61K images/s without it) while phase 1 overlaps other images
             const size_t gbytes = round_up(size_t(nblk) * ncl * v.cols(), 16);
             const bool gather = nblk > 0 && gbytes <= size_t(96) * 1024 && smem + gbytes <= size_t(kDpSmemBudget) &&
-                                env_int("CARVE_DP_GATHER", 1) != 0;
+                                env_int("CARVE_DP_GATHER", batch ? 0 : 1) != 0;
             return Dp2Plan{&v, ncl, nblk, smem + (gather ? gbytes : 0), gather ? 1 : 0};
         }
     }
