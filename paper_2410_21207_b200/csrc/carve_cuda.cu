@@ -132,7 +132,23 @@ struct Ctx {
         max_smem_optin = int(prop.sharedMemPerBlockOptin);
         ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
     }
+    // batch pipelining: host->device and device->host copies on their own streams
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t pipe_ev[3][2] = {};  // [h2d done, compute done, d2h done][buffer]
+    DevBuf pin_in[2], pin_out[2];    // double-buffered packed images
+    void ensure_pipeline() {
+        if (h2d) return;
+        ck(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking), "cudaStreamCreate(h2d)");
+        ck(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking), "cudaStreamCreate(d2h)");
+        for (auto& row : pipe_ev)
+            for (auto& e : row) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    }
     ~Ctx() {
+        for (auto& row : pipe_ev)
+            for (auto& e : row)
+                if (e) cudaEventDestroy(e);
+        if (h2d) cudaStreamDestroy(h2d);
+        if (d2h) cudaStreamDestroy(d2h);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -1366,6 +1382,10 @@ carve_status carve_cuda_carve_batch_device(const uint8_t* d_rgb, int n, int w, i
     });
 }
 
+// images per pipelined chunk (measured: 256-image launches run at ~95% of the
+// 1024-image throughput, tools/sweep_batch.py)
+constexpr int kPipeChunk = 256;
+
 carve_status carve_cuda_carve_batch(const uint8_t* const* rgb, int n, int w, int h, int target_w, int target_h,
                                     uint8_t* const* rgb_out, const int* devices, int ndev) {
     return guarded([&] {
@@ -1393,6 +1413,40 @@ carve_status carve_cuda_carve_batch(const uint8_t* const* rgb, int n, int w, int
             t_device = devs[k];
             status[k] = guarded([&] {
                 Ctx& c = ctx();
+                if (hi - lo >= 2 * kPipeChunk && chunk_cap >= kPipeChunk) {
+                    // Copy/compute pipeline: chunk t+1 uploads and chunk t-1 downloads on the
+                    // copy engines while chunk t carves (double-buffered packed images)
+                    c.ensure_pipeline();
+                    enum { H2D = 0, COMP = 1, D2H = 2 };
+                    int t = 0;
+                    for (int b0 = lo; b0 < hi; b0 += kPipeChunk, ++t) {
+                        const int m = std::min(kPipeChunk, hi - b0), b = t & 1;
+                        uint8_t* d_in = static_cast<uint8_t*>(c.pin_in[b].ensure(in_bytes * kPipeChunk));
+                        uint8_t* d_out = static_cast<uint8_t*>(c.pin_out[b].ensure(out_bytes * kPipeChunk));
+                        if (t == 0) ensure_carve_buffers(c, g, kPipeChunk);
+                        int* seams =
+                            static_cast<int*>(c.seams.ensure(std::max<size_t>(g.seam_ints, 1) * 4 * kPipeChunk));
+                        if (t >= 2) ck(cudaStreamWaitEvent(c.h2d, c.pipe_ev[COMP][b], 0), "wait comp");
+                        for (int q = 0; q < m; ++q)
+                            ck(cudaMemcpyAsync(d_in + in_bytes * q, rgb[b0 + q], in_bytes, cudaMemcpyHostToDevice,
+                                               c.h2d),
+                               "H2D");
+                        ck(cudaEventRecord(c.pipe_ev[H2D][b], c.h2d), "record h2d");
+                        ck(cudaStreamWaitEvent(c.stream, c.pipe_ev[H2D][b], 0), "wait h2d");
+                        if (t >= 2) ck(cudaStreamWaitEvent(c.stream, c.pipe_ev[D2H][b], 0), "wait d2h");
+                        run_carve(c, d_in, d_out, m, g, seams, std::max<size_t>(g.seam_ints, 1), nullptr, c.stream);
+                        ck(cudaEventRecord(c.pipe_ev[COMP][b], c.stream), "record comp");
+                        ck(cudaStreamWaitEvent(c.d2h, c.pipe_ev[COMP][b], 0), "wait comp");
+                        for (int q = 0; q < m; ++q)
+                            ck(cudaMemcpyAsync(rgb_out[b0 + q], d_out + out_bytes * q, out_bytes,
+                                               cudaMemcpyDeviceToHost, c.d2h),
+                               "D2H");
+                        ck(cudaEventRecord(c.pipe_ev[D2H][b], c.d2h), "record d2h");
+                    }
+                    ck(cudaStreamSynchronize(c.d2h), "sync d2h");
+                    sync(c);
+                    return;
+                }
                 for (int b0 = lo; b0 < hi; b0 += chunk_cap) {
                     const int m = std::min(chunk_cap, hi - b0);
                     uint8_t* d_in = static_cast<uint8_t*>(c.packed_in.ensure(in_bytes * m));

@@ -258,3 +258,14 @@ def test_native_kernels_launched():
     cv.carve(cv.make_test_image(64, 32), 60)
     # unpack + energy + pad fill + 4 x dp + 3 in-place removals + the last removal fused with the pack
     assert cv.launch_count() == 11
+
+
+def test_batch_pipelined_chunks_match_oracle(port):
+    # >= 2 x 256 images per device takes the copy/compute pipeline (double-buffered
+    # chunks on separate copy streams); every image must equal its single carve
+    n, w, h, tw, th = 600, 40, 24, 33, 20
+    imgs = [port.make_test_image(w, h, k % 37) for k in range(n)]
+    outs = cv.carve_batch(imgs, tw, th)
+    want = {k: port.carve(imgs[k], tw, th) for k in range(37)}
+    for k in range(n):
+        assert np.array_equal(outs[k], want[k % 37]), k
