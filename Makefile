@@ -7,13 +7,19 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -fmad=false -Xcompiler -fPIC -Xptxas -v -Iinclude
 PKG := paper_2410_21207_b200
 LIB := $(PKG)/libcarve_cuda.so
-SRC := $(PKG)/csrc/carve_cuda.cu
-HDR := $(wildcard $(PKG)/csrc/*.cuh) include/carve_cuda.h
+# the DP variant instances compile in their own translation units (in parallel: make -j)
+SRCS := $(PKG)/csrc/carve_cuda.cu $(PKG)/csrc/dp_variants_a.cu $(PKG)/csrc/dp_variants_b.cu $(PKG)/csrc/dp_variants_c.cu
+OBJS := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRCS))
+HDR := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.h) include/carve_cuda.h
 
 all: $(LIB) oracle tools
 
-$(LIB): $(SRC) $(HDR)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC) 2> build/ptxas.log || (cat build/ptxas.log; false)
+build/%.o: $(PKG)/csrc/%.cu $(HDR) | build
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
+	cat build/*.ptxas.log > build/ptxas.log
 
 build:
 	@mkdir -p build

@@ -5,6 +5,7 @@
 #include "carve_cuda.h"
 #include "carve_kernels.cuh"
 #include "dp_cluster.cuh"
+#include "dp_variants.h"
 
 #include <algorithm>
 #include <atomic>
@@ -281,43 +282,19 @@ bool pdl_enabled() {
 }
 
 // ---- K2+K3 v2: cluster trapezoid DP (dp_cluster.cuh) ------------------------
-struct Dp2Variant {
-    int C, K, NW, D;
-    const void* fn;        // hot kernel (no tables)
-    const void* fn_tables; // parity-API kernel (writes the full cost / predecessor tables)
-    const void* fn_prof;   // hot kernel + clock64 phase counters (tools)
-    const void* fn_fused;  // hot kernel, energy recomputed from RGBX (batch mode)
-    const void* fn_fwd;    // forward energy from RGBX rows (fused), hot / with tables
-    const void* fn_fwd_tables;
-    const void* fn_fwdp;   // forward energy from an FP64 luma plane (dp_seam_forward API)
-    const void* fn_fwdp_tables;
-    size_t (*smem)(int nblk, int D);
-    int S() const { return 32 * C - 2 * K; }
-    int cols() const { return NW * S(); }
-};
-
-template <int C, int K, int NW, int D>
-constexpr Dp2Variant dp2_variant() {
-    return Dp2Variant{C, K, NW, D, (const void*)k_dp2<C, K, NW, D, 0>, (const void*)k_dp2<C, K, NW, D, 1>,
-                      (const void*)k_dp2<C, K, NW, D, 2>, (const void*)k_dp2<C, K, NW, D, 0, true>,
-                      (const void*)k_dp2<C, K, NW, D, 0, true, true>, (const void*)k_dp2<C, K, NW, D, 1, true, true>,
-                      (const void*)k_dp2<C, K, NW, D, 0, false, true>, (const void*)k_dp2<C, K, NW, D, 1, false, true>,
-                      &Dp2Smem<C, K, NW>::total};
+// The variant table is instantiated in dp_variants_*.cu (separate translation
+// units, compiled in parallel); indices are stable (CARVE_DP_VARIANT, orders below).
+const std::vector<Dp2Variant>& dp2_variants() {
+    static const std::vector<Dp2Variant> v = [] {
+        std::vector<Dp2Variant> t;
+        dp2_variants_a(t);
+        dp2_variants_b(t);
+        dp2_variants_c(t);
+        return t;
+    }();
+    return v;
 }
-
-// preference order: the first variant whose cluster fits (<= 8 CTAs, then <= 16) wins
-const Dp2Variant kDp2Variants[] = {
-    dp2_variant<2, 16, 4, 16>(),  // 0: S=32,  128 cols/CTA, one warp per scheduler (C1/C2/C5-wide rows)
-    dp2_variant<2, 16, 8, 16>(),  // 1: S=32,  256 cols/CTA (C3, up to 4096 columns)
-    dp2_variant<2, 16, 8, 8>(),   // 2: S=32,  256 cols/CTA, 8-row ring
-    dp2_variant<4, 16, 8, 8>(),   // 3: S=96,  768 cols/CTA (C4: 7680 columns in 10 CTAs)
-    dp2_variant<2, 8, 16, 8>(),   // 4: S=48,  768 cols/CTA
-    dp2_variant<4, 16, 4, 8>(),   // 5: S=96,  384 cols/CTA (batches)
-    dp2_variant<4, 16, 4, 16>(),  // 6: S=96,  384 cols/CTA, 16-row ring
-    dp2_variant<4, 32, 4, 8>(),   // 7: S=64,  256 cols/CTA
-    dp2_variant<2, 16, 4, 8>(),   // 8: S=32,  128 cols/CTA, 8-row ring
-};
-constexpr int kNumDp2Variants = int(sizeof(kDp2Variants) / sizeof(kDp2Variants[0]));
+#define kDp2Variants dp2_variants()
 
 void init_kernel_attributes(Ctx& c) {
     for (const Dp2Variant& v : kDp2Variants)
@@ -348,21 +325,34 @@ int env_int(const char* name, int dflt) {
 // wins. Single images are latency-bound and favour one C=2 warp per
 // scheduler; batches are throughput-bound and favour less halo redundancy.
 const int kDp2Order[] = {0, 1, 2, 3, 4, 6, 5, 7, 8};
-const int kDp2BatchOrder[] = {5, 6, 0, 1, 2, 3, 4, 7, 8};
+// large batches (>= one image per SM): one 10-warp CTA per image, 2 per SM;
+// smaller batches spread each image over a 3-CTA cluster to fill the SMs
+// (measured, tools/sweep_batch.py: 1024 images 2.05 -> 1.58 ms per seam with
+// variant 9 <4,8,10,4>; 128 images 0.32 (v9) vs 0.28 ms (v5))
+const int kDp2BatchOrder[] = {9, 5, 6, 0, 1, 2, 3, 4, 7, 8};
+const int kDp2SmallBatchOrder[] = {5, 6, 0, 1, 2, 3, 4, 7, 8};
 
-Dp2Plan dp2_plan(int W, int H, bool batch = false) {
+int device_sm_count() {
+    int dev = 0, nsm = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "SM count");
+    return nsm;
+}
+
+Dp2Plan dp2_plan(int W, int H, bool batch = false, bool fused = false, int nimg = 1) {
     const int nblk = H > 1 ? (H - 1 + LBLK - 1) / LBLK : 0;
     const int forced = env_int("CARVE_DP_VARIANT", -1);
     const int max_ncl = env_int("CARVE_DP_MAX_NCL", 16);
     for (int pass = 0; pass < 2; ++pass) {
         std::vector<int> order;
-        if (forced >= 0 && forced < kNumDp2Variants) order.push_back(forced);
-        else if (batch) order.assign(std::begin(kDp2BatchOrder), std::end(kDp2BatchOrder));
+        if (forced >= 0 && forced < int(dp2_variants().size())) order.push_back(forced);
+        else if (batch && nimg >= device_sm_count()) order.assign(std::begin(kDp2BatchOrder), std::end(kDp2BatchOrder));
+        else if (batch) order.assign(std::begin(kDp2SmallBatchOrder), std::end(kDp2SmallBatchOrder));
         else order.assign(std::begin(kDp2Order), std::end(kDp2Order));
         for (int k : order) {
             const Dp2Variant& v = kDp2Variants[k];
             const int ncl = (W + v.cols() - 1) / v.cols();
-            const size_t smem = v.smem(nblk, v.D);
+            const size_t smem = fused ? v.smem_fused(nblk, v.D) : v.smem(nblk, v.D);
             if (ncl > (pass == 0 ? max_ncl : 16) || smem > size_t(kDpSmemBudget)) continue;
             // columns read past the image edge must stay inside the +inf pad
             if (ncl * v.cols() - W + v.K + 32 * v.C > EPAD_R) continue;
@@ -426,6 +416,17 @@ void launch_compact_inplace(const CompactParams& p, int nimg, cudaStream_t s) {
             if (nb == 8) ck(cudaLaunchKernelEx(&cfg, k_compact_warp<8, true>, p), "launch k_compact_warp");
             else if (nb == 2) ck(cudaLaunchKernelEx(&cfg, k_compact_warp<2, true>, p), "launch k_compact_warp");
             else ck(cudaLaunchKernelEx(&cfg, k_compact_warp<4, true>, p), "launch k_compact_warp");
+        } else if (p.rgb_edges) {  // batches: R rows per warp
+            const int R = env_int("CARVE_COMPACT_ROWS", 2);  // measured: R=2 0.712, 1 0.730, 4 0.954 ms per seam (C5)
+            if (R > 1) {
+                cfg.gridDim = dim3((p.H + wpb * R - 1) / (wpb * R), nimg);
+                if (R == 2) ck(cudaLaunchKernelEx(&cfg, k_compact_rows<2>, p), "launch k_compact_rows");
+                else if (R == 8) ck(cudaLaunchKernelEx(&cfg, k_compact_rows<8>, p), "launch k_compact_rows");
+                else ck(cudaLaunchKernelEx(&cfg, k_compact_rows<4>, p), "launch k_compact_rows");
+                LAUNCHED("k_compact_rows");
+                return;
+            }
+            ck(cudaLaunchKernelEx(&cfg, k_compact_warp<4, false>, p), "launch k_compact_warp");
         } else {
             ck(cudaLaunchKernelEx(&cfg, k_compact_warp<4, false>, p), "launch k_compact_warp");
         }
@@ -585,7 +586,7 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
             int* seam = d_seams + seam_base + size_t(k) * H;
             unsigned long long* st = d_stamps ? d_stamps + size_t(stamp_seam0 + k) * 4 : nullptr;
             {
-                const Dp2Plan pl = dp2_plan(W, H, nimg > 1);
+                const Dp2Plan pl = dp2_plan(W, H, nimg > 1, fused, nimg);
                 Dp2Params q{};
                 q.e = e;
                 q.epitch = epitch;

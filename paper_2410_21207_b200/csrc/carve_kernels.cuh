@@ -50,8 +50,16 @@ __device__ __forceinline__ uint64_t globaltimer() {
 }
 
 // raster.hpp:68 — 0.299*r + 0.587*g + 0.114*b, left to right, no contraction.
+// byte `B` of p as an exact double: one I2F.F64.U8 with a byte selector (R.B1,
+// R.B2) instead of shift + mask + I2F.F64.U32 (5 integer ops per pixel saved)
+template <int B>
+__device__ __forceinline__ double byte_f64(uint32_t p) {
+    double d;
+    asm("{.reg .u16 t; cvt.u16.u32 t, %1; cvt.rn.f64.u8 %0, t;}" : "=d"(d) : "r"(p >> (8 * B)));
+    return d;
+}
 __device__ __forceinline__ double luma(uint32_t p) {
-    const double r = double(p & 0xffu), g = double((p >> 8) & 0xffu), b = double((p >> 16) & 0xffu);
+    const double r = byte_f64<0>(p), g = byte_f64<1>(p), b = byte_f64<2>(p);
     return __dadd_rn(__dadd_rn(__dmul_rn(0.299, r), __dmul_rn(0.587, g)), __dmul_rn(0.114, b));
 }
 
@@ -59,6 +67,9 @@ __device__ __forceinline__ double luma(uint32_t p) {
 __device__ __forceinline__ double e1(double l_left, double l_right, double l_up, double l_down) {
     return __dadd_rn(fabs(__dsub_rn(l_right, l_left)), fabs(__dsub_rn(l_down, l_up)));
 }
+
+// The DP variant translation units (dp_variants_*.cu) need only the helpers above.
+#ifndef CARVE_KERNELS_HELPERS_ONLY
 
 // ---------------------------------------------------------------------------
 // layout conversion (host boundary): packed RGB bytes <-> RGBX plane
@@ -639,6 +650,122 @@ __global__ void k_compact_transpose(const uint32_t* __restrict__ in, int ipitch,
 // kernel stays small enough for full occupancy (batches, RGBX only). The RGBX
 // replica columns -1 / W-1 the fused DP reads are written by the lanes that
 // store columns 0 / Wn-1 (no extra dependent load at the end of the row).
+// One row's in-place removal by one warp (the body of k_compact_warp, also run
+// by the fused batch DP after its backtrack): the part right of seam column s
+// moves left by one, in batches of NB 4-pixel chunks per lane.
+template <int NB, bool HAS_E>
+__device__ __forceinline__ void compact_row_warp(uint32_t* __restrict__ rgb, double* __restrict__ e, int W, int s,
+                                                 int lane, bool edges) {
+    const int Wn = W - 1;
+    // first 4-aligned chunk that changes
+    const int q0 = (s >> 2);
+    for (int qb = q0; qb * 4 < Wn; qb += 32 * NB) {
+        uint32_t o[NB][4];
+        double oe[HAS_E ? NB : 1][4];
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+            const int base = (qb + u * 32 + lane) * 4;
+            if (base < Wn) {
+                const uint4 v = *reinterpret_cast<const uint4*>(rgb + base);
+                const uint32_t a[5] = {v.x, v.y, v.z, v.w, base + 4 < W ? rgb[base + 4] : 0u};
+#pragma unroll
+                for (int t = 0; t < 4; ++t) o[u][t] = (base + t >= s) ? a[t + 1] : a[t];
+                if constexpr (HAS_E) {
+                    const double2 v0 = *reinterpret_cast<const double2*>(e + base);
+                    const double2 v1 = *reinterpret_cast<const double2*>(e + base + 2);
+                    const double b[5] = {v0.x, v0.y, v1.x, v1.y, base + 4 < W ? e[base + 4] : 0.0};
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) oe[u][t] = (base + t >= s) ? b[t + 1] : b[t];
+                }
+            }
+        }
+        __syncwarp();  // every lane's loads of this batch precede any store of it
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+            const int base = (qb + u * 32 + lane) * 4;
+            if (base + 4 <= Wn) {
+                *reinterpret_cast<uint4*>(rgb + base) = make_uint4(o[u][0], o[u][1], o[u][2], o[u][3]);
+                if constexpr (HAS_E) {
+                    *reinterpret_cast<double2*>(e + base) = make_double2(oe[u][0], oe[u][1]);
+                    *reinterpret_cast<double2*>(e + base + 2) = make_double2(oe[u][2], oe[u][3]);
+                }
+            } else if (base < Wn) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (base + t < Wn) {
+                        rgb[base + t] = o[u][t];
+                        if constexpr (HAS_E) e[base + t] = oe[u][t];
+                    }
+            }
+            if (edges && base < Wn) {  // replica columns (raster.hpp:54-58 clamping)
+                if (base == 0 && s == 0) rgb[-1] = o[u][0];
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (base + t == Wn - 1) rgb[Wn] = o[u][t];
+            }
+        }
+        __syncwarp();  // this batch's stores precede the next batch's loads
+    }
+    // seam in the row's last chunk: nothing moved, but the right replica follows column Wn-1
+    if (edges && lane == 0 && q0 * 4 >= Wn) rgb[Wn] = rgb[Wn - 1];
+    if constexpr (HAS_E) {
+        if (lane == 0) e[Wn] = dinf();  // the vacated column joins the +inf pad
+    }
+}
+
+// R rows' in-place RGBX removal by one warp at once (the fused batch DP's
+// epilogue): every lane holds one 4-pixel chunk of each of the R rows per
+// batch, so R x 512 B of loads are in flight per warp before any store. Same
+// semantics as compact_row_warp<.., false> with edges (replica columns).
+template <int R>
+__device__ __forceinline__ void compact_rows_warp(uint32_t* __restrict__ plane, long long pitch, int W, const int (&s)[R],
+                                                  int lane) {
+    const int Wn = W - 1;
+    int q0[R], nb = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        q0[r] = s[r] >> 2;
+        nb = max(nb, (Wn - 1 - q0[r] * 4 + 128) / 128);  // batches of 32 chunks this row needs (>= 0)
+    }
+    for (int t = 0; t < nb; ++t) {
+        uint32_t o[R][4];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t* row = plane + r * pitch;
+            const int base = (q0[r] + t * 32 + lane) * 4;
+            if (base < Wn) {
+                const uint4 v = *reinterpret_cast<const uint4*>(row + base);
+                const uint32_t a[5] = {v.x, v.y, v.z, v.w, base + 4 < W ? row[base + 4] : 0u};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) o[r][u] = (base + u >= s[r]) ? a[u + 1] : a[u];
+            }
+        }
+        __syncwarp();  // every lane's loads of this batch precede any store of it
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            uint32_t* row = plane + r * pitch;
+            const int base = (q0[r] + t * 32 + lane) * 4;
+            if (base + 4 <= Wn) {
+                *reinterpret_cast<uint4*>(row + base) = make_uint4(o[r][0], o[r][1], o[r][2], o[r][3]);
+            } else if (base < Wn) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (base + u < Wn) row[base + u] = o[r][u];
+            }
+            if (base < Wn) {  // replica columns (raster.hpp:54-58 clamping)
+                if (base == 0 && s[r] == 0) row[-1] = o[r][0];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (base + u == Wn - 1) row[Wn] = o[r][u];
+            }
+        }
+        __syncwarp();  // this batch's stores precede the next batch's loads
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)  // seam in the row's last chunk: only the right replica changes
+        if (lane == 0 && q0[r] * 4 >= Wn) plane[r * pitch + Wn] = plane[r * pitch + Wn - 1];
+}
+
 template <int NB, bool HAS_E>
 __global__ void __launch_bounds__(256) k_compact_warp(CompactParams p) {
     const int img = blockIdx.y;
@@ -649,65 +776,36 @@ __global__ void __launch_bounds__(256) k_compact_warp(CompactParams p) {
     if (p.stamps && blockIdx.x == 0 && threadIdx.x == 0)
         atomicCAS(&p.stamps[img * p.st_istride + 0], 0ull, (unsigned long long)globaltimer());
     if (i < p.H) {
-        const int W = p.W, Wn = W - 1;
         const int s = __ldg(p.seam + img * p.s_istride + i);
         uint32_t* rgb = p.rgb_out + img * p.p_istride + (long long)i * p.pitch;
         double* e = HAS_E ? p.e_out + img * p.e_istride + (long long)i * p.epitch : nullptr;
-        const bool edges = p.rgb_edges;
-        // first 4-aligned chunk that changes
-        const int q0 = (s >> 2);
-        for (int qb = q0; qb * 4 < Wn; qb += 32 * NB) {
-            uint32_t o[NB][4];
-            double oe[HAS_E ? NB : 1][4];
+        compact_row_warp<NB, HAS_E>(rgb, e, p.W, s, lane, p.rgb_edges);
+    }
+    if (p.stamps && threadIdx.x == 0) atomicMax(&p.stamps[img * p.st_istride + 1], (unsigned long long)globaltimer());
+}
+
+// Batches (RGBX only, replica columns refreshed): one warp removes the seam
+// from R consecutive rows at once, so R x 512 B of loads are in flight per warp
+// and the per-row seam load / ramp is amortised over R rows.
+template <int R>
+__global__ void __launch_bounds__(256) k_compact_rows(CompactParams p) {
+    const int img = blockIdx.y;
+    const int lane = threadIdx.x & 31;
+    const int i0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * R;
+    pdl_wait();  // the DP that produced this seam has completed
+    pdl_launch_dependents();
+    if (p.stamps && blockIdx.x == 0 && threadIdx.x == 0)
+        atomicCAS(&p.stamps[img * p.st_istride + 0], 0ull, (unsigned long long)globaltimer());
+    const int* seam = p.seam + img * p.s_istride;
+    uint32_t* plane = p.rgb_out + img * p.p_istride;
+    if (i0 + R <= p.H) {
+        int sr[R];
 #pragma unroll
-            for (int u = 0; u < NB; ++u) {
-                const int base = (qb + u * 32 + lane) * 4;
-                if (base < Wn) {
-                    const uint4 v = *reinterpret_cast<const uint4*>(rgb + base);
-                    const uint32_t a[5] = {v.x, v.y, v.z, v.w, base + 4 < W ? rgb[base + 4] : 0u};
-#pragma unroll
-                    for (int t = 0; t < 4; ++t) o[u][t] = (base + t >= s) ? a[t + 1] : a[t];
-                    if constexpr (HAS_E) {
-                        const double2 v0 = *reinterpret_cast<const double2*>(e + base);
-                        const double2 v1 = *reinterpret_cast<const double2*>(e + base + 2);
-                        const double b[5] = {v0.x, v0.y, v1.x, v1.y, base + 4 < W ? e[base + 4] : 0.0};
-#pragma unroll
-                        for (int t = 0; t < 4; ++t) oe[u][t] = (base + t >= s) ? b[t + 1] : b[t];
-                    }
-                }
-            }
-            __syncwarp();  // every lane's loads of this batch precede any store of it
-#pragma unroll
-            for (int u = 0; u < NB; ++u) {
-                const int base = (qb + u * 32 + lane) * 4;
-                if (base + 4 <= Wn) {
-                    *reinterpret_cast<uint4*>(rgb + base) = make_uint4(o[u][0], o[u][1], o[u][2], o[u][3]);
-                    if constexpr (HAS_E) {
-                        *reinterpret_cast<double2*>(e + base) = make_double2(oe[u][0], oe[u][1]);
-                        *reinterpret_cast<double2*>(e + base + 2) = make_double2(oe[u][2], oe[u][3]);
-                    }
-                } else if (base < Wn) {
-#pragma unroll
-                    for (int t = 0; t < 4; ++t)
-                        if (base + t < Wn) {
-                            rgb[base + t] = o[u][t];
-                            if constexpr (HAS_E) e[base + t] = oe[u][t];
-                        }
-                }
-                if (edges && base < Wn) {  // replica columns (raster.hpp:54-58 clamping)
-                    if (base == 0 && s == 0) rgb[-1] = o[u][0];
-#pragma unroll
-                    for (int t = 0; t < 4; ++t)
-                        if (base + t == Wn - 1) rgb[Wn] = o[u][t];
-                }
-            }
-            __syncwarp();  // this batch's stores precede the next batch's loads
-        }
-        // seam in the row's last chunk: nothing moved, but the right replica follows column Wn-1
-        if (edges && lane == 0 && q0 * 4 >= Wn) rgb[Wn] = rgb[Wn - 1];
-        if constexpr (HAS_E) {
-            if (lane == 0) e[Wn] = dinf();  // the vacated column joins the +inf pad
-        }
+        for (int r = 0; r < R; ++r) sr[r] = __ldg(seam + i0 + r);
+        compact_rows_warp<R>(plane + (long long)i0 * p.pitch, p.pitch, p.W, sr, lane);
+    } else {
+        for (int i = i0; i < p.H; ++i)
+            compact_row_warp<4, false>(plane + (long long)i * p.pitch, nullptr, p.W, __ldg(seam + i), lane, true);
     }
     if (p.stamps && threadIdx.x == 0) atomicMax(&p.stamps[img * p.st_istride + 1], (unsigned long long)globaltimer());
 }
@@ -934,5 +1032,7 @@ __global__ void k_expand_rows(const uint8_t* __restrict__ in, int W, int H, cons
         running += __shfl_sync(FULL, incl, 31);
     }
 }
+
+#endif  // CARVE_KERNELS_HELPERS_ONLY
 
 }  // namespace carve_dev

@@ -78,18 +78,24 @@ struct Dp2Params {
     int gather;  // 1: CTA 0 holds a gathered copy of every CTA's block-end labels (phase 1 stays local)
 };
 
-// smem layout (dynamic): labels int8 [nblk][NWARP*S] | mailbox | phase-2 dirs | reduce
-template <int C, int K, int NWARP>
+// smem layout (dynamic): labels int8 [nblk][NWARP*S], aliased by the phase-2
+// dirs (labels are dead once phase 1 has hopped through them) | mailbox |
+// reduce | energy/RGBX ring | gathered label table (optional)
+// RE = ring bytes per column: FP64 energies, or RGBX pixels in the fused mode
+template <int C, int K, int NWARP, int RE = 8>
 struct Dp2Smem {
     static constexpr int S = 32 * C - 2 * K;
     static constexpr int COLS = NWARP * S;  // useful columns per CTA
     __host__ __device__ static size_t labels_bytes(int nblk) { return (size_t(nblk) * COLS + 15) & ~size_t(15); }
     static constexpr size_t mail_bytes = size_t(2) * NWARP * 2 * K * (8 + 4);
     static constexpr size_t p2_bytes = size_t(NWARP) * LBLK * P2_COLS;
+    __host__ __device__ static size_t lp2_bytes(int nblk) {
+        return labels_bytes(nblk) > p2_bytes ? labels_bytes(nblk) : p2_bytes;
+    }
     static constexpr size_t red_bytes = 64 * 16 + NWARP * 2 * 8;  // argmin scratch + halo mbarriers
-    __host__ __device__ static constexpr size_t ring_bytes(int D) { return size_t(NWARP) * D * 32 * C * 8; }
+    __host__ __device__ static constexpr size_t ring_bytes(int D) { return size_t(NWARP) * D * 32 * C * RE; }
     __host__ __device__ static size_t total(int nblk, int D) {
-        return labels_bytes(nblk) + mail_bytes + p2_bytes + red_bytes + ring_bytes(D);
+        return lp2_bytes(nblk) + mail_bytes + red_bytes + ring_bytes(D);
     }
 };
 
@@ -275,14 +281,15 @@ __device__ __forceinline__ void argmin_combine(double& v, int& i, double ov, int
 // above and current — from RGBX rows (FUSED) or, for the dp_seam_forward API,
 // from an FP64 luma plane streamed through the ring in place of the energy
 // plane (its columns -1 and W replicate the edge columns, like the RGBX planes).
-template <int C, int K, int NWARP, int D, int MODE, bool FUSED = false, bool FWD = false>
-__global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
+template <int C, int K, int NWARP, int D, int MODE, bool FUSED = false, bool FWD = false, int MINB = 1>
+__global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
     constexpr bool TABLES = MODE == 1;
     constexpr bool PROF = MODE == 2;
     long long pf_t0 = 0, pf_wait = 0;
     if constexpr (PROF) pf_t0 = clock64();
     static_assert(K % C == 0 && (32 * C) > 2 * K, "halo must be whole lanes and leave useful columns");
-    using SM = Dp2Smem<C, K, NWARP>;
+    constexpr int RE = FUSED ? 4 : 8;  // ring bytes per column
+    using SM = Dp2Smem<C, K, NWARP, RE>;
     constexpr int S = SM::S;
     constexpr int KL = K / C;  // lanes per halo
     extern __shared__ __align__(16) unsigned char dsm[];
@@ -302,15 +309,15 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     const int cta_col0 = cta * SM::COLS;
 
     int8_t* labels = reinterpret_cast<int8_t*>(dsm);
-    double* mail_m = reinterpret_cast<double*>(dsm + SM::labels_bytes(nblk));  // [2][NWARP][2][K]
+    uint8_t* p2 = dsm;  // phase-2 dirs alias the labels
+    double* mail_m = reinterpret_cast<double*>(dsm + SM::lp2_bytes(nblk));  // [2][NWARP][2][K]
     int* mail_l = reinterpret_cast<int*>(mail_m + 2 * NWARP * 2 * K);
-    uint8_t* p2 = reinterpret_cast<uint8_t*>(mail_l + 2 * NWARP * 2 * K);
-    double* red_v = reinterpret_cast<double*>(p2 + SM::p2_bytes);
+    double* red_v = reinterpret_cast<double*>(mail_l + 2 * NWARP * 2 * K);
     int* red_i = reinterpret_cast<int*>(red_v + 32);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(red_v + 64);  // [NWARP][2 parities]: my halos have landed
-    double* ring_s = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(red_v) + SM::red_bytes);
-    // this lane's C doubles of stage u: ring_s[((warp * D + u) * 32 + lane) * C]
-    const uint32_t ring_lane = smem_u32(ring_s + (size_t(warp) * D * 32 + lane) * C);
+    unsigned char* ring_b = reinterpret_cast<unsigned char*>(red_v) + SM::red_bytes;
+    // this lane's C columns of stage u: ring_b[(((warp * D + u) * 32 + lane) * C) * RE]
+    const uint32_t ring_lane = smem_u32(ring_b + (size_t(warp) * D * 32 + lane) * C * RE);
 
     pdl_wait();  // the previous removal has completed (its planes and seam log are visible)
     pdl_launch_dependents();
@@ -435,7 +442,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     auto fetch = [&](int u) {  // this lane's C values of the next row -> ring stage u, one commit group per row
         if constexpr (FUSED) {
             const uint32_t* src = rgbf + (long long)min(frow, H - 1) * p.rpitch;
-            const uint32_t dst = ring_lane + uint32_t(u * 32 * C * 8);
+            const uint32_t dst = ring_lane + uint32_t(u * 32 * C * RE);
             if constexpr (C == 2) cp_async8(dst, src);
             else {
 #pragma unroll
@@ -456,7 +463,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
         cp_async_wait<D - 1>();  // the oldest of the D groups in flight has landed
         double ev[C], fcl[C], fcu[C], fcr[C];  // energies, or forward transition costs (FWD)
         if constexpr (FUSED) {
-            const uint32_t* src = reinterpret_cast<const uint32_t*>(ring_s + ((size_t(warp) * D + u) * 32 + lane) * C);
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(ring_b + ((size_t(warp) * D + u) * 32 + lane) * C * RE);
             uint32_t px[C];
 #pragma unroll
             for (int k = 0; k < C; ++k) px[k] = src[k];
@@ -466,7 +473,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
             if constexpr (FWD) fwd_cols<C>(Lp, Lc, oob, fcl, fcu, fcr);
             else energy_cols<C>(Lp, Lc, Ln, oob, ev);
         } else {
-            const double* src = ring_s + ((size_t(warp) * D + u) * 32 + lane) * C;
+            const double* src = reinterpret_cast<const double*>(ring_b + ((size_t(warp) * D + u) * 32 + lane) * C * RE);
 #pragma unroll
             for (int k = 0; k < C; k += 2) {
                 const double2 x = *reinterpret_cast<const double2*>(src + k);
@@ -653,7 +660,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     if constexpr (PROF) pf_fwd = clock64();
     // Small label tables are gathered into CTA 0 (plain DSMEM word stores, ordered
     // by the cluster barrier below) so phase 1's block-to-block hops are local.
-    int8_t* gtab = reinterpret_cast<int8_t*>(reinterpret_cast<unsigned char*>(ring_s) + SM::ring_bytes(D));
+    int8_t* gtab = reinterpret_cast<int8_t*>(ring_b + SM::ring_bytes(D));
     const int GS = G * S;  // gathered row stride (bytes)
     if (p.gather) {
         __syncthreads();  // every warp of this CTA has stored its block-end labels
@@ -721,10 +728,11 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
     // ---- K3b phase 2: every warp recomputes blocks g, g+G, ... in a 128-column window
     {
         uint8_t* dirs = p2 + size_t(warp) * LBLK * P2_COLS;
-        // phase-2 ring: this warp's forward-ring region, P2D rows of 128 doubles
+        // phase-2 ring: this warp's forward-ring region, P2D rows of 128 columns
         constexpr int P2D = (D * C) / 4;
+        constexpr int P2STAGE = P2_COLS * RE;  // bytes per phase-2 ring row
         static_assert(P2D >= 2, "phase-2 ring needs at least two stages");
-        const double* p2ring_ptr = ring_s + size_t(warp) * D * 32 * C + lane * 4;
+        const unsigned char* p2ring_ptr = ring_b + size_t(warp) * D * 32 * C * RE + lane * 4 * RE;
         const uint32_t p2ring = smem_u32(p2ring_ptr);
         for (int b = g; b < nblk && !(p.dbg & 1); b += G) {
             const int r0 = 1 + LBLK * b, r1 = min(LBLK * (b + 1), H - 1);
@@ -765,7 +773,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
                 }
             }
             auto p2fetch = [&](int r, int slot) {
-                const uint32_t dst = p2ring + uint32_t(slot * P2_COLS * 8);
+                const uint32_t dst = p2ring + uint32_t(slot * P2STAGE);
                 if constexpr (FUSED) {
                     cp_async16(dst, wrgb + (long long)min(r + 1, H - 1) * p.rpitch);
                 } else {
@@ -782,7 +790,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
                 cp_async_wait<P2D - 1>();
                 double ec[4], qcl[4], qcu[4], qcr[4];
                 if constexpr (FUSED) {
-                    const uint4 q = *reinterpret_cast<const uint4*>(p2ring_ptr + slot * P2_COLS);
+                    const uint4 q = *reinterpret_cast<const uint4*>(p2ring_ptr + slot * P2STAGE);
                     const uint32_t px[4] = {q.x, q.y, q.z, q.w};
                     luma_cols<4>(px, QLn);
                     if constexpr (FWD) fwd_cols<4>(QLp, QLc, qoob, qcl, qcu, qcr);
@@ -790,7 +798,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1) k_dp2(Dp2Params p) {
 #pragma unroll
                     for (int k = 0; k < 4; ++k) { QLp[k] = QLc[k]; QLc[k] = QLn[k]; }
                 } else {
-                    const double* src = p2ring_ptr + slot * P2_COLS;
+                    const double* src = reinterpret_cast<const double*>(p2ring_ptr + slot * P2STAGE);
                     const double2 x0 = *reinterpret_cast<const double2*>(src);
                     const double2 x1 = *reinterpret_cast<const double2*>(src + 2);
                     ec[0] = x0.x; ec[1] = x0.y; ec[2] = x1.x; ec[3] = x1.y;

@@ -1,0 +1,12 @@
+// DP variants 9- (large batches: one 10-warp CTA per image up to 1120 columns,
+// two CTAs per SM; measured on B200 against K=4 / K=16 / C=8 / 9-warp shapes,
+// DESIGN.md §4.3b)
+#define CARVE_KERNELS_HELPERS_ONLY
+#include "carve_kernels.cuh"
+#include "dp_variants.h"
+
+namespace carve_dev {
+void dp2_variants_c(std::vector<Dp2Variant>& t) {
+    t.push_back(dp2_variant<4, 8, 10, 4, 2>());  // 9: S=112, 1120 cols/CTA, 4-row ring
+}
+}  // namespace carve_dev
