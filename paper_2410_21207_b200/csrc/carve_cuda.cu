@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -182,7 +183,28 @@ struct Prof {
     }
 };
 
+// batch pipelines run on long-lived contexts keyed by (device, pipeline) instead
+// of the calling thread's, so their worker threads (created per call) reuse the
+// streams and device buffers; each slot's mutex serialises concurrent callers
+thread_local Ctx* t_ctx_override = nullptr;
+struct PipeSlot {
+    std::mutex m;
+    std::unique_ptr<Ctx> c;
+};
+PipeSlot& pipe_slot(int dev, int pipe) {
+    static std::mutex gm;
+    static std::map<std::pair<int, int>, std::unique_ptr<PipeSlot>> slots;
+    std::lock_guard<std::mutex> lk(gm);
+    auto& p = slots[{dev, pipe}];
+    if (!p) p = std::make_unique<PipeSlot>();
+    return *p;
+}
+
 Ctx& ctx() {
+    if (t_ctx_override) {
+        ck(cudaSetDevice(t_ctx_override->device), "cudaSetDevice");
+        return *t_ctx_override;
+    }
     auto it = t_ctx.find(t_device);
     if (it == t_ctx.end()) {
         int n = 0;
@@ -1408,11 +1430,23 @@ carve_status carve_cuda_carve_batch(const uint8_t* const* rgb, int n, int w, int
         const int chunk_cap = int(std::max<size_t>(1, (size_t(48) << 30) / per_img));
         std::vector<int> status(ndev, CARVE_OK);
         std::vector<std::string> msgs(ndev);
-        auto worker = [&](int k) {
-            const int lo = int((long long)n * k / ndev), hi = int((long long)n * (k + 1) / ndev);
+        // Per device: one host thread per pipeline. A device with at least 4 chunks
+        // runs two pipelines on halves of its share (each thread has its own context:
+        // stream, buffers), so one pipeline's launches fill the other's wave tails.
+        auto worker = [&](int k, int pipe, int lo, int hi, int& st_out, std::string& msg_out) {
             if (lo >= hi) return;
             t_device = devs[k];
-            status[k] = guarded([&] {
+            PipeSlot& slot = pipe_slot(devs[k], pipe);
+            std::lock_guard<std::mutex> lk(slot.m);
+            st_out = guarded([&] {
+                if (!slot.c) {
+                    slot.c = std::make_unique<Ctx>(devs[k]);
+                    init_kernel_attributes(*slot.c);
+                }
+                t_ctx_override = slot.c.get();
+                struct Reset {
+                    ~Reset() { t_ctx_override = nullptr; }
+                } reset;
                 Ctx& c = ctx();
                 if (hi - lo >= 2 * kPipeChunk && chunk_cap >= kPipeChunk) {
                     // Copy/compute pipeline: chunk t+1 uploads and chunk t-1 downloads on the
@@ -1466,12 +1500,30 @@ carve_status carve_cuda_carve_batch(const uint8_t* const* rgb, int n, int w, int
                     sync(c);
                 }
             });
-            msgs[k] = t_err;
+            if (st_out) msg_out = t_err;
+        };
+        const int pipes = env_int("CARVE_PIPELINES", 2);
+        std::vector<int> st2(ndev, CARVE_OK);
+        std::vector<std::string> msg2(ndev);
+        auto device_worker = [&](int k) {
+            const int lo = int((long long)n * k / ndev), hi = int((long long)n * (k + 1) / ndev);
+            if (pipes > 1 && hi - lo >= 4 * kPipeChunk && chunk_cap >= kPipeChunk) {
+                const int mid = lo + ((hi - lo) / 2 + kPipeChunk - 1) / kPipeChunk * kPipeChunk;
+                std::thread second([&, k, mid, hi] { worker(k, 1, mid, hi, st2[k], msg2[k]); });
+                worker(k, 0, lo, mid, status[k], msgs[k]);
+                second.join();
+                if (!status[k] && st2[k]) {
+                    status[k] = st2[k];
+                    msgs[k] = msg2[k];
+                }
+            } else {
+                worker(k, 0, lo, hi, status[k], msgs[k]);
+            }
         };
         std::vector<std::thread> pool;
-        for (int k = 1; k < ndev; ++k) pool.emplace_back(worker, k);
+        for (int k = 1; k < ndev; ++k) pool.emplace_back(device_worker, k);
         const int saved = t_device;
-        worker(0);
+        device_worker(0);
         t_device = saved;
         for (auto& th : pool) th.join();
         for (int k = 0; k < ndev; ++k)

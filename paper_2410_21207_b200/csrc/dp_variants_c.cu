@@ -1,6 +1,7 @@
 // DP variants 9- (large batches: one 10-warp CTA per image up to 1120 columns,
 // two CTAs per SM; measured on B200 against K=4 / K=16 / C=8 / 9-warp shapes,
-// DESIGN.md §4.3b)
+// DESIGN.md §4.3b). Small batches (fewer images than SMs) keep variant 5; the
+// 2- and 3-CTA shapes <2,8,8,8> <4,8,5,4> <2,8,12,8> <4,8,4,8> measured slower.
 #define CARVE_KERNELS_HELPERS_ONLY
 #include "carve_kernels.cuh"
 #include "dp_variants.h"

@@ -269,3 +269,16 @@ def test_batch_pipelined_chunks_match_oracle(port):
     want = {k: port.carve(imgs[k], tw, th) for k in range(37)}
     for k in range(n):
         assert np.array_equal(outs[k], want[k % 37]), k
+
+
+def test_batch_two_pipelines_match_oracle(port):
+    # >= 4 x 256 images per device: two concurrent copy/compute pipelines (their own
+    # long-lived contexts and streams) share the device; halves split on a chunk
+    # boundary (768 + 332 images here, the second with a ragged last chunk)
+    n, w, h, tw, th = 1100, 36, 20, 30, 17
+    imgs = [port.make_test_image(w, h, k % 41) for k in range(n)]
+    want = {k: port.carve(imgs[k], tw, th) for k in range(41)}
+    for _ in range(2):  # the second call reuses the pipeline contexts
+        outs = cv.carve_batch(imgs, tw, th)
+        for k in range(n):
+            assert np.array_equal(outs[k], want[k % 41]), k
