@@ -346,7 +346,7 @@ int env_int(const char* name, int dflt) {
 // profiles/r01_dp_variant_sweep.jsonl): the first variant whose cluster fits
 // wins. Single images are latency-bound and favour one C=2 warp per
 // scheduler; batches are throughput-bound and favour less halo redundancy.
-const int kDp2Order[] = {0, 1, 2, 3, 4, 6, 5, 7, 8};
+const int kDp2Order[] = {0, 12, 1, 11, 10, 2, 3, 4, 6, 5, 7, 8};
 // large batches (>= one image per SM): one 10-warp CTA per image, 2 per SM;
 // smaller batches spread each image over a 3-CTA cluster to fill the SMs
 // (measured, tools/sweep_batch.py: 1024 images 2.05 -> 1.58 ms per seam with

@@ -282,3 +282,26 @@ def test_batch_two_pipelines_match_oracle(port):
         outs = cv.carve_batch(imgs, tw, th)
         for k in range(n):
             assert np.array_equal(outs[k], want[k % 41]), k
+
+
+@pytest.mark.parametrize("variant", range(13))
+def test_every_dp_variant_bitexact(port, monkeypatch, variant):
+    """Each DP shape of the variant table (forced with CARVE_DP_VARIANT; the
+    default order only reaches some of them at a given width): cost tables and
+    seams of a real-valued map, a plane-mode carve and a fused batch carve."""
+    monkeypatch.setenv("CARVE_DP_VARIANT", str(variant))
+    img = port.make_test_image(500, 77)
+    e = port.energy_e1_rgb(img)
+    seam, m, b = port.dp_seam(e)
+    r = cv.dp_seam(e)
+    assert np.array_equal(r.seam, seam)
+    assert np.array_equal(bits(r.table.m), bits(m))
+    assert np.array_equal(r.table.b, b)
+    want = port.carve(img, 480, 70)
+    monkeypatch.setenv("CARVE_FUSED", "0")
+    assert np.array_equal(cv.carve(img, 480, 70), want)
+    monkeypatch.setenv("CARVE_FUSED", "1")
+    imgs = [img, port.make_test_image(500, 77, 3)]
+    outs = cv.carve_batch(imgs, 480, 70)
+    assert np.array_equal(outs[0], want)
+    assert np.array_equal(outs[1], port.carve(imgs[1], 480, 70))
