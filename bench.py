@@ -348,7 +348,7 @@ def measured_traffic(kernel, cfg_name):
     --set full capture (profiles/r01_traffic.json), for the workload it was taken on."""
     try:
         t = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
-        return t["bytes_per_launch"].get(kernel) if cfg_name == "c2" else None
+        return t["bytes_per_launch"].get(cfg_name, {}).get(kernel)
     except Exception:
         return None
 
