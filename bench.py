@@ -369,8 +369,13 @@ def roofline_of(kern, cfg_name="c2", sm_mhz=None):
     r = {"kernel": dom, "bound": "hbm", "achieved": kd["gbs"], "peak": peak, "unit": "GB/s",
          "frac": kd["gbs"] / peak, "traffic": measured_traffic(dom, cfg_name), "peak_source": peak_src,
          "bytes_per_launch": kd["bytes_per_launch"], "avg_launch_us": kd["avg_us"], "share_of_step": kd["share"],
-         # HBM fraction of every timed kernel (algorithmic bytes / event time / peak)
-         "hbm_frac_by_kernel": {k: round(v["gbs"] / peak, 4) for k, v in kern.items()}}
+         # HBM fraction of every timed kernel (algorithmic bytes / event time / peak). The removal's
+         # algorithmic bytes follow SURVEY.md §8d (a full-row copy: read W, write W-1); the in-place
+         # kernels move only the part right of the seam, so that fraction can exceed 1 — the
+         # DRAM-measured fraction (ncu bytes per launch / event time) is in dram_frac_by_kernel
+         "hbm_frac_by_kernel": {k: round(v["gbs"] / peak, 4) for k, v in kern.items()},
+         "dram_frac_by_kernel": {k: round(measured_traffic(k, cfg_name) / (v["avg_us"] * 1e3) / peak, 4)
+                                 for k, v in kern.items() if measured_traffic(k, cfg_name)}}
     if dom == "k_dp_seam" and cfg_name in DP_ROWS and cfg_name != "c5":
         ns_row = kd["avg_us"] * 1e3 / DP_ROWS[cfg_name]
         floor = CHAIN_CYCLES_PER_ROW / ((sm_mhz or 1965.0) / 1e3)

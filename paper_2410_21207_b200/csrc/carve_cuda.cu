@@ -319,6 +319,8 @@ const std::vector<Dp2Variant>& dp2_variants() {
 #define kDp2Variants dp2_variants()
 
 void init_kernel_attributes(Ctx& c) {
+    ck(cudaFuncSetAttribute(k_compact_bulk<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024),
+       "cudaFuncSetAttribute(k_compact_bulk)");
     for (const Dp2Variant& v : kDp2Variants)
         for (const void* fn :
              {v.fn, v.fn_tables, v.fn_prof, v.fn_fused, v.fn_fwd, v.fn_fwd_tables, v.fn_fwdp, v.fn_fwdp_tables}) {
@@ -438,6 +440,18 @@ void launch_compact_inplace(const CompactParams& p, int nimg, cudaStream_t s) {
             if (nb == 8) ck(cudaLaunchKernelEx(&cfg, k_compact_warp<8, true>, p), "launch k_compact_warp");
             else if (nb == 2) ck(cudaLaunchKernelEx(&cfg, k_compact_warp<2, true>, p), "launch k_compact_warp");
             else ck(cudaLaunchKernelEx(&cfg, k_compact_warp<4, true>, p), "launch k_compact_warp");
+        } else if (p.rgb_edges && env_int("CARVE_COMPACT_BULK", 1) != 0 && p.W <= 8192) {
+            // batches: TMA bulk loads of each row's moving part, SLOTS rows in flight per CTA
+            constexpr int SLOTS = 4;
+            const int rpc = env_int("CARVE_COMPACT_RPC", 8);  // rows per CTA (C5: 8 0.541, 16 0.554, 32 0.549 ms)
+            const int slot_words = int(round_up(size_t(p.W) + 4, 32));
+            cudaLaunchConfig_t bc = cfg;
+            bc.gridDim = dim3((p.H + rpc - 1) / rpc, nimg);
+            bc.blockDim = dim3(128);
+            bc.dynamicSmemBytes = size_t(SLOTS) * slot_words * 4;
+            ck(cudaLaunchKernelEx(&bc, k_compact_bulk<SLOTS>, p, rpc, slot_words), "launch k_compact_bulk");
+            LAUNCHED("k_compact_bulk");
+            return;
         } else if (p.rgb_edges) {  // batches: R rows per warp
             const int R = env_int("CARVE_COMPACT_ROWS", 2);  // measured: R=2 0.712, 1 0.730, 4 0.954 ms per seam (C5)
             if (R > 1) {

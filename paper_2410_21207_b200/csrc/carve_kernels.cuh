@@ -810,6 +810,87 @@ __global__ void __launch_bounds__(256) k_compact_rows(CompactParams p) {
     if (p.stamps && threadIdx.x == 0) atomicMax(&p.stamps[img * p.st_istride + 1], (unsigned long long)globaltimer());
 }
 
+// Batches (RGBX only, replica columns refreshed): the moving part of each row is
+// fetched by the TMA engine (cp.async.bulk global -> shared, mbarrier completion)
+// SLOTS rows ahead, so many rows' loads are in flight per CTA without holding
+// registers; the CTA's threads then store the row shifted left by one pixel from
+// shared memory (128-bit coalesced stores). In place: a row's stores start only
+// after its whole right part has landed in shared memory.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+template <int SLOTS>
+__global__ void __launch_bounds__(128) k_compact_bulk(CompactParams p, int rows_per_cta, int slot_words) {
+    extern __shared__ __align__(128) uint32_t cb_sm[];
+    __shared__ __align__(8) uint64_t cb_bar[SLOTS];
+    const int img = blockIdx.y;
+    const int row0 = blockIdx.x * rows_per_cta;
+    const int nrows = min(rows_per_cta, p.H - row0);
+    const int W = p.W, Wn = W - 1;
+    const int* seam = p.seam + img * p.s_istride + row0;
+    uint32_t* plane = p.rgb_out + img * p.p_istride + (long long)row0 * p.pitch;
+    const uint32_t bar0 = uint32_t(__cvta_generic_to_shared(cb_bar));
+    const uint32_t sm0 = uint32_t(__cvta_generic_to_shared(cb_sm));
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < SLOTS; ++k)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * k) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    pdl_wait();  // the DP that produced this seam has completed
+    pdl_launch_dependents();
+    if (p.stamps && blockIdx.x == 0 && threadIdx.x == 0)
+        atomicCAS(&p.stamps[img * p.st_istride + 0], 0ull, (unsigned long long)globaltimer());
+    // row r's moving part: 16-byte aligned from a = floor4(s) to W (rounded up to 4 pixels;
+    // the plane pitch covers the overhang)
+    auto issue = [&](int r) {
+        const int a = __ldg(seam + r) & ~3;
+        const uint32_t bytes = uint32_t(((W - a + 3) & ~3) * 4);
+        const uint32_t b = bar0 + 8 * (r % SLOTS);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+        bulk_g2s(sm0 + uint32_t((r % SLOTS) * slot_words * 4), plane + (long long)r * p.pitch + a, bytes, b);
+    };
+    if (threadIdx.x == 0)
+        for (int r = 0; r < min(SLOTS, nrows); ++r) issue(r);
+    for (int r = 0; r < nrows; ++r) {
+        const int k = r % SLOTS;
+        const uint32_t parity = uint32_t(r / SLOTS) & 1u;
+        uint32_t ok = 0;
+        while (!ok)
+            asm volatile("{ .reg .pred q; mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2; selp.u32 %0, 1, 0, q; }"
+                         : "=r"(ok)
+                         : "r"(bar0 + 8 * k), "r"(parity)
+                         : "memory");
+        const int s = __ldg(seam + r), a = s & ~3;
+        const uint32_t* src = cb_sm + k * slot_words - a;  // src[j] = old pixel j, j in [a, W)
+        uint32_t* row = plane + (long long)r * p.pitch;
+        for (int c = a + 4 * int(threadIdx.x); c < Wn; c += 4 * int(blockDim.x)) {
+            uint32_t o[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) o[u] = src[c + u + (c + u >= s ? 1 : 0)];
+            if (c + 4 <= Wn) {
+                *reinterpret_cast<uint4*>(row + c) = make_uint4(o[0], o[1], o[2], o[3]);
+            } else {
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (c + u < Wn) row[c + u] = o[u];
+            }
+            if (c == 0 && s == 0) row[-1] = o[0];  // replica columns (raster.hpp:54-58 clamping)
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (c + u == Wn - 1) row[Wn] = o[u];
+        }
+        // the seam is in the row's last 4-pixel chunk past Wn-1: nothing moves, only the right
+        // replica follows column Wn-1 (unchanged in global memory, before the loaded part)
+        if (threadIdx.x == 0 && a >= Wn) row[Wn] = row[Wn - 1];
+        __syncthreads();  // every thread is done with slot k
+        if (threadIdx.x == 0 && r + SLOTS < nrows) issue(r + SLOTS);
+    }
+    if (p.stamps && threadIdx.x == 0) atomicMax(&p.stamps[img * p.st_istride + 1], (unsigned long long)globaltimer());
+}
+
 // ---------------------------------------------------------------------------
 // Object removal: masks travel in the RGBX planes' spare
 // byte (bit 24), so every removal and transpose kernel carries them for free.

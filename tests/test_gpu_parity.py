@@ -305,3 +305,30 @@ def test_every_dp_variant_bitexact(port, monkeypatch, variant):
     outs = cv.carve_batch(imgs, 480, 70)
     assert np.array_equal(outs[0], want)
     assert np.array_equal(outs[1], port.carve(imgs[1], 480, 70))
+
+
+def _right_heavy_image(w, h):
+    # grey ramp flattening towards the right edge: the last column has the least energy,
+    # so seams run down column W-1 (the removal's "nothing moves" case, incl. W-1 = 0 mod 4)
+    j = np.arange(w, dtype=np.float64)
+    v = np.clip(np.round(255.0 - 0.25 * (w - 1 - j) ** 2), 0, 255).astype(np.uint8)
+    return np.repeat(np.repeat(v[None, :, None], h, axis=0), 3, axis=2).copy()
+
+
+@pytest.mark.parametrize("w", [33, 34, 35, 36, 37, 65])
+def test_fused_removal_last_column_seams(port, monkeypatch, w):
+    """Seams in the last column keep the RGBX replica column right (the fused DP and the
+    forward costs read it); W=33 removes column W-1 with W-1 = 0 mod 4 on the first seam."""
+    monkeypatch.setenv("CARVE_FUSED", "1")
+    img = _right_heavy_image(w, 12)
+    tw = w - 6
+    want, want_seams = port.carve(img, tw, 12, seams=True)
+    if w == 33:
+        assert (want_seams.reshape(-1, 12) == np.arange(w - 1, tw - 1, -1)[:, None]).all()
+    outs = cv.carve_batch([img, img[::-1].copy()], tw, 12)
+    assert np.array_equal(outs[0], want)
+    assert np.array_equal(outs[1], port.carve(img[::-1].copy(), tw, 12))
+    out, seams, _ = cv.carve(img, tw, 12, seams=True, forward=True)
+    fout, fseams = port.carve_cfg(img, tw, 12, forward=True, seams=True)
+    assert np.array_equal(out, fout)
+    assert np.array_equal(np.concatenate(seams), fseams)

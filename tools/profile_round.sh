@@ -13,7 +13,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 for k in k_dp2 k_compact_warp k_energy_rows; do
   ncu --set full --clock-control none --import-source on -k regex:$k -s 4 -c 1 -o gpurun_out/full_$k $B > gpurun_out/ncu_full_$k.log 2>&1 || true
 done
-for k in k_dp2 k_compact_rows; do
+for k in k_dp2 k_compact_bulk; do
   ncu --set full --clock-control none --import-source on -k regex:$k -s 20 -c 1 -o gpurun_out/full_batch_$k \
       python tools/sweep_batch.py --child 1024 > gpurun_out/ncu_full_batch_$k.log 2>&1 || true
 done
