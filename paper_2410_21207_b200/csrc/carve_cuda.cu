@@ -159,6 +159,9 @@ thread_local std::map<int, std::unique_ptr<Ctx>> t_ctx;
 
 void init_kernel_attributes(Ctx& c);  // defined after the kernel tables
 
+// shared memory for the bulk removal's row slots (RGBX + optional FP64 part per slot)
+constexpr size_t kCompactBulkSmem = 200 * 1024;
+
 enum KernelKind { KK_ENERGY = 0, KK_DP = 1, KK_COMPACT = 2, KK_UNPACK = 3, KK_PACK = 4, KK_TRANSPOSE = 5, KK_N = 6 };
 
 // RAII bracket: records an event pair around one launch when profiling is on
@@ -319,7 +322,9 @@ const std::vector<Dp2Variant>& dp2_variants() {
 #define kDp2Variants dp2_variants()
 
 void init_kernel_attributes(Ctx& c) {
-    ck(cudaFuncSetAttribute(k_compact_bulk<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024),
+    ck(cudaFuncSetAttribute(k_compact_bulk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCompactBulkSmem)),
+       "cudaFuncSetAttribute(k_compact_bulk)");
+    ck(cudaFuncSetAttribute(k_compact_bulk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCompactBulkSmem)),
        "cudaFuncSetAttribute(k_compact_bulk)");
     for (const Dp2Variant& v : kDp2Variants)
         for (const void* fn :
@@ -422,6 +427,22 @@ void launch_dp2(Ctx& c, const Dp2Plan& pl, Dp2Params p, int nimg, cudaStream_t s
     LAUNCHED("k_dp2");
 }
 
+template <bool HAS_E>
+void launch_compact_bulk(cudaLaunchConfig_t cfg, const CompactParams& p, int nimg, int rpc) {
+    const int slot_words = int(round_up(size_t(p.W) + 4, 32));
+    const size_t slot_bytes = size_t(slot_words) * (HAS_E ? 12 : 4);
+    // up to 4 rows in flight per CTA while two CTAs still fit per SM (C3's 3840-wide rows:
+    // 2 slots; C4's 7680-wide rows: 2 slots, one CTA per SM)
+    int slots = int(std::min<size_t>(CB_MAX_SLOTS, std::max<size_t>(2, (kCompactBulkSmem / 2) / slot_bytes)));
+    slots = int(std::min<size_t>(size_t(slots), kCompactBulkSmem / slot_bytes));
+    if (slots < 1) fail(CARVE_E_IMAGE_TOO_LARGE, "row too wide for the bulk removal kernel");
+    cfg.gridDim = dim3((p.H + rpc - 1) / rpc, nimg);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = size_t(slots) * slot_bytes;
+    ck(cudaLaunchKernelEx(&cfg, k_compact_bulk<HAS_E>, p, rpc, slot_words, slots), "launch k_compact_bulk");
+    LAUNCHED("k_compact_bulk");
+}
+
 void launch_compact_inplace(const CompactParams& p, int nimg, cudaStream_t s) {
     if (env_int("CARVE_COMPACT", 2) == 2) {  // warp per row (default); 1 = CTA per row
         // warps per CTA: small CTAs spread few rows over all SMs (single images)
@@ -436,21 +457,21 @@ void launch_compact_inplace(const CompactParams& p, int nimg, cudaStream_t s) {
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = pdl_enabled() ? 1 : 0;
+        if (p.e_out && env_int("CARVE_COMPACT_BULK", 1) != 0) {
+            // rows per CTA: about two CTAs per SM over the job (C2 1080 rows: 4 -> 10.6 us;
+            // C4 4320 rows: 15 -> 72.7 us, was 84.6 with the warp-per-row kernel)
+            static const int nsm = device_sm_count();
+            const int rpc_auto = std::max(2, std::min(16, int((p.H * (long long)nimg + 2 * nsm - 1) / (2 * nsm))));
+            launch_compact_bulk<true>(cfg, p, nimg, env_int("CARVE_COMPACT_RPC_E", rpc_auto));
+            return;
+        }
         if (p.e_out) {
             if (nb == 8) ck(cudaLaunchKernelEx(&cfg, k_compact_warp<8, true>, p), "launch k_compact_warp");
             else if (nb == 2) ck(cudaLaunchKernelEx(&cfg, k_compact_warp<2, true>, p), "launch k_compact_warp");
             else ck(cudaLaunchKernelEx(&cfg, k_compact_warp<4, true>, p), "launch k_compact_warp");
-        } else if (p.rgb_edges && env_int("CARVE_COMPACT_BULK", 1) != 0 && p.W <= 8192) {
-            // batches: TMA bulk loads of each row's moving part, SLOTS rows in flight per CTA
-            constexpr int SLOTS = 4;
-            const int rpc = env_int("CARVE_COMPACT_RPC", 8);  // rows per CTA (C5: 8 0.541, 16 0.554, 32 0.549 ms)
-            const int slot_words = int(round_up(size_t(p.W) + 4, 32));
-            cudaLaunchConfig_t bc = cfg;
-            bc.gridDim = dim3((p.H + rpc - 1) / rpc, nimg);
-            bc.blockDim = dim3(128);
-            bc.dynamicSmemBytes = size_t(SLOTS) * slot_words * 4;
-            ck(cudaLaunchKernelEx(&bc, k_compact_bulk<SLOTS>, p, rpc, slot_words), "launch k_compact_bulk");
-            LAUNCHED("k_compact_bulk");
+        } else if (p.rgb_edges && env_int("CARVE_COMPACT_BULK", 1) != 0) {
+            // batches: TMA bulk loads of each row's moving part, 4 rows in flight per CTA
+            launch_compact_bulk<false>(cfg, p, nimg, env_int("CARVE_COMPACT_RPC", 8));  // C5: 8 0.541, 16 0.554 ms
             return;
         } else if (p.rgb_edges) {  // batches: R rows per warp
             const int R = env_int("CARVE_COMPACT_ROWS", 2);  // measured: R=2 0.712, 1 0.730, 4 0.954 ms per seam (C5)

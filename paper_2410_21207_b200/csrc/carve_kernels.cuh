@@ -821,20 +821,27 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
 }
-template <int SLOTS>
-__global__ void __launch_bounds__(128) k_compact_bulk(CompactParams p, int rows_per_cta, int slot_words) {
+// HAS_E: the FP64 energy plane moves too (single images; its vacated column becomes
+// the +inf pad) and the replica columns are left alone; without it (batches, fused DP)
+// the RGBX replica columns -1 / W-1 are refreshed. Shared memory per slot: the RGBX
+// part (slot_words) then, with HAS_E, the energy part (slot_words doubles).
+constexpr int CB_MAX_SLOTS = 4;
+template <bool HAS_E>
+__global__ void __launch_bounds__(128) k_compact_bulk(CompactParams p, int rows_per_cta, int slot_words, int slots) {
     extern __shared__ __align__(128) uint32_t cb_sm[];
-    __shared__ __align__(8) uint64_t cb_bar[SLOTS];
+    __shared__ __align__(8) uint64_t cb_bar[CB_MAX_SLOTS];
     const int img = blockIdx.y;
     const int row0 = blockIdx.x * rows_per_cta;
     const int nrows = min(rows_per_cta, p.H - row0);
     const int W = p.W, Wn = W - 1;
     const int* seam = p.seam + img * p.s_istride + row0;
     uint32_t* plane = p.rgb_out + img * p.p_istride + (long long)row0 * p.pitch;
+    double* eplane = HAS_E ? p.e_out + img * p.e_istride + (long long)row0 * p.epitch : nullptr;
+    const int slot_bytes = slot_words * (HAS_E ? 12 : 4);
     const uint32_t bar0 = uint32_t(__cvta_generic_to_shared(cb_bar));
     const uint32_t sm0 = uint32_t(__cvta_generic_to_shared(cb_sm));
     if (threadIdx.x == 0) {
-        for (int k = 0; k < SLOTS; ++k)
+        for (int k = 0; k < slots; ++k)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * k) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -844,19 +851,22 @@ __global__ void __launch_bounds__(128) k_compact_bulk(CompactParams p, int rows_
     if (p.stamps && blockIdx.x == 0 && threadIdx.x == 0)
         atomicCAS(&p.stamps[img * p.st_istride + 0], 0ull, (unsigned long long)globaltimer());
     // row r's moving part: 16-byte aligned from a = floor4(s) to W (rounded up to 4 pixels;
-    // the plane pitch covers the overhang)
+    // the padded pitches cover the overhang)
     auto issue = [&](int r) {
         const int a = __ldg(seam + r) & ~3;
-        const uint32_t bytes = uint32_t(((W - a + 3) & ~3) * 4);
-        const uint32_t b = bar0 + 8 * (r % SLOTS);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
-        bulk_g2s(sm0 + uint32_t((r % SLOTS) * slot_words * 4), plane + (long long)r * p.pitch + a, bytes, b);
+        const uint32_t n4 = uint32_t((W - a + 3) & ~3);
+        const uint32_t b = bar0 + 8 * (r % slots);
+        const uint32_t dst = sm0 + uint32_t((r % slots) * slot_bytes);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(n4 * (HAS_E ? 12 : 4))
+                     : "memory");
+        bulk_g2s(dst, plane + (long long)r * p.pitch + a, n4 * 4, b);
+        if constexpr (HAS_E) bulk_g2s(dst + uint32_t(slot_words * 4), eplane + (long long)r * p.epitch + a, n4 * 8, b);
     };
     if (threadIdx.x == 0)
-        for (int r = 0; r < min(SLOTS, nrows); ++r) issue(r);
+        for (int r = 0; r < min(slots, nrows); ++r) issue(r);
     for (int r = 0; r < nrows; ++r) {
-        const int k = r % SLOTS;
-        const uint32_t parity = uint32_t(r / SLOTS) & 1u;
+        const int k = r % slots;
+        const uint32_t parity = uint32_t(r / slots) & 1u;
         uint32_t ok = 0;
         while (!ok)
             asm volatile("{ .reg .pred q; mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2; selp.u32 %0, 1, 0, q; }"
@@ -864,29 +874,48 @@ __global__ void __launch_bounds__(128) k_compact_bulk(CompactParams p, int rows_
                          : "r"(bar0 + 8 * k), "r"(parity)
                          : "memory");
         const int s = __ldg(seam + r), a = s & ~3;
-        const uint32_t* src = cb_sm + k * slot_words - a;  // src[j] = old pixel j, j in [a, W)
+        const unsigned char* slot = reinterpret_cast<const unsigned char*>(cb_sm) + size_t(k) * slot_bytes;
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(slot) - a;  // src[j] = old pixel j, j in [a, W)
+        const double* esrc = reinterpret_cast<const double*>(slot + slot_words * 4) - a;
         uint32_t* row = plane + (long long)r * p.pitch;
+        double* erow = HAS_E ? eplane + (long long)r * p.epitch : nullptr;
         for (int c = a + 4 * int(threadIdx.x); c < Wn; c += 4 * int(blockDim.x)) {
             uint32_t o[4];
+            double oe[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) o[u] = src[c + u + (c + u >= s ? 1 : 0)];
+            for (int u = 0; u < 4; ++u) {
+                o[u] = src[c + u + (c + u >= s ? 1 : 0)];
+                if constexpr (HAS_E) oe[u] = esrc[c + u + (c + u >= s ? 1 : 0)];
+            }
             if (c + 4 <= Wn) {
                 *reinterpret_cast<uint4*>(row + c) = make_uint4(o[0], o[1], o[2], o[3]);
+                if constexpr (HAS_E) {
+                    *reinterpret_cast<double2*>(erow + c) = make_double2(oe[0], oe[1]);
+                    *reinterpret_cast<double2*>(erow + c + 2) = make_double2(oe[2], oe[3]);
+                }
             } else {
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
-                    if (c + u < Wn) row[c + u] = o[u];
+                    if (c + u < Wn) {
+                        row[c + u] = o[u];
+                        if constexpr (HAS_E) erow[c + u] = oe[u];
+                    }
             }
-            if (c == 0 && s == 0) row[-1] = o[0];  // replica columns (raster.hpp:54-58 clamping)
+            if constexpr (!HAS_E) {
+                if (c == 0 && s == 0) row[-1] = o[0];  // replica columns (raster.hpp:54-58 clamping)
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (c + u == Wn - 1) row[Wn] = o[u];
+                for (int u = 0; u < 4; ++u)
+                    if (c + u == Wn - 1) row[Wn] = o[u];
+            }
         }
-        // the seam is in the row's last 4-pixel chunk past Wn-1: nothing moves, only the right
-        // replica follows column Wn-1 (unchanged in global memory, before the loaded part)
-        if (threadIdx.x == 0 && a >= Wn) row[Wn] = row[Wn - 1];
+        if (threadIdx.x == 0) {
+            if constexpr (HAS_E) erow[Wn] = dinf();  // the vacated column joins the +inf pad
+            // the seam is in the row's last 4-pixel chunk past Wn-1: nothing moves, only the right
+            // replica follows column Wn-1 (unchanged in global memory, before the loaded part)
+            else if (a >= Wn) row[Wn] = row[Wn - 1];
+        }
         __syncthreads();  // every thread is done with slot k
-        if (threadIdx.x == 0 && r + SLOTS < nrows) issue(r + SLOTS);
+        if (threadIdx.x == 0 && r + slots < nrows) issue(r + slots);
     }
     if (p.stamps && threadIdx.x == 0) atomicMax(&p.stamps[img * p.st_istride + 1], (unsigned long long)globaltimer());
 }
