@@ -691,7 +691,8 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
         cluster.map_shared_rank(cl_v, 0)[cta] = bv;
         cluster.map_shared_rank(cl_i, 0)[cta] = bi;
     }
-    __threadfence();
+    // the cluster barrier (arrive.release / wait.acquire at cluster scope) orders these
+    // DSMEM stores and phase 1's seam stores below; no gpu-scope fence is needed
     if (ncl > 1) cluster.sync();
     else __syncthreads();
 
@@ -716,7 +717,6 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
             }
         }
         if (nblk > 0) seam[0] = c;
-        __threadfence();
     }
     // after this barrier no CTA touches another CTA's shared memory, so CTAs
     // may finish phase 2 and exit independently
