@@ -4,7 +4,7 @@
 //       + 2-column fix-up     prologue of k_dp2
 //   K2  cumulative-energy DP  k_dp2 (dp_cluster.cuh) (solvers.hpp:116-157, 263-289)
 //   K3  argmin + backtrack    tail of k_dp2 (solvers.hpp:94-111)
-//   K4  seam removal          k_compact_inplace (carve loop), k_compact (the
+//   K4  seam removal          k_compact_bulk (carve loop, TMA), k_compact (the
 //                             remove_seam API) (carver.hpp:71-98); transpose
 //                             kernels for horizontal seams (carver.hpp:216-222)
 //
