@@ -1443,6 +1443,7 @@ carve_status carve_cuda_carve_batch_device(const uint8_t* d_rgb, int n, int w, i
 // images per pipelined chunk (measured: 256-image launches run at ~95% of the
 // 1024-image throughput, tools/sweep_batch.py)
 constexpr int kPipeChunk = 256;
+constexpr int CARVE_MAX_PIPELINES = 4;
 
 carve_status carve_cuda_carve_batch(const uint8_t* const* rgb, int n, int w, int h, int target_w, int target_h,
                                     uint8_t* const* rgb_out, const int* devices, int ndev) {
@@ -1537,20 +1538,28 @@ carve_status carve_cuda_carve_batch(const uint8_t* const* rgb, int n, int w, int
             });
             if (st_out) msg_out = t_err;
         };
-        const int pipes = env_int("CARVE_PIPELINES", 2);
-        std::vector<int> st2(ndev, CARVE_OK);
-        std::vector<std::string> msg2(ndev);
+        const int pipes = std::max(1, std::min(CARVE_MAX_PIPELINES, env_int("CARVE_PIPELINES", 2)));
+        std::vector<std::vector<int>> pst(ndev, std::vector<int>(CARVE_MAX_PIPELINES, CARVE_OK));
+        std::vector<std::vector<std::string>> pmsg(ndev, std::vector<std::string>(CARVE_MAX_PIPELINES));
         auto device_worker = [&](int k) {
             const int lo = int((long long)n * k / ndev), hi = int((long long)n * (k + 1) / ndev);
-            if (pipes > 1 && hi - lo >= 4 * kPipeChunk && chunk_cap >= kPipeChunk) {
-                const int mid = lo + ((hi - lo) / 2 + kPipeChunk - 1) / kPipeChunk * kPipeChunk;
-                std::thread second([&, k, mid, hi] { worker(k, 1, mid, hi, st2[k], msg2[k]); });
-                worker(k, 0, lo, mid, status[k], msgs[k]);
-                second.join();
-                if (!status[k] && st2[k]) {
-                    status[k] = st2[k];
-                    msgs[k] = msg2[k];
+            // P pipelines on chunk-aligned parts of the share, each needing >= 2 chunks
+            const int nchunks = (hi - lo + kPipeChunk - 1) / kPipeChunk;
+            const int P = (chunk_cap >= kPipeChunk) ? std::max(1, std::min(pipes, nchunks / 2)) : 1;
+            if (P > 1) {
+                std::vector<std::thread> th;
+                for (int q = 1; q < P; ++q) {
+                    const int a = lo + int((long long)nchunks * q / P) * kPipeChunk;
+                    const int b = std::min(hi, lo + int((long long)nchunks * (q + 1) / P) * kPipeChunk);
+                    th.emplace_back([&, k, q, a, b] { worker(k, q, a, b, pst[k][q], pmsg[k][q]); });
                 }
+                worker(k, 0, lo, std::min(hi, lo + int((long long)nchunks / P) * kPipeChunk), status[k], msgs[k]);
+                for (auto& t : th) t.join();
+                for (int q = 1; q < P && !status[k]; ++q)
+                    if (pst[k][q]) {
+                        status[k] = pst[k][q];
+                        msgs[k] = pmsg[k][q];
+                    }
             } else {
                 worker(k, 0, lo, hi, status[k], msgs[k]);
             }

@@ -726,6 +726,7 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
     long long pf_p1 = 0;
     if constexpr (PROF) pf_p1 = clock64();
     // ---- K3b phase 2: every warp recomputes blocks g, g+G, ... in a 128-column window
+    long long q0t = 0, q1t = 0, q2t = 0, q3t = 0;  // MODE 2: the first block's sub-phases
     {
         uint8_t* dirs = p2 + size_t(warp) * LBLK * P2_COLS;
         // phase-2 ring: this warp's forward-ring region, P2D rows of 128 columns
@@ -735,6 +736,7 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
         const unsigned char* p2ring_ptr = ring_b + size_t(warp) * D * 32 * C * RE + lane * 4 * RE;
         const uint32_t p2ring = smem_u32(p2ring_ptr);
         for (int b = g; b < nblk && !(p.dbg & 1); b += G) {
+            if constexpr (PROF) { if (b == g) q0t = clock64(); }
             const int r0 = 1 + LBLK * b, r1 = min(LBLK * (b + 1), H - 1);
             const int c1 = __ldcg(seam + r1);  // phase 1 left the block's bottom column in global memory
             // 16-byte aligned lane slices: even column for double2 energies, multiple of 4 for RGBX
@@ -788,6 +790,7 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
             for (int r = r0; r <= r1; ++r) {
                 const int slot = (r - r0) % P2D;
                 cp_async_wait<P2D - 1>();
+                if constexpr (PROF) { if (b == g && r == r0) { asm volatile("" ::"d"(mm[0])); q1t = clock64(); } }
                 double ec[4], qcl[4], qcu[4], qcr[4];
                 if constexpr (FUSED) {
                     const uint4 q = *reinterpret_cast<const uint4*>(p2ring_ptr + slot * P2STAGE);
@@ -830,6 +833,7 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
             }
             cp_async_wait<0>();
             __syncwarp();
+            if constexpr (PROF) { if (b == g) q2t = clock64(); }
             if (lane == 0 && !(p.dbg & 4)) {
                 int c = c1;
                 for (int r = r1; r >= r0; --r) {
@@ -838,6 +842,7 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
                 }
             }
             __syncwarp();
+            if constexpr (PROF) { if (b == g) q3t = clock64(); }
         }
     }
     if constexpr (PROF) {
@@ -848,6 +853,9 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
             o[2] = pf_p1 - pf_fwd;   // argmin + phase 1 + barriers
             o[3] = clock64() - pf_p1;  // phase 2
             o[4] = H;
+            o[5] = q1t - q0t;  // first phase-2 block: start -> first row's data ready
+            o[6] = q2t - q1t;  //   row recompute
+            o[7] = q3t - q2t;  //   walk
         }
     }
     if (p.stamps) {

@@ -16,3 +16,7 @@ print(f"variant={os.environ.get('CARVE_DP_VARIANT')} W={W} H={H} warps={G}")
 print(" fwd cycles/row   mean %.1f  min %.1f  max %.1f" % ((a[:, 0] / H).mean(), (a[:, 0] / H).min(), (a[:, 0] / H).max()))
 print(" wait cycles/row  mean %.1f  min %.1f  max %.1f" % ((a[:, 1] / H).mean(), (a[:, 1] / H).min(), (a[:, 1] / H).max()))
 print(" argmin+p1 cycles mean %.0f, phase2 cycles mean %.0f max %.0f" % (a[:, 2].mean(), a[:, 3].mean(), a[:, 3].max()))
+w = a[:, 5] > 0
+if w.any():
+    print(" phase2 first block: start->data %.0f, rows %.0f, walk %.0f cycles (mean over %d warps)" %
+          (a[w, 5].mean(), a[w, 6].mean(), a[w, 7].mean(), int(w.sum())))
