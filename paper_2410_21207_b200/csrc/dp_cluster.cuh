@@ -787,8 +787,7 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
             };
 #pragma unroll
             for (int u = 0; u < P2D; ++u) p2fetch(r0 + u, u);
-            for (int r = r0; r <= r1; ++r) {
-                const int slot = (r - r0) % P2D;
+            auto p2row = [&](int r, int slot) {
                 cp_async_wait<P2D - 1>();
                 if constexpr (PROF) { if (b == g && r == r0) { asm volatile("" ::"d"(mm[0])); q1t = clock64(); } }
                 double ec[4], qcl[4], qcu[4], qcr[4];
@@ -813,7 +812,7 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
                         for (int k = 0; k < 4; ++k) QLp[k] = QLc[k];
                     }
                 }
-                p2fetch(r + P2D, slot);
+                if (!(PROF && (p.dbg & 16))) p2fetch(r + P2D, slot);  // dbg bit 4 (MODE 2): timing without refills
                 const double lm = __shfl_up_sync(FULL, mm[3], 1);
                 const double rm = __shfl_down_sync(FULL, mm[0], 1);
                 double pm = lane == 0 ? dinf() : lm;
@@ -824,12 +823,25 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
                     const double cm = mm[k];
                     const double nm = (k + 1 < 4) ? mm[k + 1] : rr;
                     int d, dummy;
-                    if constexpr (FWD) fwd_cell(pm, cm, nm, 0, 0, 0, qcl[k], qcu[k], qcr[k], mm[k], dummy, d);
-                    else dp_cell(pm, cm, nm, 0, 0, 0, ec[k], mm[k], dummy, d);
+                    // k = 0: the shuffled left operand is compared last (same cell, see
+                    // dp_cell_left_last), so one compare-select follows the shuffle
+                    if constexpr (FWD) {
+                        if (k == 0) fwd_cell_left_last(pm, cm, nm, 0, 0, 0, qcl[k], qcu[k], qcr[k], mm[k], dummy, d);
+                        else fwd_cell(pm, cm, nm, 0, 0, 0, qcl[k], qcu[k], qcr[k], mm[k], dummy, d);
+                    } else {
+                        if (k == 0) dp_cell_left_last(pm, cm, nm, 0, 0, 0, ec[k], mm[k], dummy, d);
+                        else dp_cell(pm, cm, nm, 0, 0, 0, ec[k], mm[k], dummy, d);
+                    }
                     db |= uint32_t(d) << (8 * k);
                     pm = cm;
                 }
                 reinterpret_cast<uint32_t*>(dirs + (r - r0) * P2_COLS)[lane] = db;
+            };
+            if (r1 - r0 + 1 == LBLK) {  // full block: unrolled, ring slots are compile-time
+#pragma unroll
+                for (int t = 0; t < LBLK; ++t) p2row(r0 + t, t % P2D);
+            } else {
+                for (int r = r0; r <= r1; ++r) p2row(r, (r - r0) % P2D);
             }
             cp_async_wait<0>();
             __syncwarp();
