@@ -787,10 +787,9 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
             };
 #pragma unroll
             for (int u = 0; u < P2D; ++u) p2fetch(r0 + u, u);
-            auto p2row = [&](int r, int slot) {
-                cp_async_wait<P2D - 1>();
-                if constexpr (PROF) { if (b == g && r == r0) { asm volatile("" ::"d"(mm[0])); q1t = clock64(); } }
-                double ec[4], qcl[4], qcu[4], qcr[4];
+            // one ring row -> this lane's 4 energies (or forward costs); rows in order (the
+            // fused luma rows roll)
+            auto p2load = [&](int slot, double (&ec)[4], double (&qcl)[4], double (&qcu)[4], double (&qcr)[4]) {
                 if constexpr (FUSED) {
                     const uint4 q = *reinterpret_cast<const uint4*>(p2ring_ptr + slot * P2STAGE);
                     const uint32_t px[4] = {q.x, q.y, q.z, q.w};
@@ -812,7 +811,15 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
                         for (int k = 0; k < 4; ++k) QLp[k] = QLc[k];
                     }
                 }
-                if (!(PROF && (p.dbg & 16))) p2fetch(r + P2D, slot);  // dbg bit 4 (MODE 2): timing without refills
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {  // the slot's values are in registers before its refill
+                    if constexpr (FWD) asm volatile("" ::"d"(qcl[k]), "d"(qcu[k]), "d"(qcr[k]));
+                    else asm volatile("" ::"d"(ec[k]));
+                }
+            };
+            // row r's cells from the previous row (mm) and its energies / costs
+            auto p2cells = [&](int r, const double (&ec)[4], const double (&qcl)[4], const double (&qcu)[4],
+                               const double (&qcr)[4]) {
                 const double lm = __shfl_up_sync(FULL, mm[3], 1);
                 const double rm = __shfl_down_sync(FULL, mm[0], 1);
                 double pm = lane == 0 ? dinf() : lm;
@@ -837,11 +844,37 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
                 }
                 reinterpret_cast<uint32_t*>(dirs + (r - r0) * P2_COLS)[lane] = db;
             };
-            if (r1 - r0 + 1 == LBLK) {  // full block: unrolled, ring slots are compile-time
+            const bool refill = !(PROF && (p.dbg & 16));  // dbg bit 4 (MODE 2): timing without refills
+            if (r1 - r0 + 1 == LBLK) {
+                // full block: unrolled (compile-time ring slots) and software-pipelined — row
+                // t+1's ring read (and fused luma/e1) is issued before row t's cells, so the
+                // shared-memory latency stays off the row-to-row chain
+                double ea[4], la[4], ua[4], ra[4];
+                cp_async_wait<P2D - 1>();
+                p2load(0, ea, la, ua, ra);
+                if constexpr (PROF) { if (b == g) { asm volatile("" ::"d"(mm[0])); q1t = clock64(); } }
 #pragma unroll
-                for (int t = 0; t < LBLK; ++t) p2row(r0 + t, t % P2D);
+                for (int t = 0; t < LBLK; ++t) {
+                    double eb[4], lb[4], ub[4], rb[4];
+                    if (t + 1 < LBLK) {
+                        cp_async_wait<P2D - 2>();
+                        p2load((t + 1) % P2D, eb, lb, ub, rb);
+                    }
+                    if (refill) p2fetch(r0 + t + P2D, t % P2D);
+                    p2cells(r0 + t, ea, la, ua, ra);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) { ea[k] = eb[k]; la[k] = lb[k]; ua[k] = ub[k]; ra[k] = rb[k]; }
+                }
             } else {
-                for (int r = r0; r <= r1; ++r) p2row(r, (r - r0) % P2D);
+                for (int r = r0; r <= r1; ++r) {
+                    const int slot = (r - r0) % P2D;
+                    double ec[4], qcl[4], qcu[4], qcr[4];
+                    cp_async_wait<P2D - 1>();
+                    p2load(slot, ec, qcl, qcu, qcr);
+                    if constexpr (PROF) { if (b == g && r == r0) { asm volatile("" ::"d"(mm[0])); q1t = clock64(); } }
+                    if (refill) p2fetch(r + P2D, slot);
+                    p2cells(r, ec, qcl, qcu, qcr);
+                }
             }
             cp_async_wait<0>();
             __syncwarp();
