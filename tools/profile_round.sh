@@ -10,7 +10,7 @@ B="python bench.py --steps 2 --warmup 3 --no-batch --no-cpu-baseline"
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c2.csv $B > gpurun_out/ncu_launches.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c5.csv \
     python bench.py --config c5 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launches_c5.log 2>&1 || true
-for k in k_dp2 k_compact_warp k_energy_rows; do
+for k in k_dp2 k_compact_bulk k_energy_rows; do
   ncu --set full --clock-control none --import-source on -k regex:$k -s 4 -c 1 -o gpurun_out/full_$k $B > gpurun_out/ncu_full_$k.log 2>&1 || true
 done
 for k in k_dp2 k_compact_bulk; do
