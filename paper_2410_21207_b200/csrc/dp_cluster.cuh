@@ -204,6 +204,22 @@ __device__ __forceinline__ void st_async_b32(uint32_t raddr, uint32_t v, uint32_
                  : "memory");
 }
 
+// predicated vector forms (one role per lane, no branch in the exchange)
+__device__ __forceinline__ void st_async_v2_b64_if(bool pr, uint32_t raddr, double a, double b, uint32_t rmbar) {
+    asm volatile(
+        "{ .reg .pred p; setp.ne.u32 p, %4, 0;\n"
+        "@p st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3]; }" ::"r"(raddr),
+        "l"(__double_as_longlong(a)), "l"(__double_as_longlong(b)), "r"(rmbar), "r"(uint32_t(pr))
+        : "memory");
+}
+__device__ __forceinline__ void st_async_v2_b32_if(bool pr, uint32_t raddr, uint32_t a, uint32_t b, uint32_t rmbar) {
+    asm volatile(
+        "{ .reg .pred p; setp.ne.u32 p, %4, 0;\n"
+        "@p st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3]; }" ::"r"(raddr),
+        "r"(a), "r"(b), "r"(rmbar), "r"(uint32_t(pr))
+        : "memory");
+}
+
 // ---- energy-row ring: per-lane cp.async (LDGSTS) into shared memory ----------
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
@@ -558,27 +574,26 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
     const int* rLl = my_l + wi0;
     const double* rRm = my_m + K + (wi0 - (32 * C - K));  // side 1
     const int* rRl = my_l + K + (wi0 - (32 * C - K));
+    // A lane sends to at most one side and receives from at most one side (4K <= 32C,
+    // K <= 16C), so each role is one predicated vector store / one selected load.
+    static_assert(4 * K <= 32 * C && K <= 16 * C, "exchange roles must not overlap");
+    const bool snd = sendL || sendR, rcv = recvL || recvR;
+    const uint32_t s_m = sendL ? aLm : aRm, s_l = sendL ? aLl : aRl, s_b = sendL ? nl_b : nr_b;
+    // non-receiving lanes read their own first mailbox slot (valid memory) and discard it
+    const double* r_m = recvL ? rLm : recvR ? rRm : my_m;
+    const int* r_l = recvL ? rLl : recvR ? rRl : my_l;
+    const bool r_inf = recvL ? gl < 0 : (recvR && gr >= G);  // no neighbour on that side: +inf halo
     // exchange, split in two so the block-end bookkeeping runs under the DSMEM latency:
     auto send = [&]() {
         // send my K leftmost / rightmost useful columns straight into the
         // neighbours' halo mailboxes; each store completes bytes on the
         // neighbour's mbarrier (no cluster-wide barrier, no memory fence)
         const uint32_t po8 = uint32_t(par * PSTRIDE * 8), po4 = uint32_t(par * PSTRIDE * 4);
-        if (sendL) {
-            const uint32_t mb = nl_b + par * 8;
+        const uint32_t mb = s_b + par * 8;
 #pragma unroll
-            for (int k = 0; k < C; ++k) {
-                st_async_b64(aLm + po8 + k * 8, m[k], mb);
-                st_async_b32(aLl + po4 + k * 4, uint32_t(lab[k]), mb);
-            }
-        }
-        if (sendR) {
-            const uint32_t mb = nr_b + par * 8;
-#pragma unroll
-            for (int k = 0; k < C; ++k) {
-                st_async_b64(aRm + po8 + k * 8, m[k], mb);
-                st_async_b32(aRl + po4 + k * 4, uint32_t(lab[k]), mb);
-            }
+        for (int k = 0; k < C; k += 2) {
+            st_async_v2_b64_if(snd, s_m + po8 + k * 8, m[k], m[k + 1], mb);
+            st_async_v2_b32_if(snd, s_l + po4 + k * 4, uint32_t(lab[k]), uint32_t(lab[k + 1]), mb);
         }
     };
     auto recv = [&]() {
@@ -590,19 +605,12 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
         }
         if constexpr (PROF) pf_wait += clock64() - w0;
         phases ^= 1u << par;
-        if (recvL) {
 #pragma unroll
-            for (int k = 0; k < C; ++k) {
-                m[k] = gl >= 0 ? rLm[par * PSTRIDE + k] : dinf();
-                lab[k] = rLl[par * PSTRIDE + k];
-            }
-        }
-        if (recvR) {
-#pragma unroll
-            for (int k = 0; k < C; ++k) {
-                m[k] = gr < G ? rRm[par * PSTRIDE + k] : dinf();
-                lab[k] = rRl[par * PSTRIDE + k];
-            }
+        for (int k = 0; k < C; ++k) {
+            const double vm = r_m[par * PSTRIDE + k];
+            const int vl = r_l[par * PSTRIDE + k];
+            m[k] = rcv ? (r_inf ? dinf() : vm) : m[k];
+            lab[k] = rcv ? vl : lab[k];
         }
         par ^= 1;
     };
