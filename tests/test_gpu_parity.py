@@ -297,6 +297,12 @@ def test_every_dp_variant_bitexact(port, monkeypatch, variant):
     assert np.array_equal(r.seam, seam)
     assert np.array_equal(bits(r.table.m), bits(m))
     assert np.array_equal(r.table.b, b)
+    monkeypatch.setenv("CARVE_DP_GATHER", "0")  # phase 1 over DSMEM (the tall/wide-image path)
+    r = cv.dp_seam(e)
+    assert np.array_equal(r.seam, seam)
+    tall = port.energy_e1_rgb(port.make_test_image(300, 700))
+    assert np.array_equal(cv.dp_seam(tall).seam, port.dp_seam(tall)[0])
+    monkeypatch.delenv("CARVE_DP_GATHER")
     want = port.carve(img, 480, 70)
     monkeypatch.setenv("CARVE_FUSED", "0")
     assert np.array_equal(cv.carve(img, 480, 70), want)
