@@ -605,12 +605,22 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
         }
         if constexpr (PROF) pf_wait += clock64() - w0;
         phases ^= 1u << par;
+        // every lane loads (asm volatile: the loads cannot be skipped, so no branch), the
+        // non-receiving lanes discard the values with selects
 #pragma unroll
-        for (int k = 0; k < C; ++k) {
-            const double vm = r_m[par * PSTRIDE + k];
-            const int vl = r_l[par * PSTRIDE + k];
-            m[k] = rcv ? (r_inf ? dinf() : vm) : m[k];
-            lab[k] = rcv ? vl : lab[k];
+        for (int k = 0; k < C; k += 2) {
+            double v0, v1;
+            uint32_t l0, l1;
+            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
+                         : "=d"(v0), "=d"(v1)
+                         : "r"(smem_u32(r_m + par * PSTRIDE + k)));
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
+                         : "=r"(l0), "=r"(l1)
+                         : "r"(smem_u32(r_l + par * PSTRIDE + k)));
+            m[k] = rcv ? (r_inf ? dinf() : v0) : m[k];
+            m[k + 1] = rcv ? (r_inf ? dinf() : v1) : m[k + 1];
+            lab[k] = rcv ? int(l0) : lab[k];
+            lab[k + 1] = rcv ? int(l1) : lab[k + 1];
         }
         par ^= 1;
     };
