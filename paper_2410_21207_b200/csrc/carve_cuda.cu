@@ -233,14 +233,14 @@ int grid_for(long long n, int block, int per_image_cap = 148 * 8) {
 
 void launch_unpack(Ctx& c, const uint8_t* in, int W, int H, uint32_t* out, int pitch, int nimg, long long in_is,
                    long long out_is, cudaStream_t s) {
-    dim3 grid(grid_for((long long)W * H, 256), nimg);
+    dim3 grid(grid_for(((long long)W * H + 3) / 4, 256), nimg);
     k_unpack<<<grid, 256, 0, s>>>(in, W, H, out, pitch, in_is, out_is);
     LAUNCHED("k_unpack");
 }
 
 void launch_pack(Ctx& c, const uint32_t* in, int pitch, int W, int H, bool transposed, uint8_t* out, int nimg,
                  long long in_is, long long out_is, cudaStream_t s) {
-    dim3 grid(grid_for((long long)W * H, 256), nimg);
+    dim3 grid(grid_for(((long long)W * H + 3) / 4, 256), nimg);
     if (transposed) k_pack<true><<<grid, 256, 0, s>>>(in, pitch, W, H, out, in_is, out_is);
     else k_pack<false><<<grid, 256, 0, s>>>(in, pitch, W, H, out, in_is, out_is);
     LAUNCHED("k_pack");
@@ -272,13 +272,29 @@ void launch_energy(const uint32_t* rgb, int pitch, int W, int H, double* e, int 
         ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_energy_rows<1, 2>, 256, 0), "K1 occupancy");
         return (long long)nsm * std::max(per_sm, 1) * 8;
     }();
+    // Shape: 3 CTAs/SM (80 registers) on large planes (C3 K1 0.44 -> 0.49 of HBM peak,
+    // C4 0.52 -> 0.61), 2 CTAs/SM with longer runs below 4 Mpx (C2 0.31 vs 0.22).
+    // CARVE_K1V forces one: 0 = 2 CTAs/SM, 1 = prefetch 4, 2 = 3 CTAs/SM, 3 = half runs.
+    const int k1v_env = env_int("CARVE_K1V", -1);  // read per call (tests switch it)
+    const int k1v = k1v_env >= 0 ? k1v_env : ((long long)W * H * nimg >= (4ll << 20) ? 2 : 0);
+    static const long long resident_warps2 = [] {
+        int dev = 0, nsm = 0, per_sm = 0;
+        ck(cudaGetDevice(&dev), "cudaGetDevice");
+        ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "SM count");
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_energy_rows<3, 2>, 256, 0), "K1 occupancy");
+        return (long long)nsm * std::max(per_sm, 1) * 8;
+    }();
     const int nstrips = (W + K1S_COLS - 1) / K1S_COLS;
     const long long units = (long long)nstrips * H * nimg;  // warp-rows of work
-    int R = int(std::max<long long>(4, (units + resident_warps - 1) / resident_warps));
-    R = (R + 1) & ~1;
+    const long long rw = k1v == 2 ? resident_warps2 : resident_warps;
+    int R = int(std::max<long long>(4, (units + rw - 1) / rw));
+    if (k1v == 3) R = std::max(4, R / 2);
+    R = k1v == 1 ? ((R + 3) & ~3) : ((R + 1) & ~1);
     const long long warps = (long long)nstrips * ((H + R - 1) / R);
     dim3 grid(unsigned((warps + 7) / 8), nimg);
-    k_energy_rows<1, 2><<<grid, 256, 0, s>>>(rgb, pitch, W, H, e, epitch, rgb_is, e_is, nstrips, R);
+    if (k1v == 1) k_energy_rows<1, 4><<<grid, 256, 0, s>>>(rgb, pitch, W, H, e, epitch, rgb_is, e_is, nstrips, R);
+    else if (k1v == 2) k_energy_rows<3, 2><<<grid, 256, 0, s>>>(rgb, pitch, W, H, e, epitch, rgb_is, e_is, nstrips, R);
+    else k_energy_rows<1, 2><<<grid, 256, 0, s>>>(rgb, pitch, W, H, e, epitch, rgb_is, e_is, nstrips, R);
     LAUNCHED("k_energy_rows");
 }
 
@@ -1441,8 +1457,11 @@ carve_status carve_cuda_carve_batch_device(const uint8_t* d_rgb, int n, int w, i
 }
 
 // images per pipelined chunk (measured: 256-image launches run at ~95% of the
-// 1024-image throughput, tools/sweep_batch.py)
-constexpr int kPipeChunk = 256;
+// 1024-image throughput, tools/sweep_batch.py); CARVE_PIPE_CHUNK overrides
+int pipe_chunk() {
+    static const int v = std::max(16, env_int("CARVE_PIPE_CHUNK", 256));
+    return v;
+}
 constexpr int CARVE_MAX_PIPELINES = 4;
 
 carve_status carve_cuda_carve_batch(const uint8_t* const* rgb, int n, int w, int h, int target_w, int target_h,
@@ -1459,6 +1478,7 @@ carve_status carve_cuda_carve_batch(const uint8_t* const* rgb, int n, int w, int
             if (devs[k] < 0 || devs[k] >= avail) fail(CARVE_E_CUDA, "invalid device index");
         }
         const CarveGeometry g = geometry(w, h, target_w, target_h);
+        const int kPipeChunk = pipe_chunk();
         const size_t in_bytes = size_t(w) * h * 3, out_bytes = size_t(target_w) * target_h * 3;
         // per-image device footprint -> chunk size (keep well inside 180 GB HBM)
         const size_t per_img = g.plane * 8 + g.eplane * 8 + size_t(g.mb_istride) * 8 + in_bytes + out_bytes +

@@ -74,15 +74,47 @@ __device__ __forceinline__ double e1(double l_left, double l_right, double l_up,
 // ---------------------------------------------------------------------------
 // layout conversion (host boundary): packed RGB bytes <-> RGBX plane
 
+// Both conversions move 4 pixels per thread: 12 packed bytes as three 32-bit
+// words (when the image base is 4-byte aligned) and the 4 RGBX words as one
+// 128-bit access when the group stays inside one plane row; one 32-bit divide
+// per group places it. Groups that straddle a row or the image end go per pixel.
+__device__ __forceinline__ void rgb12_to_px(uint32_t a, uint32_t b, uint32_t c, uint32_t (&px)[4]) {
+    px[0] = a & 0xFFFFFFu;
+    px[1] = (a >> 24) | ((b & 0xFFFFu) << 8);
+    px[2] = (b >> 16) | ((c & 0xFFu) << 16);
+    px[3] = c >> 8;
+}
+
 __global__ void k_unpack(const uint8_t* __restrict__ in, int W, int H, uint32_t* __restrict__ out, int pitch,
                          long long in_istride, long long out_istride) {
     in += blockIdx.y * in_istride;
     out += blockIdx.y * out_istride;
-    const long long n = (long long)W * H;
-    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
-        const int i = int(k / W), j = int(k - (long long)i * W);
-        const uint8_t* p = in + 3 * k;
-        out[(long long)i * pitch + j] = uint32_t(p[0]) | (uint32_t(p[1]) << 8) | (uint32_t(p[2]) << 16);
+    const unsigned n = unsigned(W) * unsigned(H), ng = (n + 3) / 4;
+    const bool in_al = (reinterpret_cast<uintptr_t>(in) & 3) == 0;
+    for (unsigned g = blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += gridDim.x * blockDim.x) {
+        const unsigned k = 4 * g, i = k / unsigned(W), j = k - i * unsigned(W);
+        uint32_t px[4];
+        if (in_al && k + 3 < n) {
+            const uint32_t* w3 = reinterpret_cast<const uint32_t*>(in + 3ull * k);
+            rgb12_to_px(w3[0], w3[1], w3[2], px);
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint8_t* p = in + 3ull * min(k + u, n - 1);
+                px[u] = uint32_t(p[0]) | (uint32_t(p[1]) << 8) | (uint32_t(p[2]) << 16);
+            }
+        }
+        uint32_t* o = out + (size_t)i * pitch + j;
+        if (j + 3 < unsigned(W) && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+            *reinterpret_cast<uint4*>(o) = make_uint4(px[0], px[1], px[2], px[3]);
+        } else {
+            unsigned ii = i, jj = j;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (k + u < n) out[(size_t)ii * pitch + jj] = px[u];
+                if (++jj == unsigned(W)) { jj = 0; ++ii; }
+            }
+        }
     }
 }
 
@@ -92,14 +124,39 @@ __global__ void k_pack(const uint32_t* __restrict__ in, int pitch, int W, int H,
                        long long in_istride, long long out_istride) {
     in += blockIdx.y * in_istride;
     out += blockIdx.y * out_istride;
-    const long long n = (long long)W * H;
-    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
-        const int i = int(k / W), j = int(k - (long long)i * W);
-        const uint32_t p = transposed ? in[(long long)j * pitch + i] : in[(long long)i * pitch + j];
-        uint8_t* o = out + 3 * k;
-        o[0] = uint8_t(p);
-        o[1] = uint8_t(p >> 8);
-        o[2] = uint8_t(p >> 16);
+    const unsigned n = unsigned(W) * unsigned(H), ng = (n + 3) / 4;
+    const bool out_al = (reinterpret_cast<uintptr_t>(out) & 3) == 0;
+    for (unsigned g = blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += gridDim.x * blockDim.x) {
+        const unsigned k = 4 * g, i = k / unsigned(W), j = k - i * unsigned(W);
+        uint32_t px[4];
+        const uint32_t* row = in + (size_t)i * pitch + j;
+        if (!transposed && j + 3 < unsigned(W) && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
+            const uint4 v = *reinterpret_cast<const uint4*>(row);
+            px[0] = v.x; px[1] = v.y; px[2] = v.z; px[3] = v.w;
+        } else {
+            unsigned ii = i, jj = j;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const unsigned ci = min(ii, unsigned(H) - 1);
+                px[u] = transposed ? in[(size_t)jj * pitch + ci] : in[(size_t)ci * pitch + jj];
+                if (++jj == unsigned(W)) { jj = 0; ++ii; }
+            }
+        }
+        if (out_al && k + 3 < n) {
+            uint32_t* w3 = reinterpret_cast<uint32_t*>(out + 3ull * k);
+            w3[0] = (px[0] & 0xFFFFFFu) | (px[1] << 24);
+            w3[1] = ((px[1] >> 8) & 0xFFFFu) | (px[2] << 16);
+            w3[2] = ((px[2] >> 16) & 0xFFu) | (px[3] << 8);
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (k + u >= n) break;
+                uint8_t* o = out + 3ull * (k + u);
+                o[0] = uint8_t(px[u]);
+                o[1] = uint8_t(px[u] >> 8);
+                o[2] = uint8_t(px[u] >> 16);
+            }
+        }
     }
 }
 

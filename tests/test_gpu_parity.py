@@ -42,6 +42,16 @@ def test_energy_rgb_bitexact(port, w, h):
         assert np.array_equal(bits(cv.to_grayscale(img)), bits(port.to_grayscale(img)))
 
 
+@pytest.mark.parametrize("k1v", ["0", "1", "2", "3", "-1"])
+def test_energy_every_k1_shape_bitexact(port, monkeypatch, k1v):
+    """Each K1 launch shape (CARVE_K1V: 2 or 3 CTAs/SM, prefetch depth, run
+    length; -1 = the size-based default, which switches shape at 4 Mpx)."""
+    monkeypatch.setenv("CARVE_K1V", k1v)
+    for w, h in [(130, 33), (1920, 1080), (2500, 1700)]:
+        img = port.make_test_image(w, h)
+        assert np.array_equal(bits(cv.energy_e1_rgb(img)), bits(port.energy_e1_rgb(img)))
+
+
 def test_energy_luma_reference_cases():
     # test_energy.cpp:33-64
     assert (cv.energy_e1(np.full((4, 6), 123.0)) == 0).all()
