@@ -281,6 +281,17 @@ def test_batch_pipelined_chunks_match_oracle(port):
         assert np.array_equal(outs[k], want[k % 37]), k
 
 
+def test_batch_unaligned_image_strides(port):
+    # 37x23 packed images are 2553 bytes apart and 30x19 outputs 1710 bytes apart:
+    # most images start off a 4-byte boundary, which takes the byte-wise side of
+    # the 4-pixel RGB<->RGBX conversion, and 4-pixel groups straddle plane rows
+    n, w, h, tw, th = 21, 37, 23, 30, 19
+    imgs = [port.make_test_image(w, h, k) for k in range(n)]
+    outs = cv.carve_batch(imgs, tw, th)
+    for k in range(n):
+        assert np.array_equal(outs[k], port.carve(imgs[k], tw, th)), k
+
+
 def test_batch_two_pipelines_match_oracle(port):
     # >= 4 x 256 images per device: two concurrent copy/compute pipelines (their own
     # long-lived contexts and streams) share the device; halves split on a chunk
