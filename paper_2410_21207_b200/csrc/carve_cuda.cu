@@ -190,6 +190,7 @@ struct Prof {
 // of the calling thread's, so their worker threads (created per call) reuse the
 // streams and device buffers; each slot's mutex serialises concurrent callers
 thread_local Ctx* t_ctx_override = nullptr;
+constexpr int CARVE_MAX_PIPELINES = 4;  // concurrent pipelines / sub-batches per device
 struct PipeSlot {
     std::mutex m;
     std::unique_ptr<Ctx> c;
@@ -1449,10 +1450,50 @@ carve_status carve_cuda_carve_batch_device(const uint8_t* d_rgb, int n, int w, i
         check_targets(w, h, target_w, target_h);
         Ctx& c = ctx();
         const CarveGeometry g = geometry(w, h, target_w, target_h);
-        ensure_carve_buffers(c, g, n);
-        int* seams = static_cast<int*>(c.seams.ensure(std::max<size_t>(g.seam_ints, 1) * 4 * n));
         cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL = the legacy default stream
-        run_carve(c, d_rgb, d_out, n, g, seams, std::max<size_t>(g.seam_ints, 1), nullptr, s);
+        // Split into P concurrent sub-batches (CARVE_DEVICE_SPLIT, forked from and joined
+        // back into `s`), each on its own (device, pipeline) context, so one sub-batch's
+        // per-seam launches fill the other's wave tails. Per-kernel event profiling
+        // (c.prof) keeps one stream so its launch timings stay serial.
+        const int want = std::max(1, std::min(CARVE_MAX_PIPELINES, env_int("CARVE_DEVICE_SPLIT", 2)));
+        const int P = c.prof ? 1 : std::max(1, std::min(want, n / 64));
+        if (P == 1) {
+            ensure_carve_buffers(c, g, n);
+            int* seams = static_cast<int*>(c.seams.ensure(std::max<size_t>(g.seam_ints, 1) * 4 * n));
+            run_carve(c, d_rgb, d_out, n, g, seams, std::max<size_t>(g.seam_ints, 1), nullptr, s);
+            return;
+        }
+        const size_t in_bytes = size_t(w) * h * 3, out_bytes = size_t(target_w) * target_h * 3;
+        const int dev = c.device;
+        cudaEvent_t fork;
+        ck(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming), "event create");
+        ck(cudaEventRecord(fork, s), "record fork");
+        std::vector<std::unique_lock<std::mutex>> locks;
+        struct Reset {
+            ~Reset() { t_ctx_override = nullptr; }
+        } reset;
+        for (int q = 0; q < P; ++q) {
+            const int a = int((long long)n * q / P), b = int((long long)n * (q + 1) / P);
+            PipeSlot& slot = pipe_slot(dev, q);
+            locks.emplace_back(slot.m);
+            if (!slot.c) {
+                slot.c = std::make_unique<Ctx>(dev);
+                init_kernel_attributes(*slot.c);
+            }
+            t_ctx_override = slot.c.get();
+            Ctx& cq = ctx();
+            ensure_carve_buffers(cq, g, b - a);
+            int* seams = static_cast<int*>(cq.seams.ensure(std::max<size_t>(g.seam_ints, 1) * 4 * (b - a)));
+            ck(cudaStreamWaitEvent(cq.stream, fork, 0), "wait fork");
+            run_carve(cq, d_rgb + in_bytes * a, d_out + out_bytes * a, b - a, g, seams,
+                      std::max<size_t>(g.seam_ints, 1), nullptr, cq.stream);
+            cudaEvent_t join;
+            ck(cudaEventCreateWithFlags(&join, cudaEventDisableTiming), "event create");
+            ck(cudaEventRecord(join, cq.stream), "record join");
+            ck(cudaStreamWaitEvent(s, join, 0), "wait join");
+            ck(cudaEventDestroy(join), "event destroy");
+        }
+        ck(cudaEventDestroy(fork), "event destroy");
     });
 }
 
@@ -1462,7 +1503,6 @@ int pipe_chunk() {
     static const int v = std::max(16, env_int("CARVE_PIPE_CHUNK", 256));
     return v;
 }
-constexpr int CARVE_MAX_PIPELINES = 4;
 
 carve_status carve_cuda_carve_batch(const uint8_t* const* rgb, int n, int w, int h, int target_w, int target_h,
                                     uint8_t* const* rgb_out, const int* devices, int ndev) {

@@ -359,3 +359,24 @@ def test_fused_removal_last_column_seams(port, monkeypatch, w):
     fout, fseams = port.carve_cfg(img, tw, 12, forward=True, seams=True)
     assert np.array_equal(out, fout)
     assert np.array_equal(np.concatenate(seams), fseams)
+
+
+@pytest.mark.parametrize("split", ["1", "2", "3"])
+def test_batch_device_resident_split_matches_oracle(port, monkeypatch, split):
+    """carve_batch_device (the bench's device-resident path) on device buffers, with
+    the batch split into concurrent sub-batches (CARVE_DEVICE_SPLIT) forked from and
+    joined back into the caller's stream."""
+    import torch
+    monkeypatch.setenv("CARVE_DEVICE_SPLIT", split)
+    n, w, h, tw, th = 200, 45, 26, 37, 21
+    imgs = [port.make_test_image(w, h, k % 23) for k in range(n)]
+    d_in = torch.from_numpy(np.stack(imgs)).cuda()
+    d_out = torch.empty((n, th, tw, 3), dtype=torch.uint8, device="cuda")
+    d_out.fill_(7)
+    st = torch.cuda.current_stream()
+    cv.carve_batch_device(d_in.data_ptr(), n, w, h, tw, th, d_out.data_ptr(), st.cuda_stream)
+    st.synchronize()
+    outs = d_out.cpu().numpy()
+    want = {k: port.carve(imgs[k], tw, th) for k in range(23)}
+    for k in range(n):
+        assert np.array_equal(outs[k], want[k % 23]), k
