@@ -1456,7 +1456,7 @@ carve_status carve_cuda_carve_batch_device(const uint8_t* d_rgb, int n, int w, i
         // per-seam launches fill the other's wave tails. Per-kernel event profiling
         // (c.prof) keeps one stream so its launch timings stay serial.
         const int want = std::max(1, std::min(CARVE_MAX_PIPELINES, env_int("CARVE_DEVICE_SPLIT", 2)));
-        const int P = c.prof ? 1 : std::max(1, std::min(want, n / 64));
+        const int P = c.prof ? 1 : std::max(1, std::min(want, n / 256));  // >= 256 images per sub-batch
         if (P == 1) {
             ensure_carve_buffers(c, g, n);
             int* seams = static_cast<int*>(c.seams.ensure(std::max<size_t>(g.seam_ints, 1) * 4 * n));

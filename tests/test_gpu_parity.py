@@ -368,7 +368,7 @@ def test_batch_device_resident_split_matches_oracle(port, monkeypatch, split):
     joined back into the caller's stream."""
     import torch
     monkeypatch.setenv("CARVE_DEVICE_SPLIT", split)
-    n, w, h, tw, th = 200, 45, 26, 37, 21
+    n, w, h, tw, th = 780, 45, 26, 37, 21  # >= 256 images per sub-batch: 3 sub-batches at most
     imgs = [port.make_test_image(w, h, k % 23) for k in range(n)]
     d_in = torch.from_numpy(np.stack(imgs)).cuda()
     d_out = torch.empty((n, th, tw, 3), dtype=torch.uint8, device="cuda")
