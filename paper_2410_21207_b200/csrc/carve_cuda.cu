@@ -385,6 +385,11 @@ int device_sm_count() {
     return nsm;
 }
 
+// concurrent carves this thread's launches share the device with (pipelines or
+// sub-batches of one batch call): the small-batch DP shapes exist to fill the GPU
+// with few images, which the other carves already do
+thread_local int t_concurrency = 1;
+
 Dp2Plan dp2_plan(int W, int H, bool batch = false, bool fused = false, int nimg = 1) {
     const int nblk = H > 1 ? (H - 1 + LBLK - 1) / LBLK : 0;
     const int forced = env_int("CARVE_DP_VARIANT", -1);
@@ -392,7 +397,7 @@ Dp2Plan dp2_plan(int W, int H, bool batch = false, bool fused = false, int nimg 
     for (int pass = 0; pass < 2; ++pass) {
         std::vector<int> order;
         if (forced >= 0 && forced < int(dp2_variants().size())) order.push_back(forced);
-        else if (batch && nimg >= device_sm_count()) order.assign(std::begin(kDp2BatchOrder), std::end(kDp2BatchOrder));
+        else if (batch && (long long)nimg * t_concurrency >= device_sm_count()) order.assign(std::begin(kDp2BatchOrder), std::end(kDp2BatchOrder));
         else if (batch) order.assign(std::begin(kDp2SmallBatchOrder), std::end(kDp2SmallBatchOrder));
         else order.assign(std::begin(kDp2Order), std::end(kDp2Order));
         for (int k : order) {
@@ -1470,8 +1475,12 @@ carve_status carve_cuda_carve_batch_device(const uint8_t* d_rgb, int n, int w, i
         ck(cudaEventRecord(fork, s), "record fork");
         std::vector<std::unique_lock<std::mutex>> locks;
         struct Reset {
-            ~Reset() { t_ctx_override = nullptr; }
+            ~Reset() {
+                t_ctx_override = nullptr;
+                t_concurrency = 1;
+            }
         } reset;
+        t_concurrency = P;
         for (int q = 0; q < P; ++q) {
             const int a = int((long long)n * q / P), b = int((long long)n * (q + 1) / P);
             PipeSlot& slot = pipe_slot(dev, q);
@@ -1529,7 +1538,7 @@ carve_status carve_cuda_carve_batch(const uint8_t* const* rgb, int n, int w, int
         // Per device: one host thread per pipeline. A device with at least 4 chunks
         // runs two pipelines on halves of its share (each thread has its own context:
         // stream, buffers), so one pipeline's launches fill the other's wave tails.
-        auto worker = [&](int k, int pipe, int lo, int hi, int& st_out, std::string& msg_out) {
+        auto worker = [&](int k, int pipe, int npipes, int lo, int hi, int& st_out, std::string& msg_out) {
             if (lo >= hi) return;
             t_device = devs[k];
             PipeSlot& slot = pipe_slot(devs[k], pipe);
@@ -1540,8 +1549,12 @@ carve_status carve_cuda_carve_batch(const uint8_t* const* rgb, int n, int w, int
                     init_kernel_attributes(*slot.c);
                 }
                 t_ctx_override = slot.c.get();
+                t_concurrency = npipes;
                 struct Reset {
-                    ~Reset() { t_ctx_override = nullptr; }
+                    ~Reset() {
+                        t_ctx_override = nullptr;
+                        t_concurrency = 1;
+                    }
                 } reset;
                 Ctx& c = ctx();
                 if (hi - lo >= 2 * kPipeChunk && chunk_cap >= kPipeChunk) {
@@ -1611,9 +1624,9 @@ carve_status carve_cuda_carve_batch(const uint8_t* const* rgb, int n, int w, int
                 for (int q = 1; q < P; ++q) {
                     const int a = lo + int((long long)nchunks * q / P) * kPipeChunk;
                     const int b = std::min(hi, lo + int((long long)nchunks * (q + 1) / P) * kPipeChunk);
-                    th.emplace_back([&, k, q, a, b] { worker(k, q, a, b, pst[k][q], pmsg[k][q]); });
+                    th.emplace_back([&, k, q, a, b, P] { worker(k, q, P, a, b, pst[k][q], pmsg[k][q]); });
                 }
-                worker(k, 0, lo, std::min(hi, lo + int((long long)nchunks / P) * kPipeChunk), status[k], msgs[k]);
+                worker(k, 0, P, lo, std::min(hi, lo + int((long long)nchunks / P) * kPipeChunk), status[k], msgs[k]);
                 for (auto& t : th) t.join();
                 for (int q = 1; q < P && !status[k]; ++q)
                     if (pst[k][q]) {
@@ -1621,7 +1634,7 @@ carve_status carve_cuda_carve_batch(const uint8_t* const* rgb, int n, int w, int
                         msgs[k] = pmsg[k][q];
                     }
             } else {
-                worker(k, 0, lo, hi, status[k], msgs[k]);
+                worker(k, 0, 1, lo, hi, status[k], msgs[k]);
             }
         };
         std::vector<std::thread> pool;
