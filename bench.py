@@ -2,19 +2,26 @@
 """Benchmark of the B200 seam-carving engine (BASELINE.json metric:
 "seams removed/sec (1080p, 4K) and images/sec batched at 1/2/4/8 B200 vs CPU").
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|c3|c4|c5] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5]
+                    [--impl ours|reference] [--emulate-world G]
 
 A step is one carve of the configuration's synthetic input(s) (make_test_image,
-bench.hpp:67-94). Default config C2: 1920x1080 -> 1728x1080 (192 vertical
-seams) per GPU; under torchrun each rank carves its own image (weak scaling,
-no collective on the data path) and `value` is the total
-seams/s over all ranks, timed as the max over ranks. C5 (--config c5) shards a
-batch of 1024 1024x768 images by image across ranks (strong scaling, images/s).
+bench.hpp:67-94). The default line is C2 (1920x1080 -> 1728x1080, 192 vertical
+seams) per GPU; under torchrun each rank carves its own image (weak scaling, no
+collective on the data path) and `value` is the total seams/s
+over all ranks, timed as the max over ranks. The default line also carries the
+metric's other halves as objects: `c3` (4K: 3840x2160 -> 3072x1728, 768
+vertical + 432 transposed horizontal seams), `batch` (C5: 1024 distinct
+1024x768 images -> 896x768, sharded by image over the ranks) and
+`batch.shares` — the per-rank share of the 1024-image batch at 2/4/8 GPUs
+(512/256/128 images) timed on this one GPU, device-resident and end to end,
+with the projected efficiency of an image-sharded G-GPU run (no data crosses
+GPUs, so a rank's time is its share's time).
 
 `value`: inputs resident in HBM, one carve enqueued through the device entry
-point, CUDA events on the launching stream, L2 flushed between steps.
-`e2e`: the public host API (paper_2410_21207_b200.carve / carve_batch) from
-pinned host buffers, host<->device copies inside the timed region.
+point, CUDA events on the launching stream, L2 flushed (256 MiB write) between
+steps. `e2e`: the public host API (paper_2410_21207_b200.carve / carve_batch)
+from pinned host buffers, host<->device copies inside the timed region.
 `--impl reference`: the reference's CPU implementation (oracle/_ref, the
 reference compiled unmodified) on this host, rank 0 only.
 """
@@ -27,6 +34,7 @@ import statistics
 import subprocess
 import sys
 import time
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -41,8 +49,17 @@ CONFIGS = {
     "c4": (7680, 4320, 7168, 4320, 1, "C4 7680x4320 -> 7168x4320 (512 vertical seams)"),
     "c5": (1024, 768, 896, 768, 1024, "C5 batch of 1024 1024x768 -> 896x768 (128 seams each)"),
 }
+SHARES = (2, 4, 8)  # world sizes whose per-rank C5 share is timed on one GPU
 
 HBM_FALLBACK_GBS = 6650.0
+L2_NOTE = "GPU arm: L2 flushed (256 MiB write) between timed steps; CPU arm: n/a"
+
+
+def config_of(cfg_name: str) -> dict:
+    """The `config` dict both arms print (byte-identical for the same workload)."""
+    W, H, TW, TH, N, desc = CONFIGS[cfg_name]
+    unit = "images sharded by image over the ranks" if N > 1 else "one image per rank"
+    return {"workload": f"{desc}; {unit}", "l2": L2_NOTE}
 
 
 def dist_env():
@@ -65,13 +82,24 @@ def shard(n: int, world: int, rank: int) -> tuple[int, int]:
     return n * rank // world, n * (rank + 1) // world
 
 
+def make_images(cv, W, H, variants, out=None):
+    """make_test_image variants (host, outside timing), generated on host threads."""
+    arrs = out if out is not None else [np.empty((H, W, 3), np.uint8) for _ in variants]
+
+    def gen(k):
+        arrs[k][...] = cv.make_test_image(W, H, variants[k])
+    with ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 1)) as ex:
+        list(ex.map(gen, range(len(variants))))
+    return arrs
+
+
 class Clocks:
     """nvidia-smi clock/throttle sampling during the timed region."""
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.path = os.path.join("/tmp", f"carve_clocks_{os.getpid()}.csv")
+        self.path = os.path.join("/tmp", f"carve_clocks_{os.getpid()}_{index}.csv")
 
     def __enter__(self):
         try:
@@ -165,16 +193,14 @@ def run_reference(args, cfg_name):
     total = sum(times)
     value = unit_per_step * args.steps / total
     line = {
-        "impl": "reference", "metric": "images removed-seam batches/sec" if cfg_name == "c5" else "seams removed/sec",
+        "impl": "reference", "metric": "images/sec" if cfg_name == "c5" else "seams removed/sec",
         "value": value, "unit": unit, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "none (CPU)",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (make_test_image, bench.hpp:67-94)",
-        "config": {"workload": desc, "solver": solver_desc},
+        "config": config_of(cfg_name), "setup": {"solver": solver_desc, "host_threads": used_cores},
         "cpu_baseline": {"value": value, "unit": unit, "cores": used_cores, "kind": kind, "sample": sample_desc},
         "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    if cfg_name == "c5":
-        line["metric"] = "images/sec"
     print(json.dumps(line), flush=True)
 
 
@@ -246,9 +272,34 @@ class Ranks:
             self.dist.destroy_process_group()
 
 
-def measure(cfg_name, args, rk, distinct_max=None):
+class Inputs:
+    """One configuration's synthetic inputs: pinned host copies (e2e) and device
+    copies (device-resident timing) of this rank's images, plus outputs."""
+
+    def __init__(self, cv, cfg_name, rank, world, local):
+        import torch
+
+        W, H, TW, TH, N, desc = CONFIGS[cfg_name]
+        self.batch = N > 1
+        self.lo, self.hi = shard(N, world, rank) if self.batch else (0, 1)
+        n = self.hi - self.lo
+        self.pin_in = torch.empty((n, H, W, 3), dtype=torch.uint8, pin_memory=True)
+        views = [self.pin_in[k].numpy() for k in range(n)]
+        # every image distinct: batch image k is make_test_image variant k (the
+        # golden C5 samples use the same rule); single images: variant = rank
+        make_images(cv, W, H, [self.lo + k for k in range(n)] if self.batch else [rank], views)
+        self.pin_out = torch.empty((n, TH, TW, 3), dtype=torch.uint8, pin_memory=True)
+        self.d_in = self.pin_in.to(f"cuda:{local}")
+        self.d_out = torch.empty((n, TH, TW, 3), dtype=torch.uint8, device=f"cuda:{local}")
+        self.in_views = views
+        self.out_views = [self.pin_out[k].numpy() for k in range(n)]
+        self.n = n
+
+
+def measure(cfg_name, args, rk, inputs=None, n_share=None, profile=True):
     """One configuration: device-resident timed region (CUDA events, L2 flushed),
-    per-kernel attribution pass, e2e through the public host API."""
+    per-kernel attribution pass, e2e through the public host API. `n_share`
+    (batches): time only the first n_share images of this rank's inputs."""
     import torch
 
     import oracle  # checker only (golden hash of the benchmarked output)
@@ -256,43 +307,36 @@ def measure(cfg_name, args, rk, distinct_max=None):
 
     rank, world, local = rk.rank, rk.world, rk.local
     W, H, TW, TH, N, desc = CONFIGS[cfg_name]
-    batch = N > 1
-    lo, hi = shard(N, world, rank) if batch else (0, 1)
-    n_local = hi - lo
+    inp = inputs or Inputs(cv, cfg_name, rank, world, local)
+    batch = inp.batch
+    n_local = n_share or inp.n
     seams_per_img = (W - TW) + (H - TH)
-    n_distinct = min(n_local, distinct_max or n_local)
-
-    # synthetic inputs (host, outside timing), pinned host buffers for e2e
-    pin_in = torch.empty((n_local, H, W, 3), dtype=torch.uint8, pin_memory=True)
-    for k in range(n_local):
-        if k < n_distinct:
-            pin_in[k].numpy()[...] = cv.make_test_image(W, H, (lo + k) if batch else rank)
-        else:
-            pin_in[k].copy_(pin_in[k % n_distinct])
-    pin_out = torch.empty((n_local, TH, TW, 3), dtype=torch.uint8, pin_memory=True)
-    d_in = pin_in.to(f"cuda:{local}")
-    d_out = torch.empty((n_local, TH, TW, 3), dtype=torch.uint8, device=f"cuda:{local}")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")  # > 126 MB L2
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
+    d_seams = None if batch else torch.empty(max(1, (W - TW) * H + (H - TH) * TW), dtype=torch.int32,
+                                             device=f"cuda:{local}")
 
-    def enqueue():
+    def enqueue(seams=False):
         if batch:
-            cv.carve_batch_device(d_in.data_ptr(), n_local, W, H, TW, TH, d_out.data_ptr(), sptr)
+            cv.carve_batch_device(inp.d_in.data_ptr(), n_local, W, H, TW, TH, inp.d_out.data_ptr(), sptr)
         else:
-            cv.carve_device(d_in.data_ptr(), W, H, TW, TH, d_out.data_ptr(), None, sptr)
+            cv.carve_device(inp.d_in.data_ptr(), W, H, TW, TH, inp.d_out.data_ptr(),
+                            d_seams.data_ptr() if seams else None, sptr)
 
     for _ in range(args.warmup):
         enqueue()
     torch.cuda.synchronize()
 
     gold = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))["configs"]
-    out0 = d_out[0].cpu().numpy()
-    gkey, verified = cfg_name.upper(), None
-    if not batch and "output" in gold.get(gkey, {}) and rank == 0:
-        verified = f"{oracle.fnv1a64(out0):016x}" == gold[gkey]["output"]
-    elif batch and str(lo) in gold.get("C5", {}).get("samples", {}):
-        verified = f"{oracle.fnv1a64(out0):016x}" == gold["C5"]["samples"][str(lo)]["output"]
+    verified = None
+    if not batch and "output" in gold.get(cfg_name.upper(), {}) and rank == 0:
+        verified = f"{oracle.fnv1a64(inp.d_out[0].cpu().numpy()):016x}" == gold[cfg_name.upper()]["output"]
+    elif batch:
+        samples = {int(k) - inp.lo: v["output"] for k, v in gold.get("C5", {}).get("samples", {}).items()
+                   if 0 <= int(k) - inp.lo < n_local}
+        if samples:
+            verified = all(f"{oracle.fnv1a64(inp.d_out[k].cpu().numpy()):016x}" == h for k, h in samples.items())
 
     # ---- device-resident timed region -------------------------------------------------
     cv.reset_launch_count()
@@ -309,21 +353,31 @@ def measure(cfg_name, args, rk, distinct_max=None):
         rk.barrier()
     launches = cv.launch_count()
     dev_ms = rk.max(sum(a.elapsed_time(b) for a, b in evs))
-    units_total = N if batch else seams_per_img * world
+    units_total = (n_local * world) if batch else seams_per_img * world
     value = units_total * args.steps / (dev_ms / 1e3)
 
     # ---- kernel attribution pass (same workload, per-kernel CUDA events) ------------
-    kern = kernel_profile(cv, enqueue, stream, W, H, TW, TH, n_local)
+    kern = {}
+    if profile:
+        kern = kernel_profile(cv, lambda: enqueue(seams=True), W, H, TW, TH, n_local)
+        if not batch:
+            moved = inplace_removal_bytes(d_seams.cpu().numpy(), W, H, TW, TH)
+            k = kern.get("k_compact")
+            if k:
+                # the in-place removal moves only the part of a row right of the seam:
+                # bytes it must read + write (RGBX 4 B + FP64 energy 8 B per element),
+                # plus the library's count for each phase's last (transposing) launch
+                k["moved_bytes_per_launch"] = moved["bytes"] / k["launches"]
+                k["moved_gbs"] = moved["bytes"] / (k["ms_total"] * 1e-3) / 1e9
 
     # ---- end-to-end through the public host API (pinned host buffers) ---------------
-    in_views = [pin_in[k].numpy() for k in range(n_local)]
-    out_views = [pin_out[k].numpy() for k in range(n_local)]
+    ins, outs = inp.in_views[:n_local], inp.out_views[:n_local]
 
     def api_step():
         if batch:
-            cv.carve_batch(in_views, TW, TH, devices=[local], out=out_views)
+            cv.carve_batch(ins, TW, TH, devices=[local], out=outs)
         else:
-            cv.carve(in_views[0], TW, TH, out=out_views[0])
+            cv.carve(ins[0], TW, TH, out=outs[0])
 
     for _ in range(args.warmup):  # same W untimed warm-up steps as the device-resident region
         api_step()
@@ -336,117 +390,41 @@ def measure(cfg_name, args, rk, distinct_max=None):
     e2e = {"value": units_total * args.steps / e2e_s, "unit": unit,
            "h2d_bytes_per_step": W * H * 3 * n_local, "d2h_bytes_per_step": TW * TH * 3 * n_local,
            "api": "paper_2410_21207_b200.carve_batch" if batch else "paper_2410_21207_b200.carve"}
-    del d_in, d_out, flush
-    torch.cuda.empty_cache()
+    del flush
     return {"value": value, "unit": unit, "ms_per_step": dev_ms / args.steps, "e2e": e2e, "kernels": kern,
             "gpu_launches": launches, "verified_vs_golden": verified, "clocks": clk.summary(), "batch": batch,
-            "desc": desc, "n_local": n_local, "n_distinct": n_distinct}
+            "desc": desc, "n_local": n_local}
 
 
-def measured_traffic(kernel, cfg_name):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu
-    --set full capture (profiles/r01_traffic.json), for the workload it was taken on."""
-    try:
-        t = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
-        return t["bytes_per_launch"].get(cfg_name, {}).get(kernel)
-    except Exception:
-        return None
+def inplace_removal_bytes(seams, W, H, TW, TH):
+    """Bytes the in-place removal (k_compact_bulk, single images) must move for the
+    recorded seams: per row, the aligned part right of the seam is read (TMA, from
+    floor4(s) rounded to 4 elements) and written back shifted (Wn - floor4(s)),
+    RGBX 4 B + FP64 energy 8 B per element. Each phase's last removal is the
+    transposing kernel: 4 B read + 3 B written per pixel (library count)."""
+    total, off = 0.0, 0
+    for (w0, h, k) in ((W, H, W - TW), (H, TW, H - TH)):
+        for t in range(k):
+            s = seams[off:off + h].astype(np.int64)
+            off += h
+            w = w0 - t
+            if t + 1 == k:
+                total += 3.0 * h * (2.0 * w - 1)
+                continue
+            a = s & ~3
+            total += 12.0 * float((((w - a + 3) & ~3) + (w - 1 - a)).sum())
+    return {"bytes": total}
 
 
-# DP rows per launch (the DP is a row-serial chain: its real bound is latency per row)
-DP_ROWS = {"c1": 512, "c2": 1080, "c3": (768 * 2160 + 432 * 3072) / 1200, "c4": 4320, "c5": 768}
-# one warp's dependent row step (2 shuffles + 2 compare/selects + DADD), measured on B200 by
-# tools/microbench.cu (profiles/r01_microbench_latency.txt)
-CHAIN_CYCLES_PER_ROW = 59.0
-
-
-def roofline_of(kern, cfg_name="c2", sm_mhz=None):
-    peak, peak_src = peaks()
-    dom = max(kern, key=lambda k: kern[k]["ms_total"]) if kern else None
-    if not dom:
-        return None
-    kd = kern[dom]
-    r = {"kernel": dom, "bound": "hbm", "achieved": kd["gbs"], "peak": peak, "unit": "GB/s",
-         "frac": kd["gbs"] / peak, "traffic": measured_traffic(dom, cfg_name), "peak_source": peak_src,
-         "bytes_per_launch": kd["bytes_per_launch"], "avg_launch_us": kd["avg_us"], "share_of_step": kd["share"],
-         # HBM fraction of every timed kernel (algorithmic bytes / event time / peak). The removal's
-         # algorithmic bytes follow SURVEY.md §8d (a full-row copy: read W, write W-1); the in-place
-         # kernels move only the part right of the seam, so that fraction can exceed 1 — the
-         # DRAM-measured fraction (ncu bytes per launch / event time) is in dram_frac_by_kernel
-         "hbm_frac_by_kernel": {k: round(v["gbs"] / peak, 4) for k, v in kern.items()},
-         "dram_frac_by_kernel": {k: round(measured_traffic(k, cfg_name) / (v["avg_us"] * 1e3) / peak, 4)
-                                 for k, v in kern.items() if measured_traffic(k, cfg_name)}}
-    if dom == "k_dp_seam" and cfg_name in DP_ROWS and cfg_name != "c5":
-        ns_row = kd["avg_us"] * 1e3 / DP_ROWS[cfg_name]
-        floor = CHAIN_CYCLES_PER_ROW / ((sm_mhz or 1965.0) / 1e3)
-        r["latency"] = {"note": "the DP is latency-bound (row-serial chain), not HBM-bound",
-                        "ns_per_row": ns_row, "chain_floor_ns_per_row": floor, "frac_of_chain_floor": floor / ns_row}
-        try:  # shared-memory fraction and barrier stalls of the committed C2 ncu capture
-            nm = json.load(open(os.path.join(ROOT, "profiles", "r01_dp_ncu_metrics.json")))
-            if cfg_name == "c2":
-                r["latency"].update(smem_frac_active_sms=nm["smem_wavefronts_frac_of_peak_active_sms"],
-                                    barrier_stall_share=nm["barrier_stall_share"],
-                                    halo_wait_stall_share=nm["stall_share"].get("long_scoreboard"),
-                                    ncu_source="profiles/r01_dp_ncu_metrics.json")
-        except Exception:
-            pass
-    return r
-
-
-def run_ours(args, cfg_name):
-    import torch
-
-    import paper_2410_21207_b200 as cv
-
-    if not torch.cuda.is_available():
-        raise SystemExit("bench.py: no CUDA device")
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    cv.set_device(local)
-    rk = Ranks()
-    m = measure(cfg_name, args, rk)
-    batch = m["batch"]
-    line = {
-        "metric": "images/sec" if batch else "seams removed/sec",
-        "value": m["value"], "unit": m["unit"], "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": m["ms_per_step"], "higher_is_better": True, "scaling": "strong" if batch else "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (make_test_image, bench.hpp:67-94)",
-        "config": {"workload": m["desc"] + ("" if batch else " per GPU"), "images_per_gpu": m["n_local"],
-                   "l2": "flushed between steps (256 MiB write)",
-                   "parallelism": f"image-sharded x{world}, no collective"},
-        "e2e": m["e2e"], "gpu_launches": m["gpu_launches"], "roofline": roofline_of(m["kernels"], cfg_name, (m["clocks"] or {}).get("sm_mhz")),
-        "kernels": m["kernels"], "verified_vs_golden": m["verified_vs_golden"], "clocks": m["clocks"],
-    }
-    if not batch and not args.no_batch:
-        # the metric's second half: images/s batched, 1024 x (1024x768 -> 896x768), sharded by image
-        b = measure("c5", argparse.Namespace(steps=max(2, min(args.steps, 3)), warmup=3), rk, distinct_max=128)
-        line["batch"] = {"metric": "images/sec", "value": b["value"], "unit": b["unit"], "workload": b["desc"],
-                         "ms_per_step": b["ms_per_step"], "scaling": "strong", "e2e": b["e2e"],
-                         "images_per_gpu": b["n_local"],
-                         "data": f"{b['n_distinct']} distinct make_test_image variants per GPU, tiled to "
-                                 f"{b['n_local']} images", "verified_vs_golden": b["verified_vs_golden"],
-                         "roofline": roofline_of(b["kernels"], "c5", (b["clocks"] or {}).get("sm_mhz")), "kernels": b["kernels"],
-                         "gpu_launches": b["gpu_launches"], "clocks": b["clocks"]}
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(cfg_name)
-        if "batch" in line:
-            line["batch"]["cpu_baseline"] = cpu_baseline("c5")
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    rk.close()
-
-
-def kernel_profile(cv, enqueue, stream, W, H, TW, TH, n_local):
+def kernel_profile(cv, enqueue, W, H, TW, TH, n_local):
     """One extra carve with per-kernel CUDA events (library profiling mode):
     average launch duration, share of the step and algorithmic GB/s per kernel
     (algorithmic bytes per SURVEY.md §8d)."""
-    try:
-        cv.set_kernel_events(True)
-    except AttributeError:
-        return {}
+    import torch
+
+    cv.set_kernel_events(True)
     try:
         enqueue()
-        import torch
         torch.cuda.synchronize()
         stats = cv.kernel_event_stats()
     finally:
@@ -460,23 +438,177 @@ def kernel_profile(cv, enqueue, stream, W, H, TW, TH, n_local):
     return stats
 
 
+def measured_traffic(kernel, cfg_name):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu
+    --set full captures (profiles/r02_traffic.json, else r01), for the workload
+    they were taken on."""
+    for f in ("r02_traffic.json", "r01_traffic.json"):
+        try:
+            t = json.load(open(os.path.join(ROOT, "profiles", f)))
+            v = t["bytes_per_launch"].get(cfg_name, {}).get(kernel)
+            if v:
+                return v
+        except Exception:
+            pass
+    return None
+
+
+# DP rows per launch (the DP is a row-serial chain: its real bound is latency per row)
+DP_ROWS = {"c1": 512, "c2": 1080, "c3": (768 * 2160 + 432 * 3072) / 1200, "c4": 4320, "c5": 768}
+# one warp's dependent row step (2 shuffles + 2 compare/selects + DADD), measured on B200 by
+# tools/microbench.cu (profiles/r01_microbench_latency.txt)
+CHAIN_CYCLES_PER_ROW = 59.0
+
+
+def roofline_of(kern, cfg_name="c2", sm_mhz=None):
+    """The dominant kernel's bound. Single images: the DP (K2+K3) is a row-serial
+    latency chain, reported as ns per row against the measured chain floor; the
+    HBM-bound kernels (K1 energy, K4 removal) are reported against the measured
+    HBM peak in `hbm_kernels` — algorithmic bytes / event time, and ncu DRAM
+    bytes / event time where a capture exists (profiles/r0*_traffic.json)."""
+    peak, peak_src = peaks()
+    dom = max(kern, key=lambda k: kern[k]["ms_total"]) if kern else None
+    if not dom:
+        return None
+    kd = kern[dom]
+    hbm = {}
+    for k, v in kern.items():
+        e = {"algorithmic_gbs": round(v["gbs"], 1), "frac": round(v["gbs"] / peak, 4),
+             "avg_launch_us": round(v["avg_us"], 3), "bytes_per_launch": v["bytes_per_launch"]}
+        if "moved_gbs" in v:
+            e["moved_gbs"] = round(v["moved_gbs"], 1)
+            e["moved_frac"] = round(v["moved_gbs"] / peak, 4)
+        t = measured_traffic(k, cfg_name)
+        if t:
+            e["dram_bytes_per_launch"] = t
+            e["dram_frac"] = round(t / (v["avg_us"] * 1e3) / peak, 4)
+        hbm[k] = e
+    r = {"kernel": dom, "traffic": measured_traffic(dom, cfg_name), "bytes_per_launch": kd["bytes_per_launch"],
+         "avg_launch_us": kd["avg_us"], "share_of_step": kd["share"], "peak_source": peak_src,
+         "hbm_kernels": hbm}
+    if dom == "k_dp_seam" and cfg_name != "c5":
+        ns_row = kd["avg_us"] * 1e3 / DP_ROWS[cfg_name]
+        floor = CHAIN_CYCLES_PER_ROW / ((sm_mhz or 1965.0) / 1e3)
+        r.update(bound="latency", achieved=ns_row, peak=floor, unit="ns/row (lower is better)",
+                 frac=floor / ns_row, frac_of_chain_floor=floor / ns_row,
+                 note="row-serial DP chain; peak = measured 59-cycle chain floor at the sampled SM clock; "
+                      "its HBM view: " + f"{kd['gbs']:.0f} GB/s = {kd['gbs'] / peak:.3f} of {peak:.0f} GB/s")
+        try:  # shared-memory fraction and barrier stalls of the committed C2 ncu capture
+            nm = json.load(open(os.path.join(ROOT, "profiles", "r01_dp_ncu_metrics.json")))
+            if cfg_name == "c2":
+                r.update(smem_frac_active_sms=nm["smem_wavefronts_frac_of_peak_active_sms"],
+                         barrier_stall_share=nm["barrier_stall_share"],
+                         halo_wait_stall_share=nm["stall_share"].get("long_scoreboard"),
+                         ncu_source="profiles/r01_dp_ncu_metrics.json")
+        except Exception:
+            pass
+    else:
+        r.update(bound="hbm", achieved=kd["gbs"], peak=peak, unit="GB/s", frac=kd["gbs"] / peak)
+    return r
+
+
+def batch_object(cv, args, rk, local):
+    """C5 (1024 distinct images, sharded by image over the ranks) plus, at N=1,
+    the per-rank share of a 2/4/8-GPU run timed on this GPU."""
+    inp = Inputs(cv, "c5", rk.rank, rk.world, local)
+    nargs = argparse.Namespace(steps=max(2, min(args.steps, 3)), warmup=3)
+    b = measure("c5", nargs, rk, inputs=inp)
+    obj = {"metric": "images/sec", "value": b["value"], "unit": b["unit"], "config": config_of("c5"),
+           "ms_per_step": b["ms_per_step"], "scaling": "strong", "e2e": b["e2e"], "images_per_gpu": b["n_local"],
+           "data": f"{inp.n} distinct make_test_image variants (variant = image index) per GPU",
+           "verified_vs_golden": b["verified_vs_golden"],
+           "roofline": roofline_of(b["kernels"], "c5", (b["clocks"] or {}).get("sm_mhz")), "kernels": b["kernels"],
+           "gpu_launches": b["gpu_launches"], "clocks": b["clocks"]}
+    if rk.world == 1 and not args.no_shares:
+        shares = {}
+        for G in SHARES:
+            n = inp.n // G
+            s = measure("c5", nargs, rk, inputs=inp, n_share=n, profile=False)
+            shares[str(G)] = {
+                "images": n, "device_img_s": s["value"], "e2e_img_s": s["e2e"]["value"],
+                "projected_job_img_s_e2e": G * s["e2e"]["value"], "projected_job_img_s_device": G * s["value"],
+                "projected_efficiency_e2e": s["e2e"]["value"] / b["e2e"]["value"],
+                "projected_efficiency_device": s["value"] / b["value"], "clocks": s["clocks"],
+                "verified_vs_golden": s["verified_vs_golden"]}
+        obj["shares"] = {
+            "note": "one rank's share of the 1024-image batch at G GPUs, timed on this one GPU (device-resident "
+                    "and e2e from pinned host buffers through carve_batch); ranks share nothing, so a G-GPU run's "
+                    "time is its slowest share's time; projected efficiency = share rate / 1024-image rate",
+            **shares}
+    return obj
+
+
+def run_ours(args, cfg_name, default_line):
+    import torch
+
+    import paper_2410_21207_b200 as cv
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device")
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    cv.set_device(local)
+    rk = Ranks()
+    if cfg_name == "c5" and args.emulate_world:
+        # one rank's share of a G-GPU run, on this GPU
+        inp = Inputs(cv, "c5", 0, args.emulate_world, local)
+        m = measure("c5", args, rk, inputs=inp)
+    else:
+        m = measure(cfg_name, args, rk)
+    batch = m["batch"]
+    line = {
+        "metric": "images/sec" if batch else "seams removed/sec",
+        "value": m["value"], "unit": m["unit"], "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": m["ms_per_step"], "higher_is_better": True, "scaling": "strong" if batch else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (make_test_image, bench.hpp:67-94)",
+        "config": config_of(cfg_name),
+        "setup": {"images_per_gpu": m["n_local"], "parallelism": f"image-sharded x{world}, no collective",
+                  "emulated_world": args.emulate_world or None},
+        "e2e": m["e2e"], "gpu_launches": m["gpu_launches"],
+        "roofline": roofline_of(m["kernels"], cfg_name, (m["clocks"] or {}).get("sm_mhz")),
+        "kernels": m["kernels"], "verified_vs_golden": m["verified_vs_golden"], "clocks": m["clocks"],
+    }
+    if default_line:
+        # the metric's other halves: 4K seams/s and the C5 batch (+ per-rank shares)
+        c3 = measure("c3", argparse.Namespace(steps=max(2, min(args.steps, 3)), warmup=3), rk)
+        line["c3"] = {"metric": "seams removed/sec", "value": c3["value"], "unit": c3["unit"],
+                      "config": config_of("c3"), "ms_per_step": c3["ms_per_step"], "e2e": c3["e2e"],
+                      "verified_vs_golden": c3["verified_vs_golden"],
+                      "roofline": roofline_of(c3["kernels"], "c3", (c3["clocks"] or {}).get("sm_mhz")),
+                      "kernels": c3["kernels"], "gpu_launches": c3["gpu_launches"], "clocks": c3["clocks"]}
+        line["batch"] = batch_object(cv, args, rk, local)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg_name)
+        if "c3" in line:
+            line["c3"]["cpu_baseline"] = cpu_baseline("c3")
+        if "batch" in line:
+            line["batch"]["cpu_baseline"] = cpu_baseline("c5")
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    rk.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--emulate-world", type=int, default=0,
+                    help="--config c5: time one rank's share (1024/G images) of a G-GPU run on this GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-batch", action="store_true", help="skip the C5 batch object in the default line")
+    ap.add_argument("--no-batch", action="store_true", help="default line: skip the C3 and C5 objects")
+    ap.add_argument("--no-shares", action="store_true", help="default line: skip the per-rank share timings")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("bench.py: warmup raised to 3 (timing rule)", file=sys.stderr)
         args.warmup = 3
+    cfg = args.config or "c2"
     if args.impl == "reference":
-        run_reference(args, args.config)
+        run_reference(args, cfg)
     else:
-        run_ours(args, args.config)
+        run_ours(args, cfg, default_line=args.config is None and not args.no_batch)
 
 
 if __name__ == "__main__":

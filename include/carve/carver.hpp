@@ -76,6 +76,25 @@ inline std::pair<PixelGrid, CarveReport> carve_device(const PixelGrid& grid, int
     return {std::move(out), std::move(rep)};
 }
 
+/// carver.hpp:57-67: column deletion on a row-major scalar grid (row i loses
+/// column seam[i]); on the device. Like the reference it does not require a
+/// connected seam; columns outside [0, width) throw invalid_seam.
+inline std::vector<double> drop_columns(const std::vector<double>& values, int width, int height,
+                                        const Seam& seam) {
+    std::vector<double> out(size_t(std::max(width - 1, 0)) * height);
+    check(carve_cuda_remove_seam_f64(values.data(), width, height, seam.data(), int(seam.size()), out.data()));
+    return out;
+}
+
+/// carver.hpp:118-132: per-row duplication without the seam-connectivity
+/// requirement (replayed recorded seams may jump more than one column).
+inline PixelGrid insert_columns(const PixelGrid& grid, const std::vector<int>& cols) {
+    PixelGrid out(grid.width + 1, grid.height);
+    check(carve_cuda_insert_columns_rgb(grid.bytes(), grid.width, grid.height, cols.data(), int(cols.size()),
+                                        out.bytes()));
+    return out;
+}
+
 } // namespace detail
 
 inline PixelGrid remove_seam(const PixelGrid& grid, const Seam& seam) {
@@ -84,6 +103,34 @@ inline PixelGrid remove_seam(const PixelGrid& grid, const Seam& seam) {
     PixelGrid out(grid.width - 1, grid.height);
     detail::check(carve_cuda_remove_seam_rgb(grid.bytes(), grid.width, grid.height, seam.data(), int(seam.size()),
                                              out.bytes()));
+    return out;
+}
+
+/// carver.hpp:84-98: the LumaGrid and EnergyMap overloads (detail::drop_columns).
+inline LumaGrid remove_seam(const LumaGrid& gray, const Seam& seam) {
+    LumaGrid out;
+    out.width = gray.width - 1;
+    out.height = gray.height;
+    out.values = detail::drop_columns(gray.values, gray.width, gray.height, seam);
+    return out;
+}
+
+inline EnergyMap remove_seam(const EnergyMap& energy, const Seam& seam) {
+    EnergyMap out;
+    out.width = energy.width - 1;
+    out.height = energy.height;
+    out.values = detail::drop_columns(energy.values, energy.width, energy.height, seam);
+    return out;
+}
+
+/// carver.hpp:100-112: the RemovalMask overload.
+inline RemovalMask remove_seam(const RemovalMask& mask, const Seam& seam) {
+    RemovalMask out;
+    out.width = mask.width - 1;
+    out.height = mask.height;
+    out.flags.resize(size_t(std::max(out.width, 0)) * out.height);
+    detail::check(carve_cuda_remove_seam_u8(mask.flags.data(), mask.width, mask.height, seam.data(),
+                                            int(seam.size()), out.flags.data()));
     return out;
 }
 

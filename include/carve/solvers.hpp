@@ -81,20 +81,18 @@ inline SeamResult parallel_dp_seam(const EnergyMap& energy, unsigned workers = 0
     return dp_seam(energy);
 }
 
-/// solvers.hpp:294-326 forward-energy DP on the B200. The device recomputes the
-/// transition costs from `gray` in registers, so `costs` must be
-/// forward_costs(gray) (the reference's only producer); other costs are
-/// rejected with usage_error rather than silently ignored.
+/// solvers.hpp:294-326 forward-energy DP on the B200 over the caller's three
+/// cost planes (any finite values; `gray` only supplies the dimensions, as in
+/// the reference). Non-finite costs throw usage_error: the device scan assumes
+/// finite candidates where the reference starts from best = +inf.
 inline SeamResult dp_seam_forward(const LumaGrid& gray, const ForwardCosts& costs) {
     if (gray.width < 1 || gray.height < 1) fail(Errc::empty_image, "image is empty");
     if (gray.width != costs.width || gray.height != costs.height)
         fail(Errc::dimension_mismatch, "forward costs do not match image dimensions");
-    const ForwardCosts own = forward_costs(gray);
-    if (own.cost_left != costs.cost_left || own.cost_up != costs.cost_up || own.cost_right != costs.cost_right)
-        detail::unsupported("dp_seam_forward with costs other than forward_costs(gray)");
     SeamResult r{Seam(size_t(gray.height)), CostTable(gray.width, gray.height)};
-    detail::check(carve_cuda_dp_seam_forward(gray.values.data(), gray.width, gray.height, r.table.m.data(),
-                                             r.table.b.data(), r.seam.data()));
+    detail::check(carve_cuda_dp_seam_forward_costs(costs.cost_left.data(), costs.cost_up.data(),
+                                                   costs.cost_right.data(), gray.width, gray.height,
+                                                   r.table.m.data(), r.table.b.data(), r.seam.data()));
     return r;
 }
 

@@ -65,8 +65,8 @@ enum {
  * have no output effect on this path (dp == pardp; e1 only). */
 typedef struct carve_cuda_config {
     int forward;   /* forward energy: dp_seam_forward on forward_costs(to_grayscale(current)) */
-    int recompute; /* 0: e1 once, then the map is carved alongside (carver.hpp:176-188);
-                      forward with recompute = 0 returns CARVE_E_USAGE_ERROR (not supported) */
+    int recompute; /* 0: the phase's first e1 map (or, with forward, its three forward-cost
+                      planes) is computed once and then only carved (carver.hpp:175-188) */
 } carve_cuda_config;
 
 typedef struct carve_seam_timing {
@@ -125,6 +125,12 @@ carve_status carve_cuda_forward_costs(const double* luma, int w, int h, double* 
  * and seam, bit-identical. */
 carve_status carve_cuda_dp_seam_forward(const double* luma, int w, int h, double* m_out, int32_t* b_out,
                                         int32_t* seam_out);
+/* replaces dp_seam_forward(gray, costs) for arbitrary caller-given costs
+ * (solvers.hpp:294-326; gray only supplies the dimensions there): three w*h
+ * planes, row-major. Finite costs only: a non-finite cost returns
+ * CARVE_E_USAGE_ERROR (the reference's best = +inf start would then differ). */
+carve_status carve_cuda_dp_seam_forward_costs(const double* left, const double* up, const double* right, int w,
+                                              int h, double* m_out, int32_t* b_out, int32_t* seam_out);
 
 /* ---- object removal (energy.hpp:220-253, carver.hpp:287-340) ---------- */
 /* replaces mask_from_image: flags (w*h bytes) = luma >= 128 */
@@ -145,6 +151,11 @@ carve_status carve_cuda_remove_object(const uint8_t* rgb, int w, int h, const ui
  * :117-130); out is (w+1)*h*3 bytes */
 carve_status carve_cuda_insert_seam_rgb(const uint8_t* rgb, int w, int h, const int32_t* seam, int n,
                                         uint8_t* out);
+/* replaces detail::insert_columns (carver.hpp:118-132): as insert_seam but
+ * without the connectivity check (replayed recorded seams may jump); columns
+ * must lie in [0, w) (CARVE_E_INVALID_SEAM otherwise) */
+carve_status carve_cuda_insert_columns_rgb(const uint8_t* rgb, int w, int h, const int32_t* cols, int n,
+                                           uint8_t* out);
 /* replaces record_seams (carver.hpp:226-262) with the default CarveConfig:
  * seams_out receives count*h ints, seam t's column of row i at [t*h + i], in
  * original-image coordinates. timings_out (nullable): count entries. */
@@ -162,6 +173,13 @@ carve_status carve_cuda_enlarge(const uint8_t* rgb, int w, int h, int target_w, 
 /* replaces remove_seam(PixelGrid) (carver.hpp:71-82); out is (w-1)*h*3 bytes */
 carve_status carve_cuda_remove_seam_rgb(const uint8_t* rgb, int w, int h, const int32_t* seam, int n,
                                         uint8_t* out);
+/* replace remove_seam(LumaGrid) / remove_seam(EnergyMap) (f64) and
+ * remove_seam(RemovalMask) (u8) = detail::drop_columns (carver.hpp:57-67,
+ * 84-112): the w*h plane minus column seam[i] of row i, out is (w-1)*h values.
+ * Like the reference these do not require a connected seam; n must equal h and
+ * every column must lie in [0, w) (CARVE_E_INVALID_SEAM otherwise). */
+carve_status carve_cuda_remove_seam_f64(const double* in, int w, int h, const int32_t* seam, int n, double* out);
+carve_status carve_cuda_remove_seam_u8(const uint8_t* in, int w, int h, const int32_t* seam, int n, uint8_t* out);
 /* replaces run_resize's carving (cli.hpp:249-256): carve_to_width(target_w)
  * then, if target_h != h, carve_to_height(target_h) (carver.hpp:191-222).
  * rgb_out: target_w*target_h*3 bytes.
@@ -176,17 +194,29 @@ carve_status carve_cuda_carve_cfg(const uint8_t* rgb, int w, int h, int target_w
 carve_status carve_cuda_carve(const uint8_t* rgb, int w, int h, int target_w, int target_h, uint8_t* rgb_out,
                               int32_t* seams_out, carve_seam_timing* timings_out);
 
-/* Batch of n same-size images carved to target_w x target_h, sharded by image
- * across `ndev` devices (devices == NULL: 0..ndev-1; ndev <= 0: all), one host
- * thread per device, no inter-device communication. */
+/* Batch of n same-size images carved to target_w x target_h across `ndev`
+ * devices (devices == NULL: 0..ndev-1; ndev <= 0: all; a device may be listed
+ * more than once). One host thread per listed device claims chunks of whole
+ * images from a shared atomic counter (SURVEY.md §8e work queue) and runs P
+ * copy/compute pipelines on them: chunk uploads, carves and downloads overlap.
+ * No inter-device communication. */
 carve_status carve_cuda_carve_batch(const uint8_t* const* rgb, int n, int w, int h, int target_w, int target_h,
                                     uint8_t* const* rgb_out, const int* devices, int ndev);
+/* The host pipeline shape carve_cuda_carve_batch uses for n images over ndev
+ * devices: pipelines per device and images per chunk (pure host logic; honours
+ * CARVE_PIPELINES / CARVE_PIPE_CHUNK). */
+carve_status carve_cuda_batch_plan(int n, int w, int h, int target_w, int target_h, int ndev, int* pipes,
+                                   int* chunk);
 
 /* ---- device-resident entry points (inputs already in HBM) --------------
  * d_rgb / d_out are device pointers to packed RGB on the current device;
  * `stream` is a cudaStream_t (NULL = the legacy default stream). These
  * enqueue work and return without synchronizing (the bench times them with
- * CUDA events on `stream`). d_seams (nullable) receives seams as above. */
+ * CUDA events on `stream`). The work runs on library-owned streams forked
+ * from `stream` by an event and joined back into it, so the library's scratch
+ * is always ordered on one stream: later calls of this thread (synchronous or
+ * asynchronous, on any stream) wait for it. d_seams (nullable) receives seams
+ * as above. */
 carve_status carve_cuda_carve_device(const uint8_t* d_rgb, int w, int h, int target_w, int target_h,
                                      uint8_t* d_out, int32_t* d_seams, void* stream);
 carve_status carve_cuda_carve_batch_device(const uint8_t* d_rgb, int n, int w, int h, int target_w, int target_h,

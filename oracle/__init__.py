@@ -105,6 +105,16 @@ class _Checker:
             np.ascontiguousarray(luma, np.float64), w, h, m, b, seam))
         return seam, m, b
 
+    def dp_seam_forward_costs(self, cl: np.ndarray, cu: np.ndarray, cr: np.ndarray):
+        """solvers.hpp:294-326 with arbitrary costs -> (seam, m, b)"""
+        h, w = cl.shape
+        m = np.empty((h, w), np.float64)
+        b = np.empty((h, w), np.int32)
+        seam = np.empty(h, np.int32)
+        self._check(self._fn("dp_seam_forward_costs", _f8p, _f8p, _f8p, C.c_int, C.c_int, _f8p, _i4p, _i4p)(
+            *(np.ascontiguousarray(x, np.float64) for x in (cl, cu, cr)), w, h, m, b, seam))
+        return seam, m, b
+
     def carve_cfg(self, img: np.ndarray, target_w: int, target_h: int | None = None, forward: bool = False,
                   recompute: bool = True, seams: bool = False):
         """run_resize with CarveConfig::forward / ::recompute"""
@@ -180,6 +190,16 @@ class Port(_Checker):
 
     prefix = "or_"
 
+    def remove_seam_plane(self, plane: np.ndarray, seam) -> np.ndarray:
+        """carver.hpp:57-67, 84-112: a float64 (LumaGrid/EnergyMap) or uint8 (RemovalMask) plane."""
+        a = np.ascontiguousarray(plane)
+        h, w = a.shape
+        s = np.ascontiguousarray(seam, np.int32)
+        out = np.empty((h, max(w - 1, 0)), a.dtype)
+        f = self._fn("drop_columns", C.c_void_p, C.c_int, C.c_int, _i4p, C.c_int, C.c_int, C.c_void_p)
+        self._check(f(a.ctypes.data, w, h, s, len(s), a.dtype.itemsize, out.ctypes.data))
+        return out
+
     def make_test_image(self, w: int, h: int, variant: int = 0) -> np.ndarray:
         out = np.empty((h, w, 3), np.uint8)
         self._check(self._fn("make_test_image", C.c_int, C.c_int, C.c_uint32, _u8p)(w, h, variant, out))
@@ -226,6 +246,30 @@ class Reference(_Checker):
     """The unmodified reference, compiled from /root/reference (ref_shim.cpp)."""
 
     prefix = "ref_"
+
+    def remove_seam_plane(self, plane: np.ndarray, seam, kind: str = "energy") -> np.ndarray:
+        """remove_seam(LumaGrid) (kind "luma"), (EnergyMap) ("energy") or (RemovalMask) (uint8 plane)."""
+        a = np.ascontiguousarray(plane)
+        h, w = a.shape
+        s = np.ascontiguousarray(seam, np.int32)
+        out = np.empty((h, max(w - 1, 0)), a.dtype)
+        if a.dtype == np.uint8:
+            f = self._fn("remove_seam_u8", _u8p, C.c_int, C.c_int, _i4p, C.c_int, C.c_void_p)
+            self._check(f(a, w, h, s, len(s), out.ctypes.data))
+        else:
+            f = self._fn("remove_seam_f64", _f8p, C.c_int, C.c_int, _i4p, C.c_int, C.c_int, C.c_void_p)
+            self._check(f(a, w, h, s, len(s), 0 if kind == "luma" else 1, out.ctypes.data))
+        return out
+
+    def bench_record(self, img: np.ndarray, full: bool, scale: float = 1.0, forward: bool = False, reps: int = 1):
+        """BenchRecord fields of time_full_carve / time_single_seam (bench.hpp:140-201)."""
+        h, w, _ = img.shape
+        out = np.zeros(5, np.int32)
+        sc = np.zeros(1, np.float64)
+        f = self._fn("bench_record", _u8p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, _i4p, _f8p)
+        self._check(f(np.ascontiguousarray(img), w, h, int(full), scale, int(forward), reps, out, sc))
+        return {"solver": int(out[0]), "n": int(out[1]), "phase": int(out[2]),
+                "scale": float(sc[0]) if out[3] else None, "repetitions": int(out[4])}
 
     def last_error(self) -> str:
         return self._fn("last_error", restype=C.c_char_p)().decode()

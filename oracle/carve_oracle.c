@@ -236,18 +236,16 @@ int or_forward_costs(const double* g, int w, int h, double* left, double* up, do
     return OR_OK;
 }
 
-/* solvers.hpp:294-326 dp_seam_forward(g, forward_costs(g)): candidates
- * prev + transition cost in the order left, up, right, strict <. m/b nullable. */
-int or_dp_seam_forward(const double* g, int w, int h, double* m_out, int* b_out, int* seam) {
+/* solvers.hpp:294-326 dp_seam_forward(gray, costs) for arbitrary costs (gray
+ * only supplies the dimensions): candidates prev + transition cost in the
+ * order left, up, right, strict <, best starting at +inf. m/b nullable. */
+int or_dp_seam_forward_costs(const double* cl, const double* cu, const double* cr, int w, int h, double* m_out,
+                             int* b_out, int* seam) {
     if (w < 1 || h < 1) return OR_EMPTY_IMAGE;
     const size_t n = (size_t)w * h;
-    double* cl = (double*)malloc(n * 8);
-    double* cu = (double*)malloc(n * 8);
-    double* cr = (double*)malloc(n * 8);
     double* m = m_out ? m_out : (double*)malloc(n * 8);
     int* b = b_out ? b_out : (int*)malloc(n * 4);
-    if (!cl || !cu || !cr || !m || !b) return OR_NO_MEMORY;
-    or_forward_costs(g, w, h, cl, cu, cr);
+    if (!m || !b) return OR_NO_MEMORY;
     for (int j = 0; j < w; ++j) {
         m[j] = cu[j];
         b[j] = j;
@@ -281,11 +279,40 @@ int or_dp_seam_forward(const double* g, int w, int h, double* m_out, int* b_out,
         if (last[j] < last[c]) c = j;
     seam[h - 1] = c;
     for (int i = h - 1; i > 0; --i) seam[i - 1] = b[(size_t)i * w + seam[i]];
+    if (!m_out) free(m);
+    if (!b_out) free(b);
+    return OR_OK;
+}
+
+/* solvers.hpp:294-326 dp_seam_forward(g, forward_costs(g)) */
+int or_dp_seam_forward(const double* g, int w, int h, double* m_out, int* b_out, int* seam) {
+    if (w < 1 || h < 1) return OR_EMPTY_IMAGE;
+    const size_t n = (size_t)w * h;
+    double* cl = (double*)malloc(n * 8);
+    double* cu = (double*)malloc(n * 8);
+    double* cr = (double*)malloc(n * 8);
+    if (!cl || !cu || !cr) return OR_NO_MEMORY;
+    or_forward_costs(g, w, h, cl, cu, cr);
+    const int st = or_dp_seam_forward_costs(cl, cu, cr, w, h, m_out, b_out, seam);
     free(cl);
     free(cu);
     free(cr);
-    if (!m_out) free(m);
-    if (!b_out) free(b);
+    return st;
+}
+
+/* carver.hpp:57-67 detail::drop_columns, the body of remove_seam(LumaGrid /
+ * EnergyMap) (:84-98) and of remove_seam(RemovalMask) (:100-112): row i loses
+ * column seam[i]; no connectivity requirement (the reference does not
+ * validate these overloads). elem = 8 (doubles) or 1 (mask bytes). */
+int or_drop_columns(const void* in, int w, int h, const int* seam, int n, int elem, void* out) {
+    if (n != h) return OR_INVALID_SEAM;
+    for (int i = 0; i < h; ++i) {
+        if (seam[i] < 0 || seam[i] >= w) return OR_INVALID_SEAM;
+        const uint8_t* src = (const uint8_t*)in + (size_t)i * w * elem;
+        uint8_t* dst = (uint8_t*)out + (size_t)i * (w - 1) * elem;
+        memcpy(dst, src, (size_t)seam[i] * elem);
+        memcpy(dst + (size_t)seam[i] * elem, src + (size_t)(seam[i] + 1) * elem, (size_t)(w - seam[i] - 1) * elem);
+    }
     return OR_OK;
 }
 
@@ -299,10 +326,24 @@ static int carve_width_cfg(uint8_t* work, int w, int h, int target_w, int forwar
     double* e2 = (double*)malloc(sizeof(double) * (size_t)w * h);
     uint8_t* tmp = (uint8_t*)malloc((size_t)w * h * 3);
     int* seam = (int*)malloc(sizeof(int) * (size_t)h);
+    /* forward + recompute=false: the cached ForwardCosts (carver.hpp:157-160, 177-183) */
+    double* fc[3] = {NULL, NULL, NULL};
     if (!e || !e2 || !tmp || !seam) return OR_NO_MEMORY;
     if (!recompute && !forward) or_energy_e1_rgb(work, w, h, e);
+    if (!recompute && forward) {
+        for (int k = 0; k < 3; ++k)
+            if (!(fc[k] = (double*)malloc(sizeof(double) * (size_t)w * h))) return OR_NO_MEMORY;
+        or_to_grayscale(work, w, h, e);
+        or_forward_costs(e, w, h, fc[0], fc[1], fc[2]);
+    }
     for (int cw = w; cw > target_w; --cw) {
-        if (forward) {
+        if (forward && !recompute) {
+            or_dp_seam_forward_costs(fc[0], fc[1], fc[2], cw, h, NULL, NULL, seam);
+            for (int k = 0; k < 3; ++k) { /* drop_columns on each cost plane (carver.hpp:179-181) */
+                or_drop_columns(fc[k], cw, h, seam, h, 8, e2);
+                memcpy(fc[k], e2, sizeof(double) * (size_t)(cw - 1) * h);
+            }
+        } else if (forward) {
             or_to_grayscale(work, cw, h, e);
             or_dp_seam_forward(e, cw, h, NULL, NULL, seam);
         } else {
@@ -329,6 +370,7 @@ static int carve_width_cfg(uint8_t* work, int w, int h, int target_w, int forwar
     free(e2);
     free(tmp);
     free(seam);
+    for (int k = 0; k < 3; ++k) free(fc[k]);
     return OR_OK;
 }
 

@@ -207,6 +207,79 @@ int ref_dp_seam_forward(const double* luma, int w, int h, double* m_out, int* b_
     });
 }
 
+// solvers.hpp:294-326 dp_seam_forward(gray, costs) with arbitrary caller costs
+// (gray only supplies the dimensions there)
+int ref_dp_seam_forward_costs(const double* left, const double* up, const double* right, int w, int h,
+                              double* m_out, int* b_out, int* seam_out) {
+    return guarded([&] {
+        carve_ref::LumaGrid g;
+        g.width = w;
+        g.height = h;
+        g.values.assign(size_t(w) * h, 0.0);
+        carve_ref::ForwardCosts fc;
+        fc.width = w;
+        fc.height = h;
+        const size_t n = size_t(w) * h;
+        fc.cost_left.assign(left, left + n);
+        fc.cost_up.assign(up, up + n);
+        fc.cost_right.assign(right, right + n);
+        auto r = carve_ref::dp_seam_forward(g, fc);
+        std::memcpy(m_out, r.table.m.data(), r.table.m.size() * 8);
+        std::memcpy(b_out, r.table.b.data(), r.table.b.size() * 4);
+        std::memcpy(seam_out, r.seam.data(), r.seam.size() * 4);
+    });
+}
+
+// carver.hpp:84-112 remove_seam(LumaGrid) (kind 0) / remove_seam(EnergyMap) (kind 1)
+int ref_remove_seam_f64(const double* in, int w, int h, const int* seam, int n, int kind, double* out) {
+    return guarded([&] {
+        const carve_ref::Seam s(seam, seam + n);
+        std::vector<double> v;
+        if (kind == 0) {
+            carve_ref::LumaGrid g;
+            g.width = w;
+            g.height = h;
+            g.values.assign(in, in + size_t(w) * h);
+            v = carve_ref::remove_seam(g, s).values;
+        } else {
+            v = carve_ref::remove_seam(map_from(in, w, h), s).values;
+        }
+        std::memcpy(out, v.data(), v.size() * 8);
+    });
+}
+
+// carver.hpp:100-112 remove_seam(RemovalMask)
+int ref_remove_seam_u8(const std::uint8_t* in, int w, int h, const int* seam, int n, std::uint8_t* out) {
+    return guarded([&] {
+        carve_ref::RemovalMask m;
+        m.width = w;
+        m.height = h;
+        m.flags.assign(in, in + size_t(w) * h);
+        auto r = carve_ref::remove_seam(m, carve_ref::Seam(seam, seam + n));
+        std::memcpy(out, r.flags.data(), r.flags.size());
+    });
+}
+
+// bench.hpp:140-174 time_single_seam / :177-201 time_full_carve: the BenchRecord
+// fields (solver, n, phase, scale, repetitions) of one call, for the drop-in's
+// BenchRecord test. out: [solver, n, phase, has_scale, repetitions], scale_out
+int ref_bench_record(const std::uint8_t* rgb, int w, int h, int full, double scale, int forward, int reps,
+                     int* out, double* scale_out) {
+    return guarded([&] {
+        carve_ref::CarveConfig cfg;
+        cfg.forward = forward != 0;
+        const auto img = grid_from(rgb, w, h);
+        const carve_ref::BenchRecord r = full ? carve_ref::time_full_carve(img, scale, cfg, reps)
+                                              : carve_ref::time_single_seam(img, cfg, reps);
+        out[0] = int(r.solver);
+        out[1] = r.n;
+        out[2] = int(r.phase);
+        out[3] = r.scale.has_value() ? 1 : 0;
+        out[4] = r.repetitions;
+        *scale_out = r.scale.value_or(0.0);
+    });
+}
+
 // run_resize (cli.hpp:242-259) with CarveConfig::forward / ::recompute
 // (carver.hpp:15-24, 153-188); seams_out as ref_carve.
 int ref_carve_cfg(const std::uint8_t* rgb, int w, int h, int target_w, int target_h, int forward, int recompute,

@@ -182,7 +182,11 @@ def library() -> C.CDLL:
             "carve_cuda_apply_mask": ([vp, i, i, vp, vp], i),
             "carve_cuda_remove_object": ([vp, i, i, vp, vp, i, vp, vp, vp, vp, vp], i),
             "carve_cuda_dp_seam_forward": ([vp, i, i, vp, vp, vp], i),
+            "carve_cuda_dp_seam_forward_costs": ([vp, vp, vp, i, i, vp, vp, vp], i),
+            "carve_cuda_remove_seam_f64": ([vp, i, i, vp, i, vp], i),
+            "carve_cuda_remove_seam_u8": ([vp, i, i, vp, i, vp], i),
             "carve_cuda_carve_batch": ([vp, i, i, i, i, i, vp, vp, i], i),
+            "carve_cuda_batch_plan": ([i, i, i, i, i, i, vp, vp], i),
             "carve_cuda_carve_device": ([vp, i, i, i, i, vp, vp, vp], i),
             "carve_cuda_carve_batch_device": ([vp, i, i, i, i, i, vp, vp], i),
             "carve_make_test_image": ([i, i, C.c_uint32, vp], i),
@@ -347,7 +351,23 @@ def validate_seam(seam, width: int, height: int) -> None:
 
 # -- pipelines --------------------------------------------------------------------
 def remove_seam(img: np.ndarray, seam) -> np.ndarray:
-    """carver.hpp:71-82"""
+    """remove_seam overloads (carver.hpp:71-112), dispatched on the array like the
+    reference's on the type: (H, W, 3) uint8 PixelGrid (validated seam, W >= 2);
+    (H, W) float64 LumaGrid / EnergyMap and (H, W) uint8 RemovalMask =
+    detail::drop_columns (carver.hpp:57-67), no connectivity requirement."""
+    arr = np.asarray(img)
+    if arr.ndim == 2:
+        s = np.ascontiguousarray(seam, dtype=np.int32)
+        h, w = arr.shape
+        if arr.dtype == np.uint8:
+            a = np.ascontiguousarray(arr)
+            out = np.empty((h, max(w - 1, 0)), np.uint8)
+            _check(library().carve_cuda_remove_seam_u8(_ptr(a), w, h, _ptr(s), len(s), _ptr(out)))
+        else:
+            a = np.ascontiguousarray(arr, dtype=np.float64)
+            out = np.empty((h, max(w - 1, 0)), np.float64)
+            _check(library().carve_cuda_remove_seam_f64(_ptr(a), w, h, _ptr(s), len(s), _ptr(out)))
+        return out
     a = _img(img)
     h, w, _ = a.shape
     s = np.ascontiguousarray(seam, dtype=np.int32)
@@ -449,21 +469,24 @@ def forward_costs(luma: np.ndarray):
 
 
 def dp_seam_forward(luma: np.ndarray, costs=None) -> SeamResult:
-    """solvers.hpp:294-326 forward-energy DP. The device derives the transition
-    costs from `luma`; `costs` (if given) must equal forward_costs(luma)."""
+    """solvers.hpp:294-326 forward-energy DP on the device. costs = (left, up,
+    right) planes, any finite values (the reference's gray only supplies the
+    dimensions); None = forward_costs(luma), derived on the device."""
     g = np.ascontiguousarray(luma, dtype=np.float64)
     if g.ndim != 2 or g.size == 0:
         raise CarveError(Errc.empty_image, "image is empty")
     h, w = g.shape
-    if costs is not None:
-        if any(np.shape(c) != (h, w) for c in costs):
-            raise CarveError(Errc.dimension_mismatch, "forward costs do not match image dimensions")
-        if not all(np.array_equal(a, b) for a, b in zip(costs, forward_costs(g))):
-            _unsupported("dp_seam_forward with costs other than forward_costs(gray)")
     m = np.empty((h, w), np.float64)
     b = np.empty((h, w), np.int32)
     seam = np.empty(h, np.int32)
-    _check(library().carve_cuda_dp_seam_forward(_ptr(g), w, h, _ptr(m), _ptr(b), _ptr(seam)))
+    if costs is not None:
+        if len(costs) != 3 or any(np.shape(c) != (h, w) for c in costs):
+            raise CarveError(Errc.dimension_mismatch, "forward costs do not match image dimensions")
+        cl, cu, cr = (np.ascontiguousarray(c, dtype=np.float64) for c in costs)
+        _check(library().carve_cuda_dp_seam_forward_costs(_ptr(cl), _ptr(cu), _ptr(cr), w, h, _ptr(m), _ptr(b),
+                                                          _ptr(seam)))
+    else:
+        _check(library().carve_cuda_dp_seam_forward(_ptr(g), w, h, _ptr(m), _ptr(b), _ptr(seam)))
     return SeamResult(seam, CostTable(w, h, m, b))
 
 
@@ -623,6 +646,14 @@ def carve_batch(imgs, target_width: int, target_height: int | None = None, devic
     _check(library().carve_cuda_carve_batch(C.cast(ins, C.c_void_p), n, w, h, target_width, th,
                                             C.cast(ous, C.c_void_p), C.cast(devs, C.c_void_p) if devs else None, nd))
     return outs
+
+
+def batch_plan(n: int, width: int, height: int, target_width: int, target_height: int, ndev: int = 1):
+    """(pipelines per device, images per chunk) that carve_batch uses (host logic only)."""
+    p, ch = C.c_int(), C.c_int()
+    _check(library().carve_cuda_batch_plan(n, width, height, target_width, target_height, ndev, C.addressof(p),
+                                           C.addressof(ch)))
+    return p.value, ch.value
 
 
 def carve_device(d_in: int, width: int, height: int, target_width: int, target_height: int, d_out: int,

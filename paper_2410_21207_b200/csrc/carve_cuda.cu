@@ -390,7 +390,10 @@ int device_sm_count() {
 // with few images, which the other carves already do
 thread_local int t_concurrency = 1;
 
-Dp2Plan dp2_plan(int W, int H, bool batch = false, bool fused = false, int nimg = 1) {
+// ring kind of a DP launch: FP64 energy plane, RGBX rows (fused), three FP64 cost planes
+enum RingKind { RING_ENERGY = 0, RING_RGBX = 1, RING_COSTS = 2 };
+
+Dp2Plan dp2_plan(int W, int H, bool batch = false, int ring = RING_ENERGY, int nimg = 1) {
     const int nblk = H > 1 ? (H - 1 + LBLK - 1) / LBLK : 0;
     const int forced = env_int("CARVE_DP_VARIANT", -1);
     const int max_ncl = env_int("CARVE_DP_MAX_NCL", 16);
@@ -403,7 +406,9 @@ Dp2Plan dp2_plan(int W, int H, bool batch = false, bool fused = false, int nimg 
         for (int k : order) {
             const Dp2Variant& v = kDp2Variants[k];
             const int ncl = (W + v.cols() - 1) / v.cols();
-            const size_t smem = fused ? v.smem_fused(nblk, v.D) : v.smem(nblk, v.D);
+            const size_t smem = ring == RING_RGBX    ? v.smem_fused(nblk, v.D)
+                                : ring == RING_COSTS ? v.smem_costs(nblk, v.D)
+                                                     : v.smem(nblk, v.D);
             if (ncl > (pass == 0 ? max_ncl : 16) || smem > size_t(kDpSmemBudget)) continue;
             // columns read past the image edge must stay inside the +inf pad
             if (ncl * v.cols() - W + v.K + 32 * v.C > EPAD_R) continue;
@@ -614,8 +619,6 @@ CarveOpts opts_of(const carve_cuda_config* cfg) {
         o.forward = cfg->forward != 0;
         o.recompute = cfg->recompute != 0;
     }
-    if (o.forward && !o.recompute)
-        fail(CARVE_E_USAGE_ERROR, "forward energy with recompute=false is not supported by the B200 engine");
     return o;
 }
 
@@ -642,14 +645,28 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
     // Forward energy always runs fused (transition costs from the RGBX rows);
     // recompute=false needs the carried energy plane.
     const int fused_env = env_int("CARVE_FUSED", -1);
-    const bool fused = o.forward || (o.recompute && (fused_env >= 0 ? fused_env != 0 : nimg > 1));
+    // forward + recompute=false (carver.hpp:175-184): the forward costs of the phase's
+    // first image are computed once into three planes and then only carved
+    // (drop_columns), as the reference carves its cached ForwardCosts; the DP streams them
+    const bool costs = o.forward && !o.recompute;
+    const bool fused = (o.forward && o.recompute) || (o.recompute && (fused_env >= 0 ? fused_env != 0 : nimg > 1));
+    // cost-plane sets A/B (3 padded planes each, ping-pong per seam)
+    double* cset[2] = {costs ? c.e[0].as<double>() + EPAD_L : nullptr, costs ? c.e[1].as<double>() + EPAD_L : nullptr};
+    const long long cplane = (long long)g.eplane;  // plane stride inside a set
     // `finish`: what the phase's last removal writes (fused with K4, see k_compact_transpose):
     // OUT_PLANE  the transposed RGBX plane for the height phase (rgb[cur ^ 1], pitch_b)
     // OUT_PACKED the final image, transposed back, packed RGB into d_out
     // OUT_ROWS   the final image, packed RGB into d_out
     auto phase = [&](int W0, int H, int ntake, int pitch, int epitch, int seam_base, int stamp_seam0, int finish) {
         if (ntake <= 0) return;
-        if (fused) {
+        int cs = 0;  // current cost-plane set
+        if (costs) {
+            for (int im = 0; im < nimg; ++im) {
+                k_forward_costs_rgbx<<<grid_for((long long)W0 * H, 256), 256, 0, s>>>(
+                    rgb[cur] + im * pis, pitch, W0, H, cset[0] + im * 3 * cplane, epitch, cplane);
+                LAUNCHED("k_forward_costs_rgbx");
+            }
+        } else if (fused) {
             launch_rgb_edges(rgb[cur], pitch, W0, H, nimg, pis, s);
         } else {
             {
@@ -665,17 +682,18 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
             int* seam = d_seams + seam_base + size_t(k) * H;
             unsigned long long* st = d_stamps ? d_stamps + size_t(stamp_seam0 + k) * 4 : nullptr;
             {
-                const Dp2Plan pl = dp2_plan(W, H, nimg > 1, fused, nimg);
+                const Dp2Plan pl = dp2_plan(W, H, nimg > 1, fused ? RING_RGBX : costs ? RING_COSTS : RING_ENERGY, nimg);
                 Dp2Params q{};
-                q.e = e;
+                q.e = costs ? cset[cs] : e;
                 q.epitch = epitch;
+                q.cplane = cplane;
                 q.W = W;
                 q.H = H;
                 q.mbound = c.mbound.as<double>();
                 q.mpitch = g.mpitch;
                 q.seam = seam;
                 q.stamps = st;
-                q.e_istride = eis;
+                q.e_istride = costs ? 3 * cplane : eis;
                 q.mb_istride = g.mb_istride;
                 q.s_istride = (long long)seam_istride;
                 q.st_istride = (long long)sw;
@@ -683,17 +701,26 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
                 q.rpitch = pitch;
                 q.rgb_istride = pis;
                 // fix up the energy around the previous seam (removed from width W + 1)
-                if (k > 0 && !fused && o.recompute) q.prev_seam = seam - H;
+                if (k > 0 && !fused && !costs && o.recompute) q.prev_seam = seam - H;
                 // algorithmic: 8 B FP64 energy read per cell (no direction
                 // plane); fused: 4 B RGBX read per cell
                 Prof pr(c, s, KK_DP, (fused ? 4.0 : 8.0) * W * H * nimg);
                 launch_dp2(c, pl, q, nimg, s, fused, o.forward);
             }
+            if (costs && k + 1 < ntake) {  // drop_columns of the three cost planes (carver.hpp:179-181)
+                for (int im = 0; im < nimg; ++im) {
+                    k_drop_col_planes<<<dim3(unsigned((W + 255) / 256), unsigned(H), 3u), 256, 0, s>>>(
+                        cset[cs] + im * 3 * cplane, cset[cs ^ 1] + im * 3 * cplane, epitch, cplane, W, H,
+                        seam + im * (long long)seam_istride);
+                    LAUNCHED("k_drop_col_planes");
+                }
+                cs ^= 1;
+            }
             CompactParams q{};
             const bool last = (k + 1 == ntake);
             q.rgb_in = q.rgb_out = rgb[cur];
-            q.e_in = q.e_out = (last || fused) ? nullptr : e;  // the final width needs no energy
-            q.rgb_edges = fused && !last;
+            q.e_in = q.e_out = (last || fused || costs) ? nullptr : e;  // the final width needs no energy
+            q.rgb_edges = (fused || costs) && !last;
             q.pitch = pitch;
             q.epitch = epitch;
             q.W = W;
@@ -741,10 +768,12 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
     }
 }
 
-void ensure_carve_buffers(Ctx& c, const CarveGeometry& g, int nimg) {
+void ensure_carve_buffers(Ctx& c, const CarveGeometry& g, int nimg, bool cost_planes = false) {
     c.rgb[0].ensure(g.plane * 4 * nimg);
     if (g.th != g.h) c.rgb[1].ensure(g.plane * 4 * nimg);
-    c.e[0].ensure(g.eplane * 8 * nimg);
+    // cost_planes: two sets of three FP64 cost planes (forward + recompute=false)
+    c.e[0].ensure(g.eplane * 8 * nimg * (cost_planes ? 3 : 1));
+    if (cost_planes) c.e[1].ensure(g.eplane * 8 * nimg * 3);
     c.mbound.ensure(size_t(g.mb_istride) * 8 * nimg);
 }
 
@@ -825,7 +854,7 @@ void record_device(Ctx& c, const uint8_t* d_in, int w, int h, int count, int* d_
                    CarveOpts o = {}) {
     if (count <= 0) return;
     const CarveGeometry g = geometry(w, h, w - count, h);
-    ensure_carve_buffers(c, g, 1);
+    ensure_carve_buffers(c, g, 1, o.forward && !o.recompute);
     int* d_log = static_cast<int*>(c.seams.ensure(std::max<size_t>(g.seam_ints, 1) * 4));
     uint8_t* d_scratch = static_cast<uint8_t*>(c.scratch_a.ensure(size_t(w - count) * h * 3));
     run_carve(c, d_in, d_scratch, 1, g, d_log, g.seam_ints, d_st, c.stream, o);
@@ -853,7 +882,7 @@ void carve_one_host(Ctx& c, const uint8_t* rgb, int w, int h, int tw, int th, ui
     const size_t in_bytes = size_t(w) * h * 3, out_bytes = size_t(tw) * th * 3;
     uint8_t* d_in = static_cast<uint8_t*>(c.packed_in.ensure(in_bytes));
     uint8_t* d_out = static_cast<uint8_t*>(c.packed_out.ensure(out_bytes));
-    ensure_carve_buffers(c, g, 1);
+    ensure_carve_buffers(c, g, 1, o.forward && !o.recompute);
     int* d_seams = static_cast<int*>(c.seams.ensure(std::max<size_t>(g.seam_ints, 1) * 4));
     unsigned long long* d_st = nullptr;
     if (timings) {
@@ -872,6 +901,100 @@ void carve_one_host(Ctx& c, const uint8_t* rgb, int w, int h, int tw, int th, ui
     }
     sync(c);
     if (timings) stamps_to_timings(st, g.nseams, timings);
+}
+
+// ---------------------------------------------------------------------------
+// stream / context plumbing for the asynchronous and batch entry points
+
+// Fork `into` from the caller's stream `s` (an event), join it back at the end.
+// RAII: the fork event is destroyed on every path.
+struct StreamFork {
+    cudaStream_t s;
+    cudaStream_t into = nullptr;
+    cudaEvent_t fork = nullptr;
+    explicit StreamFork(cudaStream_t s_) : s(s_) {
+        ck(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming), "event create");
+        ck(cudaEventRecord(fork, s), "record fork");
+    }
+    StreamFork(cudaStream_t s_, cudaStream_t into_) : StreamFork(s_) {
+        into = into_;
+        fork_into(into);
+    }
+    void fork_into(cudaStream_t x) { ck(cudaStreamWaitEvent(x, fork, 0), "wait fork"); }
+    void join_from(cudaStream_t x) {
+        cudaEvent_t j;
+        ck(cudaEventCreateWithFlags(&j, cudaEventDisableTiming), "event create");
+        const cudaError_t e1 = cudaEventRecord(j, x);
+        const cudaError_t e2 = e1 == cudaSuccess ? cudaStreamWaitEvent(s, j, 0) : e1;
+        cudaEventDestroy(j);
+        ck(e2, "join");
+    }
+    void join() { join_from(into); }
+    ~StreamFork() {
+        if (fork) cudaEventDestroy(fork);
+    }
+    StreamFork(const StreamFork&) = delete;
+    StreamFork& operator=(const StreamFork&) = delete;
+};
+
+// The (device, pipeline) slot contexts 0..P-1, locked for the scope (in index
+// order, so concurrent callers cannot deadlock) and created on first use.
+// `lane`: the position of the device in a batch call's device list, so a device
+// listed twice gets two independent sets of contexts (two concurrent workers).
+struct SlotSet {
+    int dev;
+    std::vector<std::unique_lock<std::mutex>> locks;
+    std::vector<Ctx*> ctxs;
+    SlotSet(int dev_, int P, int lane = 0) : dev(dev_) {
+        for (int q = 0; q < P; ++q) {
+            PipeSlot& slot = pipe_slot(dev, lane * CARVE_MAX_PIPELINES + q);
+            locks.emplace_back(slot.m);
+            if (!slot.c) {
+                slot.c = std::make_unique<Ctx>(dev);
+                init_kernel_attributes(*slot.c);
+            }
+            ctxs.push_back(slot.c.get());
+        }
+    }
+    // make slot q the calling thread's current context (ctx() returns it)
+    Ctx& use(int q) {
+        t_ctx_override = ctxs[q];
+        return ctx();
+    }
+    ~SlotSet() { t_ctx_override = nullptr; }
+};
+
+// concurrent carves the DP shape choice counts (dp2_plan), for one scope
+struct ConcurrencyScope {
+    explicit ConcurrencyScope(int p) { t_concurrency = p; }
+    ~ConcurrencyScope() { t_concurrency = 1; }
+};
+
+// Host batch pipeline shape: P pipelines per device, chunks of `chunk` images.
+// CARVE_PIPELINES / CARVE_PIPE_CHUNK override (read per call).
+struct BatchPlan {
+    int pipes, chunk;
+};
+
+BatchPlan batch_plan(int n, int ndev, const CarveGeometry& g) {
+    const int share = (n + ndev - 1) / ndev;
+    // measured on B200 (tools/share_sweep.py --grid, profiles/r02_share_grid.txt): 128-image
+    // chunks on up to 4 pipelines for shares >= 256 (1024: 3.42K e2e images/s vs 3.34K with
+    // 2 x 256; 512: 3.25K vs 2.90K), two 64-image chunks for a 128-image share (2.32K vs
+    // 2.12K); 32-image chunks lose (a 32-image carve cannot fill the SMs)
+    int P = std::max(1, std::min(CARVE_MAX_PIPELINES, env_int("CARVE_PIPELINES", 4)));
+    // per-image device footprint (planes, energy, M rows, packed in/out double
+    // buffers, seam log): the chunks in flight stay well inside 180 GB of HBM
+    const size_t in_bytes = size_t(g.w) * g.h * 3, out_bytes = size_t(g.tw) * g.th * 3;
+    const size_t per_img = g.plane * 8 + g.eplane * 8 + size_t(g.mb_istride) * 8 + 2 * (in_bytes + out_bytes) +
+                           g.seam_ints * 4;
+    const int cap = int(std::max<size_t>(1, (size_t(48) << 30) / (per_img * size_t(P))));
+    int ch = env_int("CARVE_PIPE_CHUNK", 0);
+    if (ch <= 0) ch = std::max(16, std::min(128, (share + 1) / 2));
+    ch = std::max(1, std::min({ch, cap, share}));
+    const int nchunks = (share + ch - 1) / ch;
+    P = std::max(1, std::min(P, nchunks));
+    return BatchPlan{P, ch};
 }
 
 }  // namespace
@@ -1083,6 +1206,27 @@ carve_status carve_cuda_dp_profile(const double* e, int w, int h, long long* cou
     });
 }
 
+carve_status carve_cuda_insert_columns_rgb(const uint8_t* rgb, int w, int h, const int32_t* cols, int n,
+                                           uint8_t* out) {
+    return guarded([&] {
+        // detail::insert_columns (carver.hpp:118-132): no connectivity requirement;
+        // columns outside [0, w) would be undefined behaviour in the reference
+        if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "PixelGrid dimensions must be >= 1");
+        if (n != h) fail(CARVE_E_INVALID_SEAM, "one column per row is required");
+        for (int i = 0; i < n; ++i)
+            if (cols[i] < 0 || cols[i] >= w) fail(CARVE_E_INVALID_SEAM, "column out of range");
+        Ctx& c = ctx();
+        uint8_t* d_in = static_cast<uint8_t*>(c.packed_in.ensure(size_t(w) * h * 3));
+        uint8_t* d_out = static_cast<uint8_t*>(c.packed_out.ensure(size_t(w + 1) * h * 3));
+        int* ds = static_cast<int*>(c.rec.ensure(size_t(h) * 4));
+        ck(cudaMemcpyAsync(d_in, rgb, size_t(w) * h * 3, cudaMemcpyHostToDevice, c.stream), "H2D");
+        ck(cudaMemcpyAsync(ds, cols, size_t(h) * 4, cudaMemcpyHostToDevice, c.stream), "H2D cols");
+        launch_expand_rows(d_in, w, h, ds, 1, h, d_out, c.stream);
+        ck(cudaMemcpyAsync(out, d_out, size_t(w + 1) * h * 3, cudaMemcpyDeviceToHost, c.stream), "D2H");
+        sync(c);
+    });
+}
+
 carve_status carve_cuda_insert_seam_rgb(const uint8_t* rgb, int w, int h, const int32_t* seam, int n, uint8_t* out) {
     return guarded([&] {
         validate_seam_host(seam, n, w, h);  // carver.hpp:138
@@ -1221,7 +1365,7 @@ carve_status carve_cuda_forward_costs(const double* luma, int w, int h, double* 
         const size_t n = size_t(w) * h;
         double* l = static_cast<double*>(c.scratch_a.ensure(n * 8 * 4));
         ck(cudaMemcpyAsync(l, luma, n * 8, cudaMemcpyHostToDevice, c.stream), "H2D luma");
-        k_forward_costs<<<grid_for((long long)n, 256), 256, 0, c.stream>>>(l, w, h, l + n, l + 2 * n, l + 3 * n);
+        k_forward_costs<<<grid_for((long long)n, 256), 256, 0, c.stream>>>(l, w, h, l + n, l + 2 * n, l + 3 * n, w);
         LAUNCHED("k_forward_costs");
         ck(cudaMemcpyAsync(left, l + n, n * 8, cudaMemcpyDeviceToHost, c.stream), "D2H left");
         ck(cudaMemcpyAsync(up, l + 2 * n, n * 8, cudaMemcpyDeviceToHost, c.stream), "D2H up");
@@ -1230,49 +1374,129 @@ carve_status carve_cuda_forward_costs(const double* luma, int w, int h, double* 
     });
 }
 
+}  // extern "C"
+namespace {
+// dp_seam_forward (solvers.hpp:294-326) on three padded device cost planes
+// (cost_left at d_costs, cost_up at + cplane, cost_right at + 2*cplane)
+void dp_forward_on_planes(Ctx& c, double* d_costs, int epitch, long long cplane, int w, int h, double* m_out,
+                          int32_t* b_out, int32_t* seam_out) {
+    const Dp2Plan pl = dp2_plan(w, h, false, RING_COSTS);
+    const int pitch = int(round_up(w, 32));
+    double* mb = static_cast<double*>(c.mbound.ensure(size_t(pl.nblk + 1) * pitch * 8));
+    int* dseam = static_cast<int*>(c.seams.ensure(size_t(h) * 4));
+    double* dm = nullptr;
+    int* db = nullptr;
+    if (m_out) {
+        dm = static_cast<double*>(c.scratch_a.ensure(size_t(w) * h * 8));
+        db = static_cast<int*>(c.scratch_b.ensure(size_t(w) * h * 4));
+    }
+    Dp2Params p{};
+    p.e = d_costs;
+    p.cplane = cplane;
+    p.epitch = epitch;
+    p.W = w;
+    p.H = h;
+    p.mbound = mb;
+    p.mpitch = pitch;
+    p.seam = dseam;
+    p.m_out = dm;
+    p.b_out = db;
+    launch_dp2(c, pl, p, 1, c.stream, false, true);
+    ck(cudaMemcpyAsync(seam_out, dseam, size_t(h) * 4, cudaMemcpyDeviceToHost, c.stream), "D2H seam");
+    if (m_out) {
+        ck(cudaMemcpyAsync(m_out, dm, size_t(w) * h * 8, cudaMemcpyDeviceToHost, c.stream), "D2H m");
+        ck(cudaMemcpyAsync(b_out, db, size_t(w) * h * 4, cudaMemcpyDeviceToHost, c.stream), "D2H b");
+    }
+    sync(c);
+}
+
+// three padded FP64 cost planes in c.e[0] (rows of epitch doubles, EPAD_B spare rows)
+double* cost_planes(Ctx& c, int w, int h, int& epitch, long long& cplane) {
+    epitch = padded_epitch(w);
+    cplane = (long long)epitch * (h + EPAD_B);
+    return static_cast<double*>(c.e[0].ensure(size_t(cplane) * 3 * 8)) + EPAD_L;
+}
+}  // namespace
+extern "C" {
+
 carve_status carve_cuda_dp_seam_forward(const double* luma, int w, int h, double* m_out, int32_t* b_out,
                                         int32_t* seam_out) {
     return guarded([&] {
         if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "image is empty");
         if ((m_out == nullptr) != (b_out == nullptr)) fail(CARVE_E_USAGE_ERROR, "m_out and b_out go together");
         Ctx& c = ctx();
-        const Dp2Plan pl = dp2_plan(w, h);
-        const int pitch = int(round_up(w, 32));
-        const int epitch = padded_epitch(w);
-        // the luma plane streams through the DP like an energy plane; its columns
-        // -1 and w replicate the edge columns (at_clamped, raster.hpp:54-58)
-        double* dl = static_cast<double*>(c.e[0].ensure(size_t(epitch) * (h + EPAD_B) * 8)) + EPAD_L;
-        double* mb = static_cast<double*>(c.mbound.ensure(size_t(pl.nblk + 1) * pitch * 8));
-        int* dseam = static_cast<int*>(c.seams.ensure(size_t(h) * 4));
-        double* dm = nullptr;
-        int* db = nullptr;
-        if (m_out) {
-            dm = static_cast<double*>(c.scratch_a.ensure(size_t(w) * h * 8));
-            db = static_cast<int*>(c.scratch_b.ensure(size_t(w) * h * 4));
-        }
-        ck(cudaMemcpy2DAsync(dl, size_t(epitch) * 8, luma, size_t(w) * 8, size_t(w) * 8, h, cudaMemcpyHostToDevice,
-                             c.stream),
-           "H2D luma");
-        k_edge_replicas_f64<<<grid_for(h, 256), 256, 0, c.stream>>>(dl, epitch, w, h);
-        LAUNCHED("k_edge_replicas_f64");
-        Dp2Params p{};
-        p.e = dl;
-        p.epitch = epitch;
-        p.W = w;
-        p.H = h;
-        p.mbound = mb;
-        p.mpitch = pitch;
-        p.seam = dseam;
-        p.m_out = dm;
-        p.b_out = db;
-        launch_dp2(c, pl, p, 1, c.stream, false, true);
-        ck(cudaMemcpyAsync(seam_out, dseam, size_t(h) * 4, cudaMemcpyDeviceToHost, c.stream), "D2H seam");
-        if (m_out) {
-            ck(cudaMemcpyAsync(m_out, dm, size_t(w) * h * 8, cudaMemcpyDeviceToHost, c.stream), "D2H m");
-            ck(cudaMemcpyAsync(b_out, db, size_t(w) * h * 4, cudaMemcpyDeviceToHost, c.stream), "D2H b");
-        }
-        sync(c);
+        int epitch;
+        long long cplane;
+        double* d = cost_planes(c, w, h, epitch, cplane);
+        // forward_costs(gray) on the device, straight into the DP's padded planes
+        double* dl = static_cast<double*>(c.scratch_b.ensure(size_t(w) * h * 8));
+        ck(cudaMemcpyAsync(dl, luma, size_t(w) * h * 8, cudaMemcpyHostToDevice, c.stream), "H2D luma");
+        k_forward_costs<<<grid_for((long long)w * h, 256), 256, 0, c.stream>>>(dl, w, h, d, d + cplane,
+                                                                              d + 2 * cplane, epitch);
+        LAUNCHED("k_forward_costs");
+        dp_forward_on_planes(c, d, epitch, cplane, w, h, m_out, b_out, seam_out);
     });
+}
+
+carve_status carve_cuda_dp_seam_forward_costs(const double* left, const double* up, const double* right, int w,
+                                              int h, double* m_out, int32_t* b_out, int32_t* seam_out) {
+    return guarded([&] {
+        if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "image is empty");
+        if ((m_out == nullptr) != (b_out == nullptr)) fail(CARVE_E_USAGE_ERROR, "m_out and b_out go together");
+        // the device scan compares finite candidates (out-of-image neighbours are +inf);
+        // the reference's best = +inf start differs from it only for non-finite costs
+        const size_t n = size_t(w) * h;
+        for (const double* pl : {left, up, right})
+            for (size_t k = 0; k < n; ++k)
+                if (!std::isfinite(pl[k]))
+                    fail(CARVE_E_USAGE_ERROR, "non-finite forward costs are not supported by the B200 engine");
+        Ctx& c = ctx();
+        int epitch;
+        long long cplane;
+        double* d = cost_planes(c, w, h, epitch, cplane);
+        const double* src[3] = {left, up, right};
+        for (int k = 0; k < 3; ++k)
+            ck(cudaMemcpy2DAsync(d + k * cplane, size_t(epitch) * 8, src[k], size_t(w) * 8, size_t(w) * 8, h,
+                                 cudaMemcpyHostToDevice, c.stream),
+               "H2D costs");
+        dp_forward_on_planes(c, d, epitch, cplane, w, h, m_out, b_out, seam_out);
+    });
+}
+
+}  // extern "C"
+namespace {
+// remove_seam on a scalar plane (carver.hpp:84-112): the reference does not
+// validate these overloads; out-of-range columns would be undefined behaviour
+// there, so they are rejected here with invalid_seam
+template <typename T>
+void drop_columns_device(const T* in, int w, int h, const int32_t* seam, int n, T* out) {
+    if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "plane dimensions must be >= 1");
+    if (n != h) fail(CARVE_E_INVALID_SEAM, "seam length does not match the plane height");
+    for (int i = 0; i < n; ++i)
+        if (seam[i] < 0 || seam[i] >= w) fail(CARVE_E_INVALID_SEAM, "seam column out of range");
+    Ctx& c = ctx();
+    const size_t nin = size_t(w) * h, nout = size_t(w - 1) * h;
+    T* d_in = static_cast<T*>(c.scratch_a.ensure(nin * sizeof(T)));
+    T* d_out = static_cast<T*>(c.scratch_b.ensure(std::max<size_t>(nout, 1) * sizeof(T)));
+    int* ds = static_cast<int*>(c.seams.ensure(size_t(h) * 4));
+    ck(cudaMemcpyAsync(d_in, in, nin * sizeof(T), cudaMemcpyHostToDevice, c.stream), "H2D plane");
+    ck(cudaMemcpyAsync(ds, seam, size_t(h) * 4, cudaMemcpyHostToDevice, c.stream), "H2D seam");
+    if (nout) {
+        k_drop_columns<T><<<grid_for((long long)nout, 256), 256, 0, c.stream>>>(d_in, w, h, ds, d_out);
+        LAUNCHED("k_drop_columns");
+        ck(cudaMemcpyAsync(out, d_out, nout * sizeof(T), cudaMemcpyDeviceToHost, c.stream), "D2H plane");
+    }
+    sync(c);
+}
+}  // namespace
+extern "C" {
+
+carve_status carve_cuda_remove_seam_f64(const double* in, int w, int h, const int32_t* seam, int n, double* out) {
+    return guarded([&] { drop_columns_device<double>(in, w, h, seam, n, out); });
+}
+
+carve_status carve_cuda_remove_seam_u8(const uint8_t* in, int w, int h, const int32_t* seam, int n, uint8_t* out) {
+    return guarded([&] { drop_columns_device<uint8_t>(in, w, h, seam, n, out); });
 }
 
 carve_status carve_cuda_mask_from_rgb(const uint8_t* rgb, int w, int h, uint8_t* flags) {
@@ -1443,8 +1667,12 @@ carve_status carve_cuda_carve_device(const uint8_t* d_rgb, int w, int h, int tar
         const CarveGeometry g = geometry(w, h, target_w, target_h);
         ensure_carve_buffers(c, g, 1);
         int* seams = d_seams ? d_seams : static_cast<int*>(c.seams.ensure(std::max<size_t>(g.seam_ints, 1) * 4));
-        cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL = the legacy default stream
-        run_carve(c, d_rgb, d_out, 1, g, seams, g.seam_ints, nullptr, s);
+        // the context's scratch is ordered on its own stream: forked from and joined back
+        // into the caller's stream (NULL = the legacy default stream), so a later call on
+        // any stream of this thread cannot overwrite scratch this carve still uses
+        StreamFork f(static_cast<cudaStream_t>(stream), c.stream);
+        run_carve(c, d_rgb, d_out, 1, g, seams, g.seam_ints, nullptr, c.stream);
+        f.join();
     });
 }
 
@@ -1456,61 +1684,59 @@ carve_status carve_cuda_carve_batch_device(const uint8_t* d_rgb, int n, int w, i
         Ctx& c = ctx();
         const CarveGeometry g = geometry(w, h, target_w, target_h);
         cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL = the legacy default stream
-        // Split into P concurrent sub-batches (CARVE_DEVICE_SPLIT, forked from and joined
-        // back into `s`), each on its own (device, pipeline) context, so one sub-batch's
-        // per-seam launches fill the other's wave tails. Per-kernel event profiling
-        // (c.prof) keeps one stream so its launch timings stay serial.
+        // Split into P concurrent sub-batches (CARVE_DEVICE_SPLIT, of at least
+        // CARVE_DEVICE_SPLIT_MIN images), each on its own (device, pipeline) context and
+        // stream, forked from and joined back into `s`, so one sub-batch's per-seam
+        // launches fill the other's wave tails. Per-kernel event profiling (c.prof) keeps
+        // the calling thread's context (one stream, serial launch timings).
         const int want = std::max(1, std::min(CARVE_MAX_PIPELINES, env_int("CARVE_DEVICE_SPLIT", 2)));
-        const int P = c.prof ? 1 : std::max(1, std::min(want, n / 256));  // >= 256 images per sub-batch
-        if (P == 1) {
+        // measured (profiles/r02_share_grid.txt): 128 images as 2 x 64 2.70K vs 2.61K images/s;
+        // 256 as 2 x 128 or 1 x 256 the same
+        const int min_sub = std::max(1, env_int("CARVE_DEVICE_SPLIT_MIN", 64));
+        const int P = c.prof ? 1 : std::max(1, std::min(want, n / min_sub));
+        const size_t in_bytes = size_t(w) * h * 3, out_bytes = size_t(target_w) * target_h * 3;
+        if (c.prof) {
             ensure_carve_buffers(c, g, n);
             int* seams = static_cast<int*>(c.seams.ensure(std::max<size_t>(g.seam_ints, 1) * 4 * n));
-            run_carve(c, d_rgb, d_out, n, g, seams, std::max<size_t>(g.seam_ints, 1), nullptr, s);
+            StreamFork f(s, c.stream);
+            run_carve(c, d_rgb, d_out, n, g, seams, std::max<size_t>(g.seam_ints, 1), nullptr, c.stream);
+            f.join();
             return;
         }
-        const size_t in_bytes = size_t(w) * h * 3, out_bytes = size_t(target_w) * target_h * 3;
-        const int dev = c.device;
-        cudaEvent_t fork;
-        ck(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming), "event create");
-        ck(cudaEventRecord(fork, s), "record fork");
-        std::vector<std::unique_lock<std::mutex>> locks;
-        struct Reset {
-            ~Reset() {
-                t_ctx_override = nullptr;
-                t_concurrency = 1;
-            }
-        } reset;
-        t_concurrency = P;
+        // every slot's buffers are ensured before any work is enqueued, so a failure
+        // (e.g. an allocation) leaves nothing in flight
+        SlotSet slots(c.device, P);
         for (int q = 0; q < P; ++q) {
             const int a = int((long long)n * q / P), b = int((long long)n * (q + 1) / P);
-            PipeSlot& slot = pipe_slot(dev, q);
-            locks.emplace_back(slot.m);
-            if (!slot.c) {
-                slot.c = std::make_unique<Ctx>(dev);
-                init_kernel_attributes(*slot.c);
-            }
-            t_ctx_override = slot.c.get();
-            Ctx& cq = ctx();
+            Ctx& cq = slots.use(q);
             ensure_carve_buffers(cq, g, b - a);
-            int* seams = static_cast<int*>(cq.seams.ensure(std::max<size_t>(g.seam_ints, 1) * 4 * (b - a)));
-            ck(cudaStreamWaitEvent(cq.stream, fork, 0), "wait fork");
-            run_carve(cq, d_rgb + in_bytes * a, d_out + out_bytes * a, b - a, g, seams,
-                      std::max<size_t>(g.seam_ints, 1), nullptr, cq.stream);
-            cudaEvent_t join;
-            ck(cudaEventCreateWithFlags(&join, cudaEventDisableTiming), "event create");
-            ck(cudaEventRecord(join, cq.stream), "record join");
-            ck(cudaStreamWaitEvent(s, join, 0), "wait join");
-            ck(cudaEventDestroy(join), "event destroy");
+            cq.seams.ensure(std::max<size_t>(g.seam_ints, 1) * 4 * (b - a));
         }
-        ck(cudaEventDestroy(fork), "event destroy");
+        ConcurrencyScope cs(P);
+        StreamFork f(s);
+        for (int q = 0; q < P; ++q) {
+            const int a = int((long long)n * q / P), b = int((long long)n * (q + 1) / P);
+            Ctx& cq = slots.use(q);
+            f.fork_into(cq.stream);
+            run_carve(cq, d_rgb + in_bytes * a, d_out + out_bytes * a, b - a, g, cq.seams.as<int>(),
+                      std::max<size_t>(g.seam_ints, 1), nullptr, cq.stream);
+            f.join_from(cq.stream);
+        }
     });
 }
 
-// images per pipelined chunk (measured: 256-image launches run at ~95% of the
-// 1024-image throughput, tools/sweep_batch.py); CARVE_PIPE_CHUNK overrides
-int pipe_chunk() {
-    static const int v = std::max(16, env_int("CARVE_PIPE_CHUNK", 256));
-    return v;
+carve_status carve_cuda_batch_plan(int n, int w, int h, int target_w, int target_h, int ndev, int* pipes,
+                                   int* chunk) {
+    return guarded([&] {
+        if (n < 1) fail(CARVE_E_EMPTY_INPUT, "empty batch");
+        if (ndev < 1) fail(CARVE_E_USAGE_ERROR, "ndev must be >= 1");
+        if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "PixelGrid dimensions must be >= 1");
+        if (target_w < 1 || target_w > w || target_h < 1 || target_h > h)
+            fail(CARVE_E_INVALID_TARGET, "target must be in [1, size]");
+        const BatchPlan p = batch_plan(n, ndev, geometry(w, h, target_w, target_h));
+        *pipes = p.pipes;
+        *chunk = p.chunk;
+    });
 }
 
 carve_status carve_cuda_carve_batch(const uint8_t* const* rgb, int n, int w, int h, int target_w, int target_h,
@@ -1527,115 +1753,72 @@ carve_status carve_cuda_carve_batch(const uint8_t* const* rgb, int n, int w, int
             if (devs[k] < 0 || devs[k] >= avail) fail(CARVE_E_CUDA, "invalid device index");
         }
         const CarveGeometry g = geometry(w, h, target_w, target_h);
-        const int kPipeChunk = pipe_chunk();
+        const BatchPlan plan = batch_plan(n, ndev, g);
         const size_t in_bytes = size_t(w) * h * 3, out_bytes = size_t(target_w) * target_h * 3;
-        // per-image device footprint -> chunk size (keep well inside 180 GB HBM)
-        const size_t per_img = g.plane * 8 + g.eplane * 8 + size_t(g.mb_istride) * 8 + in_bytes + out_bytes +
-                               g.seam_ints * 4;
-        const int chunk_cap = int(std::max<size_t>(1, (size_t(48) << 30) / per_img));
+        // SURVEY.md §8e work queue: chunks of whole images are claimed from one atomic
+        // counter by one host thread per listed device, so a faster (or less loaded)
+        // device takes more chunks; there is no inter-device communication.
+        std::atomic<int> next{0};
         std::vector<int> status(ndev, CARVE_OK);
         std::vector<std::string> msgs(ndev);
-        // Per device: one host thread per pipeline. A device with at least 4 chunks
-        // runs two pipelines on halves of its share (each thread has its own context:
-        // stream, buffers), so one pipeline's launches fill the other's wave tails.
-        auto worker = [&](int k, int pipe, int npipes, int lo, int hi, int& st_out, std::string& msg_out) {
-            if (lo >= hi) return;
-            t_device = devs[k];
-            PipeSlot& slot = pipe_slot(devs[k], pipe);
-            std::lock_guard<std::mutex> lk(slot.m);
-            st_out = guarded([&] {
-                if (!slot.c) {
-                    slot.c = std::make_unique<Ctx>(devs[k]);
-                    init_kernel_attributes(*slot.c);
-                }
-                t_ctx_override = slot.c.get();
-                t_concurrency = npipes;
-                struct Reset {
-                    ~Reset() {
-                        t_ctx_override = nullptr;
-                        t_concurrency = 1;
-                    }
-                } reset;
-                Ctx& c = ctx();
-                if (hi - lo >= 2 * kPipeChunk && chunk_cap >= kPipeChunk) {
-                    // Copy/compute pipeline: chunk t+1 uploads and chunk t-1 downloads on the
-                    // copy engines while chunk t carves (double-buffered packed images)
-                    c.ensure_pipeline();
-                    enum { H2D = 0, COMP = 1, D2H = 2 };
-                    int t = 0;
-                    for (int b0 = lo; b0 < hi; b0 += kPipeChunk, ++t) {
-                        const int m = std::min(kPipeChunk, hi - b0), b = t & 1;
-                        uint8_t* d_in = static_cast<uint8_t*>(c.pin_in[b].ensure(in_bytes * kPipeChunk));
-                        uint8_t* d_out = static_cast<uint8_t*>(c.pin_out[b].ensure(out_bytes * kPipeChunk));
-                        if (t == 0) ensure_carve_buffers(c, g, kPipeChunk);
-                        int* seams =
-                            static_cast<int*>(c.seams.ensure(std::max<size_t>(g.seam_ints, 1) * 4 * kPipeChunk));
-                        if (t >= 2) ck(cudaStreamWaitEvent(c.h2d, c.pipe_ev[COMP][b], 0), "wait comp");
-                        for (int q = 0; q < m; ++q)
-                            ck(cudaMemcpyAsync(d_in + in_bytes * q, rgb[b0 + q], in_bytes, cudaMemcpyHostToDevice,
-                                               c.h2d),
-                               "H2D");
-                        ck(cudaEventRecord(c.pipe_ev[H2D][b], c.h2d), "record h2d");
-                        ck(cudaStreamWaitEvent(c.stream, c.pipe_ev[H2D][b], 0), "wait h2d");
-                        if (t >= 2) ck(cudaStreamWaitEvent(c.stream, c.pipe_ev[D2H][b], 0), "wait d2h");
-                        run_carve(c, d_in, d_out, m, g, seams, std::max<size_t>(g.seam_ints, 1), nullptr, c.stream);
-                        ck(cudaEventRecord(c.pipe_ev[COMP][b], c.stream), "record comp");
-                        ck(cudaStreamWaitEvent(c.d2h, c.pipe_ev[COMP][b], 0), "wait comp");
-                        for (int q = 0; q < m; ++q)
-                            ck(cudaMemcpyAsync(rgb_out[b0 + q], d_out + out_bytes * q, out_bytes,
-                                               cudaMemcpyDeviceToHost, c.d2h),
-                               "D2H");
-                        ck(cudaEventRecord(c.pipe_ev[D2H][b], c.d2h), "record d2h");
-                    }
-                    ck(cudaStreamSynchronize(c.d2h), "sync d2h");
-                    sync(c);
-                    return;
-                }
-                for (int b0 = lo; b0 < hi; b0 += chunk_cap) {
-                    const int m = std::min(chunk_cap, hi - b0);
-                    uint8_t* d_in = static_cast<uint8_t*>(c.packed_in.ensure(in_bytes * m));
-                    uint8_t* d_out = static_cast<uint8_t*>(c.packed_out.ensure(out_bytes * m));
-                    ensure_carve_buffers(c, g, m);
-                    int* seams = static_cast<int*>(c.seams.ensure(std::max<size_t>(g.seam_ints, 1) * 4 * m));
-                    for (int q = 0; q < m; ++q)
-                        ck(cudaMemcpyAsync(d_in + in_bytes * q, rgb[b0 + q], in_bytes, cudaMemcpyHostToDevice,
-                                           c.stream),
-                           "H2D");
-                    run_carve(c, d_in, d_out, m, g, seams, std::max<size_t>(g.seam_ints, 1), nullptr, c.stream);
-                    for (int q = 0; q < m; ++q)
-                        ck(cudaMemcpyAsync(rgb_out[b0 + q], d_out + out_bytes * q, out_bytes, cudaMemcpyDeviceToHost,
-                                           c.stream),
-                           "D2H");
-                    sync(c);
-                }
-            });
-            if (st_out) msg_out = t_err;
-        };
-        const int pipes = std::max(1, std::min(CARVE_MAX_PIPELINES, env_int("CARVE_PIPELINES", 2)));
-        std::vector<std::vector<int>> pst(ndev, std::vector<int>(CARVE_MAX_PIPELINES, CARVE_OK));
-        std::vector<std::vector<std::string>> pmsg(ndev, std::vector<std::string>(CARVE_MAX_PIPELINES));
         auto device_worker = [&](int k) {
-            const int lo = int((long long)n * k / ndev), hi = int((long long)n * (k + 1) / ndev);
-            // P pipelines on chunk-aligned parts of the share, each needing >= 2 chunks
-            const int nchunks = (hi - lo + kPipeChunk - 1) / kPipeChunk;
-            const int P = (chunk_cap >= kPipeChunk) ? std::max(1, std::min(pipes, nchunks / 2)) : 1;
-            if (P > 1) {
-                std::vector<std::thread> th;
-                for (int q = 1; q < P; ++q) {
-                    const int a = lo + int((long long)nchunks * q / P) * kPipeChunk;
-                    const int b = std::min(hi, lo + int((long long)nchunks * (q + 1) / P) * kPipeChunk);
-                    th.emplace_back([&, k, q, a, b, P] { worker(k, q, P, a, b, pst[k][q], pmsg[k][q]); });
-                }
-                worker(k, 0, P, lo, std::min(hi, lo + int((long long)nchunks / P) * kPipeChunk), status[k], msgs[k]);
-                for (auto& t : th) t.join();
-                for (int q = 1; q < P && !status[k]; ++q)
-                    if (pst[k][q]) {
-                        status[k] = pst[k][q];
-                        msgs[k] = pmsg[k][q];
+            t_device = devs[k];
+            status[k] = guarded([&] {
+                // P pipelines per device, each a (device, pipeline) context with its own
+                // compute stream and buffers; the copies of all of them go through one H2D
+                // and one D2H stream (slot 0's), in claim order, so the first chunk's
+                // upload does not share PCIe bandwidth with later ones
+                const int P = plan.pipes, ch = plan.chunk;
+                SlotSet slots(devs[k], P, k);
+                Ctx& c0 = slots.use(0);
+                c0.ensure_pipeline();
+                for (int q = 0; q < P; ++q) {  // allocate everything before enqueuing any work
+                    Ctx& cq = slots.use(q);
+                    cq.ensure_pipeline();
+                    ensure_carve_buffers(cq, g, ch);
+                    cq.seams.ensure(std::max<size_t>(g.seam_ints, 1) * 4 * ch);
+                    for (int b = 0; b < 2; ++b) {
+                        cq.pin_in[b].ensure(in_bytes * ch);
+                        cq.pin_out[b].ensure(out_bytes * ch);
                     }
-            } else {
-                worker(k, 0, 1, lo, hi, status[k], msgs[k]);
-            }
+                }
+                enum { H2D = 0, COMP = 1, D2H = 2 };
+                struct Reset {
+                    ~Reset() { t_concurrency = 1; }
+                } reset;
+                for (int t = 0;; ++t) {
+                    const int b0 = next.fetch_add(ch);
+                    if (b0 >= n) break;
+                    const int m = std::min(ch, n - b0), q = t % P, b = (t / P) & 1;
+                    Ctx& cq = slots.use(q);
+                    // flow control: at most 2P chunks in flight per device; the buffer pair
+                    // (q, b) is reused only after its previous chunk has fully drained
+                    if (t >= 2 * P) ck(cudaEventSynchronize(cq.pipe_ev[D2H][b]), "wait d2h");
+                    uint8_t* d_in = cq.pin_in[b].as<uint8_t>();
+                    uint8_t* d_out = cq.pin_out[b].as<uint8_t>();
+                    for (int i = 0; i < m; ++i)
+                        ck(cudaMemcpyAsync(d_in + in_bytes * i, rgb[b0 + i], in_bytes, cudaMemcpyHostToDevice,
+                                           c0.h2d),
+                           "H2D");
+                    ck(cudaEventRecord(cq.pipe_ev[H2D][b], c0.h2d), "record h2d");
+                    ck(cudaStreamWaitEvent(cq.stream, cq.pipe_ev[H2D][b], 0), "wait h2d");
+                    // the DP shape counts the other pipelines' carves (they fill the SMs
+                    // alongside this one) unless the whole share is this one chunk
+                    t_concurrency = (t == 0 && b0 + m >= n) ? 1 : P;
+                    run_carve(cq, d_in, d_out, m, g, cq.seams.as<int>(), std::max<size_t>(g.seam_ints, 1), nullptr,
+                              cq.stream);
+                    ck(cudaEventRecord(cq.pipe_ev[COMP][b], cq.stream), "record comp");
+                    ck(cudaStreamWaitEvent(c0.d2h, cq.pipe_ev[COMP][b], 0), "wait comp");
+                    for (int i = 0; i < m; ++i)
+                        ck(cudaMemcpyAsync(rgb_out[b0 + i], d_out + out_bytes * i, out_bytes,
+                                           cudaMemcpyDeviceToHost, c0.d2h),
+                           "D2H");
+                    ck(cudaEventRecord(cq.pipe_ev[D2H][b], c0.d2h), "record d2h");
+                }
+                ck(cudaStreamSynchronize(c0.d2h), "sync d2h");
+                for (int q = 0; q < P; ++q) sync(slots.use(q));
+            });
+            if (status[k]) msgs[k] = t_err;
         };
         std::vector<std::thread> pool;
         for (int k = 1; k < ndev; ++k) pool.emplace_back(device_worker, k);

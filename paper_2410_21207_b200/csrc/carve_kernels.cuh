@@ -1093,20 +1093,69 @@ __global__ void k_fixup_energy(double* __restrict__ e, int epitch, const uint32_
 // ---------------------------------------------------------------------------
 // Forward energy helpers
 
-// forward_costs (energy.hpp:196-216) of an arbitrary luma plane (the API entry;
-// the carve loop computes the same costs in registers inside the DP)
+// forward_costs (energy.hpp:196-216): cu = |R - L|, cl = cu + |A - L|,
+// cr = cu + |A - R| over clamped neighbours (at_clamped, raster.hpp:54-58),
+// left to right, no contraction
+__device__ __forceinline__ void fwd_costs_of(double l, double r, double a, double& cl, double& cu, double& cr) {
+    cu = fabs(__dsub_rn(r, l));
+    cl = __dadd_rn(cu, fabs(__dsub_rn(a, l)));
+    cr = __dadd_rn(cu, fabs(__dsub_rn(a, r)));
+}
+
+// ... of an arbitrary luma plane (pitch W in, pitch opitch out; the API entry and
+// the dp_seam_forward(gray) path; the default forward carve loop computes the
+// same costs in registers inside the fused DP)
 __global__ void k_forward_costs(const double* __restrict__ g, int W, int H, double* __restrict__ left,
-                                double* __restrict__ up, double* __restrict__ right) {
+                                double* __restrict__ up, double* __restrict__ right, int opitch) {
     const long long n = (long long)W * H;
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
         const int i = int(k / W), j = int(k - (long long)i * W);
         const double* row = g + (long long)i * W;
         const double l = row[max(j - 1, 0)], r = row[min(j + 1, W - 1)];
         const double a = g[(long long)max(i - 1, 0) * W + j];
-        const double cu = fabs(__dsub_rn(r, l));
-        up[k] = cu;
-        left[k] = __dadd_rn(cu, fabs(__dsub_rn(a, l)));
-        right[k] = __dadd_rn(cu, fabs(__dsub_rn(a, r)));
+        const long long o = (long long)i * opitch + j;
+        fwd_costs_of(l, r, a, left[o], up[o], right[o]);
+    }
+}
+
+// ... of to_grayscale of an RGBX plane, into three padded planes (plane stride
+// cplane): the recompute=false forward loop's cost state at the start of a phase
+__global__ void k_forward_costs_rgbx(const uint32_t* __restrict__ rgb, int rpitch, int W, int H,
+                                     double* __restrict__ costs, int epitch, long long cplane) {
+    const long long n = (long long)W * H;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const int i = int(k / W), j = int(k - (long long)i * W);
+        const uint32_t* row = rgb + (long long)i * rpitch;
+        const double l = luma(row[max(j - 1, 0)]), r = luma(row[min(j + 1, W - 1)]);
+        const double a = luma(rgb[(long long)max(i - 1, 0) * rpitch + j]);
+        const long long o = (long long)i * epitch + j;
+        fwd_costs_of(l, r, a, costs[o], costs[o + cplane], costs[o + 2 * cplane]);
+    }
+}
+
+// detail::drop_columns (carver.hpp:57-67) on `np` FP64 planes at once (plane
+// stride pstride, pitch `pitch`, out of place): out[i][j] = in[i][j + (j >= s_i)]
+// for j < W - 1. One CTA row per image row, consecutive columns per thread.
+__global__ void k_drop_col_planes(const double* __restrict__ in, double* __restrict__ out, int pitch,
+                                  long long pstride, int W, int H, const int* __restrict__ seam) {
+    const int i = blockIdx.y, pl = blockIdx.z;
+    const int s = __ldg(seam + i);
+    const double* src = in + pl * pstride + (long long)i * pitch;
+    double* dst = out + pl * pstride + (long long)i * pitch;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < W - 1; j += gridDim.x * blockDim.x)
+        dst[j] = src[j + (j >= s ? 1 : 0)];
+}
+
+// remove_seam(LumaGrid / EnergyMap / RemovalMask) (carver.hpp:84-112): the
+// row-major w x h plane minus column s_i of every row, out of place, packed
+// pitch w - 1. One thread per output element; T = double or uint8_t.
+template <typename T>
+__global__ void k_drop_columns(const T* __restrict__ in, int W, int H, const int* __restrict__ seam,
+                               T* __restrict__ out) {
+    const long long n = (long long)(W - 1) * H;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const int i = int(k / (W - 1)), j = int(k - (long long)i * (W - 1));
+        out[k] = in[(long long)i * W + j + (j >= __ldg(seam + i) ? 1 : 0)];
     }
 }
 

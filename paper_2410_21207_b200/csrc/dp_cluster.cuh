@@ -76,6 +76,8 @@ struct Dp2Params {
     int rpitch;
     long long rgb_istride;
     int gather;  // 1: CTA 0 holds a gathered copy of every CTA's block-end labels (phase 1 stays local)
+    long long cplane;  // FWD without FUSED: element stride from the cost_left plane (e) to cost_up and
+                       // from cost_up to cost_right (three padded planes of the same pitch)
 };
 
 // smem layout (dynamic): labels int8 [nblk][NWARP*S], aliased by the phase-2
@@ -161,11 +163,16 @@ __device__ __forceinline__ void fwd_cell_left_last(double L, double M, double R,
     d = left ? 0 : td;
 }
 
+// `coherent`: the row may have been written earlier in this same launch (the
+// prologue's fix-up), so it is read through L2 (ld.global.cg) rather than the
+// read-only path, which is only defined for data constant during the kernel.
 template <int C>
-__device__ __forceinline__ void load_row(const double* __restrict__ row, int col0, double (&v)[C]) {
+__device__ __forceinline__ void load_row(const double* __restrict__ row, int col0, double (&v)[C],
+                                         bool coherent = false) {
 #pragma unroll
     for (int k = 0; k < C; k += 2) {
-        const double2 x = __ldg(reinterpret_cast<const double2*>(row + col0 + k));
+        const double2* a = reinterpret_cast<const double2*>(row + col0 + k);
+        const double2 x = coherent ? __ldcg(a) : __ldg(a);
         v[k] = x.x;
         v[k + 1] = x.y;
     }
@@ -293,10 +300,13 @@ __device__ __forceinline__ void argmin_combine(double& v, int& i, double ov, int
 // streamed through the same ring (rolling three luma rows per lane). Used for
 // batches, where the energy plane's 16 B/px/seam of traffic bounds throughput.
 // FWD: forward energy (CarveConfig::forward, carver.hpp:155-169): the cells take
-// dp_seam_forward's transition costs, computed in registers from the luma rows
-// above and current — from RGBX rows (FUSED) or, for the dp_seam_forward API,
-// from an FP64 luma plane streamed through the ring in place of the energy
-// plane (its columns -1 and W replicate the edge columns, like the RGBX planes).
+// dp_seam_forward's transition costs — with FUSED computed in registers from the
+// luma of the RGBX rows above and current; without FUSED streamed from three
+// caller-given FP64 cost planes (cost_left at e, cost_up at e + cplane,
+// cost_right at e + 2*cplane), 24 B per column through the same ring: the
+// dp_seam_forward(gray, costs) API with arbitrary costs (solvers.hpp:294-326)
+// and the recompute=false forward loop, whose costs are carved, not recomputed
+// (carver.hpp:175-184).
 template <int C, int K, int NWARP, int D, int MODE, bool FUSED = false, bool FWD = false, int MINB = 1>
 __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
     constexpr bool TABLES = MODE == 1;
@@ -304,7 +314,7 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
     long long pf_t0 = 0, pf_wait = 0;
     if constexpr (PROF) pf_t0 = clock64();
     static_assert(K % C == 0 && (32 * C) > 2 * K, "halo must be whole lanes and leave useful columns");
-    constexpr int RE = FUSED ? 4 : 8;  // ring bytes per column
+    constexpr int RE = FUSED ? 4 : (FWD ? 24 : 8);  // ring bytes per column
     using SM = Dp2Smem<C, K, NWARP, RE>;
     constexpr int S = SM::S;
     constexpr int KL = K / C;  // lanes per halo
@@ -426,15 +436,16 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
         } else {
             energy_cols<C>(Lp, Lc, Ln, oob, m);  // M[0] = e[0]
         }
-    } else if constexpr (FWD) {  // luma plane: row 0's luma, M[0] = cost_up(0, j)
+    } else if constexpr (FWD) {  // cost planes: M[0] = cost_up(0, j); +inf outside the image
 #pragma unroll
         for (int k = 0; k < C; ++k)
             if (col0 + k < 0 || col0 + k >= W) oob |= 1u << k;
-        load_row<C>(e, col0, Lc);
-        double cl0[C], cr0[C];
-        fwd_cols<C>(Lc, Lc, oob, cl0, m, cr0);
+        load_row<C>(e + p.cplane, col0, m);
+#pragma unroll
+        for (int k = 0; k < C; ++k)
+            if (oob >> k & 1) m[k] = dinf();
     } else {
-        load_row<C>(e, col0, m);
+        load_row<C>(e, col0, m, p.prev_seam != nullptr);
     }
 #pragma unroll
     for (int k = 0; k < C; ++k) lab[k] = col0 + k;
@@ -466,8 +477,12 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
             }
             ++frow;
         } else {
+            // this lane's C values of each plane: [plane 0 (C)][plane 1][plane 2] per stage
 #pragma unroll
-            for (int k = 0; k < C; k += 2) cp_async16(ring_lane + uint32_t(u * 32 * C * 8 + k * 8), nrow + k);
+            for (int pl = 0; pl < (FWD ? 3 : 1); ++pl)
+#pragma unroll
+                for (int k = 0; k < C; k += 2)
+                    cp_async16(ring_lane + uint32_t(u * 32 * C * RE + (pl * C + k) * 8), nrow + pl * p.cplane + k);
             nrow += p.epitch;
         }
         cp_async_commit();
@@ -490,16 +505,28 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
             else energy_cols<C>(Lp, Lc, Ln, oob, ev);
         } else {
             const double* src = reinterpret_cast<const double*>(ring_b + ((size_t(warp) * D + u) * 32 + lane) * C * RE);
+            if constexpr (FWD) {  // the ring row is cost row i of the three planes
 #pragma unroll
-            for (int k = 0; k < C; k += 2) {
-                const double2 x = *reinterpret_cast<const double2*>(src + k);
-                ev[k] = x.x;
-                ev[k + 1] = x.y;
-            }
-            if constexpr (FWD) {  // the ring row is luma row i
+                for (int k = 0; k < C; k += 2) {
+                    const double2 a = *reinterpret_cast<const double2*>(src + k);
+                    const double2 b = *reinterpret_cast<const double2*>(src + C + k);
+                    const double2 c = *reinterpret_cast<const double2*>(src + 2 * C + k);
+                    fcl[k] = a.x; fcl[k + 1] = a.y;
+                    fcu[k] = b.x; fcu[k + 1] = b.y;
+                    fcr[k] = c.x; fcr[k + 1] = c.y;
+                }
+                if (oob) {
 #pragma unroll
-                for (int k = 0; k < C; ++k) { Lp[k] = Lc[k]; Lc[k] = ev[k]; }
-                fwd_cols<C>(Lp, Lc, oob, fcl, fcu, fcr);
+                    for (int k = 0; k < C; ++k)
+                        if (oob >> k & 1) fcl[k] = fcu[k] = fcr[k] = dinf();
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < C; k += 2) {
+                    const double2 x = *reinterpret_cast<const double2*>(src + k);
+                    ev[k] = x.x;
+                    ev[k + 1] = x.y;
+                }
             }
         }
         const double lm = __shfl_up_sync(FULL, m[C - 1], 1);
@@ -785,12 +812,10 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) px[k] = __ldg(rb + k);
                 luma_cols<4>(px, QLc);
-            } else if constexpr (FWD) {  // luma plane: the row above the block
+            } else if constexpr (FWD) {  // cost planes: columns outside the image are +inf
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
+                for (int k = 0; k < 4; ++k)
                     if (wc0 + k < 0 || wc0 + k >= W) qoob |= 1u << k;
-                    QLp[k] = e[(long long)(r0 - 1) * p.epitch + wc0 + k];
-                }
             }
             auto p2fetch = [&](int r, int slot) {
                 const uint32_t dst = p2ring + uint32_t(slot * P2STAGE);
@@ -798,8 +823,11 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
                     cp_async16(dst, wrgb + (long long)min(r + 1, H - 1) * p.rpitch);
                 } else {
                     const double* src = e + (long long)min(r, r1) * p.epitch + wc0;
-                    cp_async16(dst, src);
-                    cp_async16(dst + 16, src + 2);
+#pragma unroll
+                    for (int pl = 0; pl < (FWD ? 3 : 1); ++pl) {
+                        cp_async16(dst + pl * 32, src + pl * p.cplane);
+                        cp_async16(dst + pl * 32 + 16, src + pl * p.cplane + 2);
+                    }
                 }
                 cp_async_commit();
             };
@@ -821,12 +849,17 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
                     const double2 x0 = *reinterpret_cast<const double2*>(src);
                     const double2 x1 = *reinterpret_cast<const double2*>(src + 2);
                     ec[0] = x0.x; ec[1] = x0.y; ec[2] = x1.x; ec[3] = x1.y;
-                    if constexpr (FWD) {  // luma row r
+                    if constexpr (FWD) {  // cost row r of the three planes
+                        const double2 y0 = *reinterpret_cast<const double2*>(src + 4);
+                        const double2 y1 = *reinterpret_cast<const double2*>(src + 6);
+                        const double2 z0 = *reinterpret_cast<const double2*>(src + 8);
+                        const double2 z1 = *reinterpret_cast<const double2*>(src + 10);
+                        qcl[0] = x0.x; qcl[1] = x0.y; qcl[2] = x1.x; qcl[3] = x1.y;
+                        qcu[0] = y0.x; qcu[1] = y0.y; qcu[2] = y1.x; qcu[3] = y1.y;
+                        qcr[0] = z0.x; qcr[1] = z0.y; qcr[2] = z1.x; qcr[3] = z1.y;
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) QLc[k] = ec[k];
-                        fwd_cols<4>(QLp, QLc, qoob, qcl, qcu, qcr);
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) QLp[k] = QLc[k];
+                        for (int k = 0; k < 4; ++k)
+                            if (qoob >> k & 1) qcl[k] = qcu[k] = qcr[k] = dinf();
                     }
                 }
 #pragma unroll

@@ -17,10 +17,11 @@ struct Dp2Variant {
     const void* fn_fused;  // hot kernel, energy recomputed from RGBX (batch mode)
     const void* fn_fwd;    // forward energy from RGBX rows (fused), hot / with tables
     const void* fn_fwd_tables;
-    const void* fn_fwdp;   // forward energy from an FP64 luma plane (dp_seam_forward API)
-    const void* fn_fwdp_tables;
+    const void* fn_fwdp;   // forward energy from three FP64 cost planes (dp_seam_forward API,
+    const void* fn_fwdp_tables;  // the recompute=false forward loop)
     size_t (*smem)(int nblk, int D);        // energy-plane ring (8 B per column)
     size_t (*smem_fused)(int nblk, int D);  // RGBX ring (4 B per column)
+    size_t (*smem_costs)(int nblk, int D);  // cost-plane ring (3 x 8 B per column)
     int S() const { return 32 * C - 2 * K; }
     int cols() const { return NW * S(); }
 };
@@ -38,7 +39,8 @@ Dp2Variant dp2_variant() {
                       (const void*)k_dp2<C, K, NW, D, 0, false, true, MINB>,
                       (const void*)k_dp2<C, K, NW, D, 1, false, true, MINB>,
                       &Dp2Smem<C, K, NW, 8>::total,
-                      &Dp2Smem<C, K, NW, 4>::total};
+                      &Dp2Smem<C, K, NW, 4>::total,
+                      &Dp2Smem<C, K, NW, 24>::total};
 }
 
 // each appends its variants in index order (a: 0-3, b: 4-8, c: 9-)

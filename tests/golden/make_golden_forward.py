@@ -6,10 +6,12 @@ reference headers compiled unmodified). Run in the build container:
 
 Outputs:
   forward.npz   luma maps with forward_costs (energy.hpp:196-216) and
-                dp_seam_forward tables/seams (solvers.hpp:294-326); small images
-                carved with forward=true and with recompute=false (run_resize order)
-  golden.json   configs["C1_FORWARD"], configs["C1_NORECOMPUTE"]: FNV-1a-64 of the
-                512x512 -> 448x512 carve output and seams under those configs
+                dp_seam_forward tables/seams (solvers.hpp:294-326); arbitrary
+                cost planes with their dp_seam_forward tables/seams; small images
+                carved with forward=true, with recompute=false and with both
+                (run_resize order)
+  golden.json   configs["C1_FORWARD"], ["C1_NORECOMPUTE"], ["C1_FORWARD_NORECOMPUTE"]:
+                FNV-1a-64 of the 512x512 -> 448x512 carve output and seams
 """
 from __future__ import annotations
 
@@ -59,12 +61,35 @@ def main() -> None:
             out[f"norec{k}"], out[f"norecseams{k}"] = ref.carve_cfg(img, tw, th, recompute=False, seams=True)
             k += 1
     out["nimgs"] = np.array(k)
+    # round 2: dp_seam_forward with arbitrary caller costs (gray supplies only the
+    # dimensions, solvers.hpp:294-326) and forward + recompute=false carves, whose
+    # cost planes are carved by drop_columns (carver.hpp:175-184)
+    rng2 = np.random.default_rng(0xF1)
+    ncm = 0
+    cost_shapes = [tuple(int(v) for v in rng2.integers(1, 13, 2)) for _ in range(120)]
+    cost_shapes += [(1, 1), (1, 9), (9, 1), (300, 40), (2000, 9), (64, 700), (130, 33)]
+    for j, (w, h) in enumerate(cost_shapes):
+        if j % 3 == 0:  # integer costs: many ties
+            cs = [np.floor(rng2.uniform(0, 4, (h, w))) for _ in range(3)]
+        elif j % 3 == 1:  # signed real costs
+            cs = [rng2.uniform(-50, 50, (h, w)) for _ in range(3)]
+        else:  # costs of some other luma (not this image's forward_costs)
+            cs = list(ref.forward_costs(rng2.uniform(0, 255, (h, w))))
+        for key, c in zip(("fcl", "fcu", "fcr"), cs):
+            out[f"{key}{ncm}"] = c
+        out[f"fseam{ncm}"], out[f"fm{ncm}"], out[f"fb{ncm}"] = ref.dp_seam_forward_costs(*cs)
+        ncm += 1
+    out["ncostmaps"] = np.array(ncm)
+    for j in range(k):
+        img, (tw, th) = out[f"img{j}"], (int(v) for v in out[f"tgt{j}"])
+        out[f"fnr{j}"], out[f"fnrseams{j}"] = ref.carve_cfg(img, tw, th, forward=True, recompute=False, seams=True)
     np.savez_compressed(os.path.join(HERE, "forward.npz"), **out)
 
     path = os.path.join(HERE, "golden.json")
     gold = json.load(open(path))
     img = ref.make_test_image(512, 512)
-    for name, fwd, rec in (("C1_FORWARD", True, True), ("C1_NORECOMPUTE", False, False)):
+    for name, fwd, rec in (("C1_FORWARD", True, True), ("C1_NORECOMPUTE", False, False),
+                           ("C1_FORWARD_NORECOMPUTE", True, False)):
         o, s = ref.carve_cfg(img, 448, 512, forward=fwd, recompute=rec, seams=True)
         gold["configs"][name] = {"W": 512, "H": 512, "target_w": 448, "target_h": 512, "forward": fwd,
                                  "recompute": rec, "input": h64(img), "output": h64(o), "seams": h64(s)}

@@ -93,3 +93,20 @@ def test_missing_library_raises(tmp_path, monkeypatch):
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         mod.library()
     importlib.reload(cv)
+
+
+def test_batch_plan_host_logic(monkeypatch):
+    """carve_batch's pipeline shape (SURVEY.md §8e work queue): chunks never
+    exceed the per-device share, and the env overrides are read per call."""
+    for n, ndev in [(1, 1), (6, 2), (128, 1), (256, 1), (1024, 1), (1024, 8), (1025, 4), (5000, 3)]:
+        p, ch = cv.batch_plan(n, 1024, 768, 896, 768, ndev)
+        share = -(-n // ndev)
+        assert 1 <= ch <= share and 1 <= p <= 4
+        assert p <= -(-share // ch)
+    monkeypatch.setenv("CARVE_PIPE_CHUNK", "16")
+    monkeypatch.setenv("CARVE_PIPELINES", "3")
+    assert cv.batch_plan(1025, 64, 48, 56, 48, 2) == (3, 16)
+    assert cv.batch_plan(20, 64, 48, 56, 48, 2) == (1, 10)
+    for bad in [(0, 8, 8, 8, 8, 1), (4, 8, 8, 9, 8, 1), (4, 8, 8, 8, 8, 0)]:
+        with pytest.raises(cv.CarveError):
+            cv.batch_plan(*bad)

@@ -54,7 +54,7 @@ def test_forward_and_norecompute_carves_golden(z):
             assert np.array_equal(flat, z[f"{key}seams{k}"][: flat.size]), (k, key)
 
 
-@pytest.mark.parametrize("name", ["C1_FORWARD", "C1_NORECOMPUTE"])
+@pytest.mark.parametrize("name", ["C1_FORWARD", "C1_NORECOMPUTE", "C1_FORWARD_NORECOMPUTE"])
 def test_c1_config_golden(name):
     c = json.load(open(os.path.join(GOLD, "golden.json")))["configs"][name]
     img = cv.make_test_image(c["W"], c["H"])
@@ -105,6 +105,53 @@ def test_forward_api_contract():
     assert ei.value.code == cv.Errc.usage_error
     out, rep = cv.carve_to_width(cv.make_test_image(16, 12), 8, cv.CarveConfig(recompute=False))
     assert out.shape == (12, 8, 3) and rep.seam_count == 8
-    with pytest.raises(cv.CarveError) as ei:  # not supported by the engine (fails loudly)
-        cv.carve(img, 9, forward=True, recompute=False)
+    out, rep = cv.carve_to_width(img, 9, cv.CarveConfig(forward=True, recompute=False))
+    assert out.shape == (10, 9, 3) and rep.seam_count == 5
+    # non-finite caller costs: the engine fails loudly instead of guessing the
+    # reference's best = +inf semantics
+    g = np.zeros((3, 4))
+    cl, cu, cr = cv.forward_costs(g)
+    cu[1, 2] = np.inf
+    with pytest.raises(cv.CarveError) as ei:
+        cv.dp_seam_forward(g, (cl, cu, cr))
     assert ei.value.code == cv.Errc.usage_error
+
+
+def test_forward_arbitrary_costs_golden(z):
+    """dp_seam_forward(gray, costs) with caller costs that are not
+    forward_costs(gray): integer (tie-heavy), signed real, another image's costs."""
+    for k in range(int(z["ncostmaps"])):
+        cs = (z[f"fcl{k}"], z[f"fcu{k}"], z[f"fcr{k}"])
+        g = np.zeros_like(cs[0])
+        r = cv.dp_seam_forward(g, cs)
+        assert np.array_equal(r.seam, z[f"fseam{k}"]), k
+        assert np.array_equal(r.table.b, z[f"fb{k}"]), k
+        assert np.array_equal(bits(r.table.m), bits(z[f"fm{k}"])), k
+
+
+def test_forward_norecompute_carves_golden(z):
+    """forward + recompute=false: the phase's forward costs are computed once and
+    carved alongside the image (carver.hpp:175-184)."""
+    for k in range(int(z["nimgs"])):
+        img = z[f"img{k}"]
+        tw, th = (int(v) for v in z[f"tgt{k}"])
+        out, seams, _ = cv.carve(img, tw, th, seams=True, forward=True, recompute=False)
+        assert np.array_equal(out, z[f"fnr{k}"]), k
+        flat = np.concatenate(seams) if seams else np.zeros(0, np.int32)
+        assert np.array_equal(flat, z[f"fnrseams{k}"][: flat.size]), k
+
+
+@pytest.mark.parametrize("w,h", [(33, 17), (300, 65), (1100, 21), (2500, 40)])
+def test_forward_norecompute_random_vs_oracle(w, h):
+    port = oracle.port()
+    rng = np.random.default_rng(3 * w + h)
+    img = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+    tw, th = w - max(1, w // 10), h - max(1, h // 5)
+    want, ws = port.carve_cfg(img, tw, th, forward=True, recompute=False, seams=True)
+    got, gs, _ = cv.carve(img, tw, th, seams=True, forward=True, recompute=False)
+    assert np.array_equal(got, want)
+    assert np.array_equal(np.concatenate(gs), ws)
+    cs = [rng.uniform(-9, 99, (h, w)) for _ in range(3)]
+    r = cv.dp_seam_forward(np.zeros((h, w)), cs)
+    s, m, b = port.dp_seam_forward_costs(*cs)
+    assert np.array_equal(r.seam, s) and np.array_equal(r.table.b, b) and np.array_equal(bits(r.table.m), bits(m))

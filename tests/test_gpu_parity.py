@@ -380,3 +380,28 @@ def test_batch_device_resident_split_matches_oracle(port, monkeypatch, split):
     want = {k: port.carve(imgs[k], tw, th) for k in range(23)}
     for k in range(n):
         assert np.array_equal(outs[k], want[k % 23]), k
+
+
+def test_remove_seam_planes_golden(golden_dir):
+    """remove_seam(LumaGrid / EnergyMap / RemovalMask) = detail::drop_columns
+    (carver.hpp:57-112) against the reference-generated api.npz: FP64 bits and
+    mask bytes, connected and arbitrary per-row columns."""
+    z = np.load(os.path.join(golden_dir, "api.npz"))
+    for k in range(int(z["n"])):
+        got = cv.remove_seam(z[f"plane{k}"], z[f"seam{k}"])
+        want = z[f"want{k}"]
+        assert got.dtype == want.dtype and got.shape == want.shape, k
+        if want.dtype == np.float64:
+            assert np.array_equal(bits(got), bits(want)), k
+        else:
+            assert np.array_equal(got, want), k
+
+
+def test_remove_seam_planes_errors():
+    for plane in (np.zeros((3, 4)), np.zeros((3, 4), np.uint8)):
+        for bad in ([0, 1], [0, 4, 1], [-1, 0, 0]):
+            with pytest.raises(cv.CarveError) as ei:
+                cv.remove_seam(plane, bad)
+            assert ei.value.code == cv.Errc.invalid_seam
+    # width 1 -> width 0 (the reference's drop_columns yields an empty grid)
+    assert cv.remove_seam(np.ones((5, 1)), [0] * 5).shape == (5, 0)

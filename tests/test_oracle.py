@@ -262,3 +262,25 @@ def test_masks_golden(port):
         L = n * _seam_len(mask)
         assert got_n == n and np.array_equal(res, z[f"res{k}"]), k
         assert np.array_equal(seams[:L], z[f"seams{k}"][:L]), k
+
+
+def test_remove_seam_planes_port_golden(port):
+    """The C restatement of detail::drop_columns against the reference's api.npz."""
+    z = np.load(os.path.join(GOLD, "api.npz"))
+    for k in range(int(z["n"])):
+        got = port.remove_seam_plane(z[f"plane{k}"], z[f"seam{k}"])
+        assert np.array_equal(got.view(np.uint8), z[f"want{k}"].view(np.uint8)), k
+
+
+def test_forward_costs_norecompute_port_golden(port):
+    """The C restatement of dp_seam_forward(gray, costs) with arbitrary costs and
+    of the forward + recompute=false loop against the reference's forward.npz."""
+    z = np.load(os.path.join(GOLD, "forward.npz"))
+    for k in range(int(z["ncostmaps"])):
+        s, m, b = port.dp_seam_forward_costs(z[f"fcl{k}"], z[f"fcu{k}"], z[f"fcr{k}"])
+        assert np.array_equal(s, z[f"fseam{k}"]) and np.array_equal(b, z[f"fb{k}"]), k
+        assert np.array_equal(m.view(np.uint64), z[f"fm{k}"].view(np.uint64)), k
+    for k in range(int(z["nimgs"])):
+        tw, th = (int(v) for v in z[f"tgt{k}"])
+        out, seams = port.carve_cfg(z[f"img{k}"], tw, th, forward=True, recompute=False, seams=True)
+        assert np.array_equal(out, z[f"fnr{k}"]) and np.array_equal(seams, z[f"fnrseams{k}"][: seams.size]), k

@@ -126,6 +126,51 @@ static int selftest() {
            Errc::empty_mask);
     EXPECT(thrown([] { remove_object(PixelGrid(4, 4), RemovalMask{3, 4, std::vector<uint8_t>(12, 1)}); }) ==
            Errc::dimension_mismatch);
+    // remove_seam overloads on scalar grids (carver.hpp:84-112; test_carver.cpp:55-73)
+    LumaGrid lg{3, 2, {1, 2, 3, 4, 5, 6}};
+    auto lr = remove_seam(lg, {1, 0});
+    EXPECT(lr.width == 2 && (lr.values == std::vector<double>{1, 3, 5, 6}));
+    EnergyMap em{3, 2, {1, 2, 3, 4, 5, 6}};
+    auto er = remove_seam(em, {2, 2});
+    EXPECT(er.width == 2 && (er.values == std::vector<double>{1, 2, 4, 5}));
+    RemovalMask rm{3, 2, {1, 0, 1, 0, 1, 0}};
+    auto mr = remove_seam(rm, {0, 2});  // not connected: allowed, like the reference
+    EXPECT(mr.width == 2 && (mr.flags == std::vector<uint8_t>{0, 1, 0, 1}));
+    EXPECT((detail::drop_columns({1, 2, 3}, 3, 1, {1}) == std::vector<double>{1, 3}));
+    EXPECT(thrown([] { remove_seam(EnergyMap{2, 1, {1, 2}}, {2}); }) == Errc::invalid_seam);
+    // detail::insert_columns: per-row columns may jump (carver.hpp:116-132)
+    PixelGrid jump(3, 2);
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 3; ++j) jump.at(i, j) = Rgb{uint8_t(10 * j), uint8_t(10 * j), uint8_t(10 * j)};
+    auto ic = detail::insert_columns(jump, {0, 2});
+    EXPECT(ic.width == 4 && (ic.at(0, 1) == Rgb{5, 5, 5}) && (ic.at(1, 3) == Rgb{20, 20, 20}));
+    // dp_seam_forward with caller costs (solvers.hpp:294-326): gray only gives the size
+    LumaGrid g0{2, 2, {0, 0, 0, 0}};
+    ForwardCosts fc{2, 2, {5, 5, 0, 9}, {1, 2, 9, 9}, {9, 9, 9, 9}};
+    auto fr = dp_seam_forward(g0, fc);
+    EXPECT((fr.table.m == std::vector<double>{1, 2, 10, 10}) && (fr.seam == Seam{0, 0}) && fr.table.b[3] == 0);
+    // forward + recompute=false is a supported configuration (carver.hpp:175-184)
+    CarveConfig fnr;
+    fnr.forward = true;
+    fnr.recompute = false;
+    EXPECT(carve_to_width(make_test_image(20, 12), 15, fnr).first.width == 15);
+    // BenchRecord timers (bench.hpp:32-59, 140-201)
+    auto bimg = make_test_image(40, 30);
+    CarveConfig dpcfg;
+    dpcfg.solver = SolverKind::Dynamic;
+    BenchRecord full = time_full_carve(bimg, 0.5, dpcfg, 2);
+    EXPECT(full.phase == Phase::full_carve && full.n == 30 && full.scale && *full.scale == 0.5);
+    EXPECT(full.repetitions == 2 && full.wall_time_s > 0.0 && full.solver == SolverKind::Dynamic);
+    EXPECT(full.energy_fn == "e1" && full.timestamp_utc.size() == 20 && full.timestamp_utc.back() == 'Z');
+    CarveConfig fwd;
+    fwd.forward = true;
+    BenchRecord single = time_single_seam(bimg, fwd, 1);
+    EXPECT(single.phase == Phase::single_seam && !single.scale && single.solver == SolverKind::ParallelDynamic);
+    EXPECT(thrown([&] { time_full_carve(bimg, 1.5, dpcfg, 1); }) == Errc::usage_error);
+    EXPECT(thrown([&] { time_single_seam(bimg, dpcfg, 0); }) == Errc::usage_error);
+    EXPECT(parse_phase("full_carve") == Phase::full_carve && !parse_phase("x"));
+    BenchRecord copy = full;
+    EXPECT(copy == full);
     std::printf(failures ? "selftest FAILED (%d)\n" : "selftest ok\n", failures);
     return failures ? 1 : 0;
 }
