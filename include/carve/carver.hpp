@@ -217,45 +217,64 @@ inline std::pair<PixelGrid, CarveReport> enlarge_to_width(const PixelGrid& grid,
     PixelGrid out(target_width, grid.height);
     std::vector<int32_t> flat(std::max<size_t>(size_t(k) * grid.height, 1));
     const carve_cuda_config c = detail::abi_config(cfg);
-    detail::check(carve_cuda_enlarge(grid.bytes(), grid.width, grid.height, target_width, grid.height, &c,
-                                     out.bytes(), flat.data()));
-    CarveReport rep;
+    std::vector<carve_seam_timing> tim(size_t(std::max(k, 1)));
+    detail::check(carve_cuda_enlarge_timed(grid.bytes(), grid.width, grid.height, target_width, grid.height, &c,
+                                           out.bytes(), flat.data(), tim.data()));
+    CarveReport rep;  // record_seams' report (carver.hpp:275)
     for (int t = 0; t < k; ++t) {
         rep.seams.emplace_back(flat.begin() + size_t(t) * grid.height, flat.begin() + size_t(t + 1) * grid.height);
-        rep.per_seam.push_back({0.0, 0.0, 0.0});
+        rep.per_seam.push_back({tim[t].energy_s, tim[t].solve_s, tim[t].remove_s});
     }
     rep.seam_count = k;
     rep.total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return {std::move(out), std::move(rep)};
 }
 
-// Paper-comparison / non-hot-path pipelines keep their declarations.
-/// carver.hpp:327-340: the whole removal loop (mask-biased e1, DP, removal of
-/// image and mask) and the restoring enlargement run on the device.
-inline std::pair<PixelGrid, CarveReport> remove_object(const PixelGrid& grid, const RemovalMask& mask,
-                                                       const CarveConfig& cfg = {}, bool restore = true) {
-    detail::check_config(cfg);
+namespace detail {
+
+// the device removal loop (carver.hpp:289-340): orientation 0 = by mask_bounds, 1 = vertical
+inline std::pair<PixelGrid, CarveReport> remove_object_device(const PixelGrid& grid, const RemovalMask& mask,
+                                                              const CarveConfig& cfg, bool restore, int orientation) {
     if (grid.width != mask.width || grid.height != mask.height)
         fail(Errc::dimension_mismatch, "mask dimensions do not match image");
     const auto t0 = std::chrono::steady_clock::now();
-    const carve_cuda_config c = detail::abi_config(cfg);
+    const carve_cuda_config c = abi_config(cfg);
     std::vector<uint8_t> buf(grid.pixels.size() * 3);
     std::vector<int32_t> flat(std::max<size_t>(grid.pixels.size(), 1));
+    std::vector<carve_seam_timing> tim(std::max<size_t>(size_t(std::max(grid.width, grid.height)), 1));
     int ow = 0, oh = 0, ns = 0;
-    detail::check(carve_cuda_remove_object(grid.bytes(), grid.width, grid.height, mask.flags.data(), &c,
-                                           restore ? 1 : 0, buf.data(), &ow, &oh, flat.data(), &ns));
+    check(carve_cuda_remove_object_ex(grid.bytes(), grid.width, grid.height, mask.flags.data(), &c, restore ? 1 : 0,
+                                      orientation, buf.data(), &ow, &oh, flat.data(), &ns, tim.data()));
     PixelGrid out(ow, oh);
     std::copy(buf.begin(), buf.begin() + size_t(ow) * oh * 3, out.bytes());
     CarveReport rep;
     rep.seam_count = ns;
     const MaskBounds b = mask_bounds(mask);
-    const size_t len = size_t(b.width() <= b.height() ? grid.height : grid.width);
+    const size_t len = size_t(orientation == 1 || b.width() <= b.height() ? grid.height : grid.width);
     for (int t = 0; t < ns; ++t) {
         rep.seams.emplace_back(flat.begin() + size_t(t) * len, flat.begin() + size_t(t + 1) * len);
-        rep.per_seam.push_back({0.0, 0.0, 0.0});
+        rep.per_seam.push_back({tim[t].energy_s, tim[t].solve_s, tim[t].remove_s});
     }
     rep.total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return {std::move(out), std::move(rep)};
+}
+
+/// carver.hpp:289-321: the removal loop along columns (then the restoring
+/// enlargement), on the device; an empty mask carves nothing.
+inline std::pair<PixelGrid, CarveReport> remove_object_vertical(const PixelGrid& grid, const RemovalMask& mask,
+                                                                const CarveConfig& cfg, bool restore) {
+    return remove_object_device(grid, mask, cfg, restore, 1);
+}
+
+} // namespace detail
+
+/// carver.hpp:327-340: the whole removal loop (mask-biased e1, DP, removal of
+/// image and mask) and the restoring enlargement run on the device; the report's
+/// per-seam energy / solve / remove laps come from device timestamps.
+inline std::pair<PixelGrid, CarveReport> remove_object(const PixelGrid& grid, const RemovalMask& mask,
+                                                       const CarveConfig& cfg = {}, bool restore = true) {
+    detail::check_config(cfg);
+    return detail::remove_object_device(grid, mask, cfg, restore, 0);
 }
 
 } // namespace carve

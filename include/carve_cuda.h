@@ -70,10 +70,12 @@ typedef struct carve_cuda_config {
 } carve_cuda_config;
 
 typedef struct carve_seam_timing {
-    double energy_s; /* K1 full map for the first seam of a phase; 0 when the
-                        incremental fix-up is fused into the removal kernel */
+    double energy_s; /* K1 full map for a phase's first seam, the DP prologue's
+                        2-column fix-up for the others; 0 where the energy is
+                        computed inside the DP (batches, forward energy) or not
+                        recomputed (recompute = 0) */
     double solve_s;  /* DP + argmin + backtrack (K2+K3) */
-    double remove_s; /* compaction + 2-column energy fix-up (K4+K1 fix-up) */
+    double remove_s; /* compaction (K4) */
 } carve_seam_timing;
 
 /* ---- library ----------------------------------------------------------- */
@@ -145,6 +147,18 @@ carve_status carve_cuda_apply_mask(const double* e, int w, int h, const uint8_t*
 carve_status carve_cuda_remove_object(const uint8_t* rgb, int w, int h, const uint8_t* mask,
                                       const carve_cuda_config* cfg, int restore, uint8_t* rgb_out, int* out_w,
                                       int* out_h, int32_t* seams_out, int* nseams);
+/* remove_object with the report's per-seam timings (timings_out: nullable, w*h
+ * entries at most; energy = the mask statistics + biased map, solve = the DP,
+ * remove = removal + 2-column fix-up) and an orientation: 0 = remove_object
+ * (auto, by mask_bounds), 1 = detail::remove_object_vertical (carver.hpp:289-321;
+ * an empty mask carves nothing instead of failing). The loop length is
+ * data-dependent, yet there is no host round trip per seam: the stop test is a
+ * device flag every kernel of the loop checks; the host reads it once per batch
+ * of iterations. */
+carve_status carve_cuda_remove_object_ex(const uint8_t* rgb, int w, int h, const uint8_t* mask,
+                                         const carve_cuda_config* cfg, int restore, int orientation,
+                                         uint8_t* rgb_out, int* out_w, int* out_h, int32_t* seams_out, int* nseams,
+                                         carve_seam_timing* timings_out);
 
 /* ---- seam recording and enlargement (carver.hpp:114-140, 226-285; cli.hpp:262-277, 301-309) */
 /* replaces insert_seam (carver.hpp:137-140: validate_seam + detail::insert_columns
@@ -168,6 +182,12 @@ carve_status carve_cuda_record_seams(const uint8_t* rgb, int w, int h, int count
  * phase's recorded seams (its CarveReport.seams), concatenated. */
 carve_status carve_cuda_enlarge(const uint8_t* rgb, int w, int h, int target_w, int target_h,
                                 const carve_cuda_config* cfg, uint8_t* rgb_out, int32_t* seams_out);
+/* carve_cuda_enlarge plus each recording's per-seam timings (the CarveReport
+ * per_seam of record_seams, carver.hpp:226-262): timings_out (nullable) receives
+ * (target_w-w) + (target_h-h) entries, width phase first. */
+carve_status carve_cuda_enlarge_timed(const uint8_t* rgb, int w, int h, int target_w, int target_h,
+                                      const carve_cuda_config* cfg, uint8_t* rgb_out, int32_t* seams_out,
+                                      carve_seam_timing* timings_out);
 
 /* ---- pipelines (carver.hpp:71-82, 191-222; cli.hpp:242-259) ----------- */
 /* replaces remove_seam(PixelGrid) (carver.hpp:71-82); out is (w-1)*h*3 bytes */

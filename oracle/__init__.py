@@ -147,7 +147,7 @@ class _Checker:
         h, w, _ = img.shape
         out = np.empty(w * h * 3, np.uint8)
         dims = np.zeros(2, np.int32)
-        seams = np.empty(max(w * h, 1), np.int32)
+        seams = np.zeros(max(w * h, 1), np.int32)
         n = np.zeros(1, np.int32)
         f = self._fn("remove_object", _u8p, C.c_int, C.c_int, _u8p, C.c_int, C.c_int, _u8p, _i4p, _i4p, _i4p)
         self._check(f(np.ascontiguousarray(img), w, h, np.ascontiguousarray(mask, np.uint8), int(forward),
@@ -260,6 +260,19 @@ class Reference(_Checker):
             f = self._fn("remove_seam_f64", _f8p, C.c_int, C.c_int, _i4p, C.c_int, C.c_int, C.c_void_p)
             self._check(f(a, w, h, s, len(s), 0 if kind == "luma" else 1, out.ctypes.data))
         return out
+
+    def remove_object_vertical(self, img: np.ndarray, mask: np.ndarray, restore: bool = True):
+        """carver.hpp:289-321 detail::remove_object_vertical -> (result, seams, count)"""
+        h, w, _ = img.shape
+        out = np.empty(w * h * 3, np.uint8)
+        dims = np.zeros(2, np.int32)
+        seams = np.zeros(max(w * h, 1), np.int32)
+        n = np.zeros(1, np.int32)
+        f = self._fn("remove_object_vertical", _u8p, C.c_int, C.c_int, _u8p, C.c_int, _u8p, _i4p, _i4p, _i4p)
+        self._check(f(np.ascontiguousarray(img), w, h, np.ascontiguousarray(mask, np.uint8), int(restore), out, dims,
+                      seams, n))
+        ow, oh = int(dims[0]), int(dims[1])
+        return out[: ow * oh * 3].reshape(oh, ow, 3).copy(), seams[: int(n[0]) * h], int(n[0])
 
     def bench_record(self, img: np.ndarray, full: bool, scale: float = 1.0, forward: bool = False, reps: int = 1):
         """BenchRecord fields of time_full_carve / time_single_seam (bench.hpp:140-201)."""

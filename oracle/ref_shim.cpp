@@ -352,6 +352,26 @@ int ref_remove_object(const std::uint8_t* rgb, int w, int h, const std::uint8_t*
     });
 }
 
+// carver.hpp:289-321 detail::remove_object_vertical (no orientation choice, no
+// empty-mask check)
+int ref_remove_object_vertical(const std::uint8_t* rgb, int w, int h, const std::uint8_t* mask, int restore,
+                               std::uint8_t* out, int* out_dims, int* seams_out, int* nseams) {
+    return guarded([&] {
+        carve_ref::CarveConfig cfg;
+        carve_ref::RemovalMask m{w, h, std::vector<std::uint8_t>(mask, mask + size_t(w) * h)};
+        auto [res, report] = carve_ref::detail::remove_object_vertical(grid_from(rgb, w, h), m, cfg, restore != 0);
+        grid_to(res, out);
+        out_dims[0] = res.width;
+        out_dims[1] = res.height;
+        size_t off = 0;
+        for (auto& s : report.seams) {
+            std::memcpy(seams_out + off, s.data(), s.size() * sizeof(int));
+            off += s.size();
+        }
+        *nseams = report.seam_count;
+    });
+}
+
 // carver.hpp:117-140 insert_seam (validate_seam + insert_columns)
 int ref_insert_seam(const std::uint8_t* rgb, int w, int h, const int* seam, int n, std::uint8_t* out) {
     return guarded([&] { grid_to(carve_ref::insert_seam(grid_from(rgb, w, h), carve_ref::Seam(seam, seam + n)), out); });

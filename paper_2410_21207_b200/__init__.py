@@ -175,12 +175,14 @@ def library() -> C.CDLL:
             "carve_cuda_insert_seam_rgb": ([vp, i, i, vp, i, vp], i),
             "carve_cuda_record_seams": ([vp, i, i, i, vp, vp, vp], i),
             "carve_cuda_enlarge": ([vp, i, i, i, i, vp, vp, vp], i),
+            "carve_cuda_enlarge_timed": ([vp, i, i, i, i, vp, vp, vp, vp], i),
             "carve_cuda_carve": ([vp, i, i, i, i, vp, vp, vp], i),
             "carve_cuda_carve_cfg": ([vp, i, i, i, i, vp, vp, vp, vp], i),
             "carve_cuda_forward_costs": ([vp, i, i, vp, vp, vp], i),
             "carve_cuda_mask_from_rgb": ([vp, i, i, vp], i),
             "carve_cuda_apply_mask": ([vp, i, i, vp, vp], i),
             "carve_cuda_remove_object": ([vp, i, i, vp, vp, i, vp, vp, vp, vp, vp], i),
+            "carve_cuda_remove_object_ex": ([vp, i, i, vp, vp, i, i, vp, vp, vp, vp, vp, vp], i),
             "carve_cuda_dp_seam_forward": ([vp, i, i, vp, vp, vp], i),
             "carve_cuda_dp_seam_forward_costs": ([vp, vp, vp, i, i, vp, vp, vp], i),
             "carve_cuda_remove_seam_f64": ([vp, i, i, vp, i, vp], i),
@@ -520,28 +522,43 @@ def mask_bounds(mask: np.ndarray):
     return (int(ys.min()), int(xs.min()), int(ys.max()), int(xs.max()))
 
 
-def remove_object(img: np.ndarray, mask: np.ndarray, cfg: CarveConfig | None = None, restore: bool = True):
-    """carver.hpp:327-340 — returns (result, CarveReport). The removal loop and
-    the restoring enlargement run on the device."""
+def _remove_object(img, mask, cfg, restore, orientation):
     import time
     a = _img(img)
     h, w, _ = a.shape
-    _check_config(cfg)
     m = np.ascontiguousarray(mask, dtype=np.uint8)
     if m.shape != (h, w):
         raise CarveError(Errc.dimension_mismatch, "mask dimensions do not match image")
     t0 = time.perf_counter()
     buf = np.empty(max(w * h * 3, 1), np.uint8)
     flat = np.empty(max(w * h, 1), np.int32)
+    tim = (_Timing * max(w, h, 1))()
     ow, oh, ns = C.c_int(), C.c_int(), C.c_int()
     c = _abi_config(cfg)
-    _check(library().carve_cuda_remove_object(_ptr(a), w, h, _ptr(m), C.byref(c), int(bool(restore)), _ptr(buf),
-                                              C.byref(ow), C.byref(oh), _ptr(flat), C.byref(ns)))
+    _check(library().carve_cuda_remove_object_ex(_ptr(a), w, h, _ptr(m), C.byref(c), int(bool(restore)), orientation,
+                                                 _ptr(buf), C.byref(ow), C.byref(oh), _ptr(flat), C.byref(ns),
+                                                 C.cast(tim, C.c_void_p)))
     out = buf[: ow.value * oh.value * 3].reshape(oh.value, ow.value, 3).copy()
     top, left, bottom, right = mask_bounds(m)
-    n = h if right - left <= bottom - top else w
+    n = h if (orientation == 1 or right - left <= bottom - top) else w
     seams = [flat[t * n:(t + 1) * n].copy() for t in range(ns.value)]
-    return out, _report(seams, [SeamTiming(0.0, 0.0, 0.0) for _ in seams], time.perf_counter() - t0)
+    per = [SeamTiming(tim[t].energy_s, tim[t].solve_s, tim[t].remove_s) for t in range(ns.value)]
+    return out, _report(seams, per, time.perf_counter() - t0)
+
+
+def remove_object(img: np.ndarray, mask: np.ndarray, cfg: CarveConfig | None = None, restore: bool = True):
+    """carver.hpp:327-340 — returns (result, CarveReport). The removal loop and
+    the restoring enlargement run on the device; per-seam timings from device
+    timestamps."""
+    _check_config(cfg)
+    return _remove_object(img, mask, cfg, restore, 0)
+
+
+def remove_object_vertical(img: np.ndarray, mask: np.ndarray, cfg: CarveConfig | None = None,
+                           restore: bool = True):
+    """detail::remove_object_vertical (carver.hpp:289-321): the loop along columns
+    whatever the mask's shape; an empty mask carves nothing."""
+    return _remove_object(img, mask, cfg, restore, 1)
 
 
 def insert_seam(img: np.ndarray, seam) -> np.ndarray:
@@ -575,10 +592,11 @@ def record_seams(img: np.ndarray, count: int, cfg: CarveConfig | None = None):
 
 
 def enlarge(img: np.ndarray, target_width: int, target_height: int | None = None, *, seams: bool = False,
-            cfg: CarveConfig | None = None):
+            cfg: CarveConfig | None = None, timings: bool = False):
     """run_enlarge (cli.hpp:262-277): enlarge_to_width on the width, then on the
     transpose for the height. Returns the image (plus the recorded seams of both
-    phases, concatenated, when `seams`)."""
+    phases, concatenated, when `seams`; plus their per-seam SeamTimings when
+    `timings`)."""
     a = _img(img)
     h, w, _ = a.shape
     th = h if target_height is None else int(target_height)
@@ -586,9 +604,17 @@ def enlarge(img: np.ndarray, target_width: int, target_height: int | None = None
     n = max(tw - w, 0) * h + max(th - h, 0) * tw
     out = np.empty((max(th, 0), max(tw, 0), 3), np.uint8)
     s = np.empty(max(n, 1), np.int32)
+    nt = max(tw - w, 0) + max(th - h, 0)
+    t = (_Timing * max(nt, 1))()
     c = _abi_config(cfg)
-    _check(library().carve_cuda_enlarge(_ptr(a), w, h, tw, th, C.byref(c), _ptr(out), _ptr(s)))
-    return (out, s[:n]) if seams else out
+    _check(library().carve_cuda_enlarge_timed(_ptr(a), w, h, tw, th, C.byref(c), _ptr(out), _ptr(s),
+                                              C.cast(t, C.c_void_p) if timings else None))
+    res = [out]
+    if seams:
+        res.append(s[:n])
+    if timings:
+        res.append([SeamTiming(t[k].energy_s, t[k].solve_s, t[k].remove_s) for k in range(nt)])
+    return res[0] if len(res) == 1 else tuple(res)
 
 
 def enlarge_to_width(img: np.ndarray, target_width: int, cfg: CarveConfig | None = None):
@@ -598,10 +624,10 @@ def enlarge_to_width(img: np.ndarray, target_width: int, cfg: CarveConfig | None
     h, w, _ = a.shape
     _check_config(cfg)
     t0 = time.perf_counter()
-    out, flat = enlarge(a, target_width, h, seams=True, cfg=cfg)
+    out, flat, tims = enlarge(a, target_width, h, seams=True, cfg=cfg, timings=True)
     k = int(target_width) - w
     seams = [flat[t * h:(t + 1) * h].copy() for t in range(k)]
-    return out, _report(seams, [SeamTiming(0.0, 0.0, 0.0) for _ in range(k)], time.perf_counter() - t0)
+    return out, _report(seams, tims[:k], time.perf_counter() - t0)
 
 
 def carve_to_height(img: np.ndarray, target_height: int, cfg: CarveConfig | None = None):

@@ -257,7 +257,7 @@ void launch_transpose(const uint32_t* in, int ipitch, int W, int H, uint32_t* ou
 int env_int(const char* name, int dflt);
 
 void launch_energy(const uint32_t* rgb, int pitch, int W, int H, double* e, int epitch, int nimg, long long rgb_is,
-                   long long e_is, cudaStream_t s) {
+                   long long e_is, cudaStream_t s, unsigned long long* st = nullptr, long long st_is = 0) {
     if (env_int("CARVE_K1", 1) == 0) {  // shared-memory tile version (kept for A/B)
         dim3 grid((W + K1_TW - 1) / K1_TW, (H + K1_TH - 1) / K1_TH, nimg);
         k_energy_full<<<grid, 256, 0, s>>>(rgb, pitch, W, H, e, epitch, rgb_is, e_is);
@@ -293,9 +293,10 @@ void launch_energy(const uint32_t* rgb, int pitch, int W, int H, double* e, int 
     R = k1v == 1 ? ((R + 3) & ~3) : ((R + 1) & ~1);
     const long long warps = (long long)nstrips * ((H + R - 1) / R);
     dim3 grid(unsigned((warps + 7) / 8), nimg);
-    if (k1v == 1) k_energy_rows<1, 4><<<grid, 256, 0, s>>>(rgb, pitch, W, H, e, epitch, rgb_is, e_is, nstrips, R);
-    else if (k1v == 2) k_energy_rows<3, 2><<<grid, 256, 0, s>>>(rgb, pitch, W, H, e, epitch, rgb_is, e_is, nstrips, R);
-    else k_energy_rows<1, 2><<<grid, 256, 0, s>>>(rgb, pitch, W, H, e, epitch, rgb_is, e_is, nstrips, R);
+    if (k1v == 1) k_energy_rows<1, 4><<<grid, 256, 0, s>>>(rgb, pitch, W, H, e, epitch, rgb_is, e_is, nstrips, R, st, st_is);
+    else if (k1v == 2)
+        k_energy_rows<3, 2><<<grid, 256, 0, s>>>(rgb, pitch, W, H, e, epitch, rgb_is, e_is, nstrips, R, st, st_is);
+    else k_energy_rows<1, 2><<<grid, 256, 0, s>>>(rgb, pitch, W, H, e, epitch, rgb_is, e_is, nstrips, R, st, st_is);
     LAUNCHED("k_energy_rows");
 }
 
@@ -603,9 +604,12 @@ void check_targets(int w, int h, int tw, int th) {
     if (th < h) dp2_plan(h, tw);
 }
 
-// stamps layout per image: [4 per seam: dp start/end, compact start/end] then
-// [4: energy full start/end for phase A, phase B]
-size_t stamp_words(const CarveGeometry& g) { return size_t(g.nseams) * 4 + 4; }
+// stamps layout per image: 6 per seam [energy start/end, solve start/end, remove
+// start/end] (+ 4 spare). Energy: the K1 full map for a phase's first seam, the DP
+// prologue's 2-column fix-up for the others; 0 where it is fused into the DP
+// (batches, forward energy) or not recomputed (recompute=false).
+constexpr int kStampsPerSeam = 6;
+size_t stamp_words(const CarveGeometry& g) { return size_t(g.nseams) * kStampsPerSeam + 4; }
 
 // CarveConfig fields that change the device loop (carver.hpp:15-24)
 struct CarveOpts {
@@ -672,7 +676,8 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
             {
                 // algorithmic bytes: 3 B RGB read + 8 B FP64 write per pixel
                 Prof pr(c, s, KK_ENERGY, 11.0 * W0 * H * nimg);
-                launch_energy(rgb[cur], pitch, W0, H, e, epitch, nimg, pis, eis, s);
+                launch_energy(rgb[cur], pitch, W0, H, e, epitch, nimg, pis, eis, s,
+                              d_stamps ? d_stamps + size_t(stamp_seam0) * kStampsPerSeam : nullptr, (long long)sw);
             }
             launch_fill_pads(e, epitch, W0, H, nimg, eis, s);
         }
@@ -680,7 +685,7 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
             const int W = W0 - k;
             t_dbg_tag = W;
             int* seam = d_seams + seam_base + size_t(k) * H;
-            unsigned long long* st = d_stamps ? d_stamps + size_t(stamp_seam0 + k) * 4 : nullptr;
+            unsigned long long* st = d_stamps ? d_stamps + size_t(stamp_seam0 + k) * kStampsPerSeam : nullptr;
             {
                 const Dp2Plan pl = dp2_plan(W, H, nimg > 1, fused ? RING_RGBX : costs ? RING_COSTS : RING_ENERGY, nimg);
                 Dp2Params q{};
@@ -726,7 +731,7 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
             q.W = W;
             q.H = H;
             q.seam = seam;
-            q.stamps = st ? st + 2 : nullptr;
+            q.stamps = st ? st + 4 : nullptr;
             q.p_istride = pis;
             q.e_istride = eis;
             q.s_istride = (long long)seam_istride;
@@ -739,7 +744,7 @@ void run_carve(Ctx& c, const uint8_t* d_in, uint8_t* d_out, int nimg, const Carv
             } else {
                 // the last removal writes the next layout directly (3 B RGB read + 3 B written per pixel)
                 Prof pr(c, s, KK_COMPACT, 3.0 * H * (2.0 * W - 1) * nimg);
-                unsigned long long* cst = st ? st + 2 : nullptr;
+                unsigned long long* cst = st ? st + 4 : nullptr;
                 const long long ls = (long long)seam_istride, lst = (long long)sw;
                 if (finish == OUT_PLANE)
                     launch_compact_transpose<OUT_PLANE>(rgb[cur], pitch, W, H, seam, rgb[cur ^ 1], g.pitch_b, nullptr,
@@ -818,13 +823,15 @@ void validate_seam_host(const int32_t* seam, int n, int w, int h) {
     }
 }
 
-// stamps -> per-seam timings (energy is folded into the DP: reported as 0)
+// stamps -> per-seam timings (SeamTiming, carver.hpp:23-27): a lap is 0 where its
+// stamps were not written (the work is fused into another kernel)
 void stamps_to_timings(const std::vector<unsigned long long>& st, int nseams, carve_seam_timing* timings) {
+    auto lap = [](unsigned long long a, unsigned long long b) { return a && b > a ? double(b - a) * 1e-9 : 0.0; };
     for (int k = 0; k < nseams; ++k) {
-        const unsigned long long* q = &st[size_t(k) * 4];
-        timings[k].energy_s = 0.0;
-        timings[k].solve_s = q[1] > q[0] ? double(q[1] - q[0]) * 1e-9 : 0.0;
-        timings[k].remove_s = q[3] > q[2] ? double(q[3] - q[2]) * 1e-9 : 0.0;
+        const unsigned long long* q = &st[size_t(k) * kStampsPerSeam];
+        timings[k].energy_s = lap(q[0], q[1]);
+        timings[k].solve_s = lap(q[2], q[3]);
+        timings[k].remove_s = lap(q[4], q[5]);
     }
 }
 
@@ -1273,6 +1280,12 @@ carve_status carve_cuda_record_seams(const uint8_t* rgb, int w, int h, int count
 
 carve_status carve_cuda_enlarge(const uint8_t* rgb, int w, int h, int target_w, int target_h,
                                 const carve_cuda_config* cfg, uint8_t* rgb_out, int32_t* seams_out) {
+    return carve_cuda_enlarge_timed(rgb, w, h, target_w, target_h, cfg, rgb_out, seams_out, nullptr);
+}
+
+carve_status carve_cuda_enlarge_timed(const uint8_t* rgb, int w, int h, int target_w, int target_h,
+                                      const carve_cuda_config* cfg, uint8_t* rgb_out, int32_t* seams_out,
+                                      carve_seam_timing* timings_out) {
     return guarded([&] {
         if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "PixelGrid dimensions must be >= 1");
         if (target_w != w) check_enlarge(w, target_w);
@@ -1288,17 +1301,24 @@ carve_status carve_cuda_enlarge(const uint8_t* rgb, int w, int h, int target_w, 
         uint8_t* e2 = static_cast<uint8_t*>(c.enl[2].ensure(big));
         const size_t nrec = size_t(kw) * h + size_t(kh) * target_w;
         int* d_orig = static_cast<int*>(c.rec.ensure(std::max<size_t>(nrec, 1) * 4));
+        // per-seam stamps of both recordings (the reports' per_seam, carver.hpp:299-309)
+        const size_t swa = size_t(kw) * kStampsPerSeam + 4, swb = size_t(kh) * kStampsPerSeam + 4;
+        unsigned long long* d_st = nullptr;
+        if (timings_out && (kw > 0 || kh > 0)) {
+            d_st = static_cast<unsigned long long*>(c.stamps.ensure((swa + swb) * 8));
+            ck(cudaMemsetAsync(d_st, 0, (swa + swb) * 8, c.stream), "memset stamps");
+        }
         ck(cudaMemcpyAsync(d_in, rgb, size_t(w) * h * 3, cudaMemcpyHostToDevice, c.stream), "H2D");
         const uint8_t* cur = d_in;
         if (kw > 0) {  // enlarge_to_width (carver.hpp:266-285)
-            record_device(c, d_in, w, h, kw, d_orig, nullptr, o);
+            record_device(c, d_in, w, h, kw, d_orig, d_st, o);
             launch_expand_rows(d_in, w, h, d_orig, kw, h, e0, c.stream);
             cur = e0;
         }
         if (kh > 0) {  // the height: enlarge_to_width of the transpose (cli.hpp:271-274)
             int* d_orig_h = d_orig + size_t(kw) * h;
             transpose_packed(c, cur, target_w, h, e1p);  // h wide, target_w high
-            record_device(c, e1p, h, target_w, kh, d_orig_h, nullptr, o);
+            record_device(c, e1p, h, target_w, kh, d_orig_h, d_st ? d_st + swa : nullptr, o);
             launch_expand_rows(e1p, h, target_w, d_orig_h, kh, target_w, e2, c.stream);
             transpose_packed(c, e2, target_h, target_w, d_out);
             cur = d_out;
@@ -1306,7 +1326,17 @@ carve_status carve_cuda_enlarge(const uint8_t* rgb, int w, int h, int target_w, 
         ck(cudaMemcpyAsync(rgb_out, cur, big, cudaMemcpyDeviceToHost, c.stream), "D2H");
         if (seams_out && nrec)
             ck(cudaMemcpyAsync(seams_out, d_orig, nrec * 4, cudaMemcpyDeviceToHost, c.stream), "D2H seams");
+        std::vector<unsigned long long> st;
+        if (d_st) {
+            st.resize(swa + swb);
+            ck(cudaMemcpyAsync(st.data(), d_st, st.size() * 8, cudaMemcpyDeviceToHost, c.stream), "D2H stamps");
+        }
         sync(c);
+        if (d_st) {
+            std::vector<unsigned long long> b(st.begin() + swa, st.end());
+            stamps_to_timings(st, kw, timings_out);
+            stamps_to_timings(b, kh, timings_out + kw);
+        }
     });
 }
 
@@ -1535,11 +1565,13 @@ carve_status carve_cuda_apply_mask(const double* e, int w, int h, const uint8_t*
     });
 }
 
-carve_status carve_cuda_remove_object(const uint8_t* rgb, int w, int h, const uint8_t* mask,
-                                      const carve_cuda_config* cfg, int restore, uint8_t* rgb_out, int* out_w,
-                                      int* out_h, int32_t* seams_out, int* nseams) {
+carve_status carve_cuda_remove_object_ex(const uint8_t* rgb, int w, int h, const uint8_t* mask,
+                                         const carve_cuda_config* cfg, int restore, int orientation,
+                                         uint8_t* rgb_out, int* out_w, int* out_h, int32_t* seams_out, int* nseams,
+                                         carve_seam_timing* timings_out) {
     return guarded([&] {
         if (w < 1 || h < 1) fail(CARVE_E_EMPTY_IMAGE, "PixelGrid dimensions must be >= 1");
+        if (orientation < 0 || orientation > 1) fail(CARVE_E_USAGE_ERROR, "orientation must be 0 (auto) or 1");
         const CarveOpts o = opts_of(cfg);
         // mask_bounds (energy.hpp:272-283) of the caller's flags: picks the orientation
         int top = h, left = w, bottom = -1, right = -1;
@@ -1551,8 +1583,10 @@ carve_status carve_cuda_remove_object(const uint8_t* rgb, int w, int h, const ui
                     bottom = std::max(bottom, i);
                     right = std::max(right, j);
                 }
-        if (bottom < top) fail(CARVE_E_EMPTY_MASK, "removal mask marks no pixels");
-        const bool transposed = right - left + 1 > bottom - top + 1;
+        // remove_object fails on an empty mask (carver.hpp:333); remove_object_vertical
+        // (orientation 1) just carves nothing (its loop condition, carver.hpp:297)
+        if (bottom < top && orientation == 0) fail(CARVE_E_EMPTY_MASK, "removal mask marks no pixels");
+        const bool transposed = orientation == 0 && right - left + 1 > bottom - top + 1;
         Ctx& c = ctx();
         cudaStream_t s = c.stream;
         const size_t n = size_t(w) * h;
@@ -1567,11 +1601,18 @@ carve_status carve_cuda_remove_object(const uint8_t* rgb, int w, int h, const ui
         double* eb = static_cast<double*>(c.e[1].ensure(plane * 8)) + EPAD_L;
         // the removal's seam log (c.seams belongs to the carve loop the restore runs)
         int* d_seams = static_cast<int*>(c.dir.ensure(std::max<size_t>(n, 1) * 4));
-        MaskStats* st = static_cast<MaskStats*>(c.stats.ensure(sizeof(MaskStats)));
+        MaskStats* st = static_cast<MaskStats*>(c.stats.ensure(sizeof(MaskStats) + 64));
+        int* d_flags = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(st) + sizeof(MaskStats) + 32);  // done, count
+        unsigned long long* d_st = nullptr;
+        if (timings_out) {
+            d_st = static_cast<unsigned long long*>(c.stamps.ensure(size_t(W) * kStampsPerSeam * 8));
+            ck(cudaMemsetAsync(d_st, 0, size_t(W) * kStampsPerSeam * 8, s), "memset stamps");
+        }
         const int mpitch = epitch;
         double* mb = static_cast<double*>(c.mbound.ensure(size_t((H + LBLK - 1) / LBLK + 1) * mpitch * 8));
         ck(cudaMemcpyAsync(d_in, rgb, n * 3, cudaMemcpyHostToDevice, s), "H2D rgb");
         ck(cudaMemcpyAsync(d_mask, mask, n, cudaMemcpyHostToDevice, s), "H2D mask");
+        ck(cudaMemsetAsync(d_flags, 0, 8, s), "memset flags");
         if (!transposed) {
             k_unpack_masked<<<grid_for((long long)n, 256), 256, 0, s>>>(d_in, d_mask, w, h, rgbx, pitch);
             LAUNCHED("k_unpack_masked");
@@ -1586,50 +1627,79 @@ carve_status carve_cuda_remove_object(const uint8_t* rgb, int w, int h, const ui
         launch_energy(rgbx, pitch, W, H, e, epitch, 1, 0, 0, s);
         launch_fill_pads(e, epitch, W, H, 1, 0, s);
         launch_fill_pads(eb, epitch, W, H, 1, 0, s);
-        unsigned long long* h_marked = nullptr;
-        ck(cudaMallocHost(&h_marked, sizeof(unsigned long long)), "cudaMallocHost");
-        std::unique_ptr<unsigned long long, decltype(&cudaFreeHost)> guard_marked(h_marked, cudaFreeHost);
-        // remove_object_vertical (carver.hpp:291-315), one seam per iteration:
-        // stats -> (stop?) -> biased map -> DP -> removal of image, mask and map -> fix-up
-        int cw = W, ns = 0;
+        // remove_object_vertical (carver.hpp:291-315), one seam per iteration: stats ->
+        // stop test -> biased map -> DP -> removal of image, mask and map -> fix-up.
+        // The loop length is data-dependent; iterations are enqueued in batches without
+        // a host round trip per seam: k_mask_decide sets a device flag once no marked
+        // pixel is left, and every later kernel of the batch returns at once. The host
+        // reads the flag once per batch (batch sizes start at the mask's bounding-box
+        // width and double).
+        int cw = W, issued = 0, ns = 0, batch = std::max(1, bottom < top ? 1 : (transposed ? bottom - top : right - left) + 1);
+        int done = 0;
+        const int* stop = d_flags;
         for (;;) {
-            ck(cudaMemsetAsync(st, 0, sizeof(MaskStats), s), "memset stats");
-            k_mask_stats<false><<<grid_for((long long)cw * H, 256), 256, 0, s>>>(e, epitch, nullptr, rgbx, pitch, cw,
-                                                                                H, st);
-            LAUNCHED("k_mask_stats");
-            ck(cudaMemcpyAsync(h_marked, &st->marked, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s),
-               "D2H marked");
+            const int nb = std::min(batch, cw - 1);  // every iteration of the batch starts at width >= 2
+            for (int b = 0; b < nb; ++b, ++issued, --cw) {
+                unsigned long long* sk = d_st ? d_st + size_t(issued) * kStampsPerSeam : nullptr;
+                ck(cudaMemsetAsync(st, 0, sizeof(MaskStats), s), "memset stats");
+                k_mask_stats<false><<<grid_for((long long)cw * H, 256), 256, 0, s>>>(e, epitch, nullptr, rgbx, pitch,
+                                                                                    cw, H, st, stop, sk);
+                LAUNCHED("k_mask_stats");
+                k_mask_decide<<<1, 1, 0, s>>>(st, d_flags, d_flags + 1);
+                LAUNCHED("k_mask_decide");
+                k_apply_mask<false><<<grid_for((long long)cw * H, 256), 256, 0, s>>>(
+                    e, epitch, nullptr, rgbx, pitch, cw, H, st, eb, epitch, 1, stop, sk ? sk + 1 : nullptr);
+                LAUNCHED("k_apply_mask");
+                int* seam = d_seams + size_t(issued) * H;
+                const Dp2Plan pl = dp2_plan(cw, H);
+                Dp2Params q{};
+                q.e = eb;
+                q.epitch = epitch;
+                q.W = cw;
+                q.H = H;
+                q.mbound = mb;
+                q.mpitch = mpitch;
+                q.seam = seam;
+                q.stop = stop;
+                q.stamps = sk;
+                launch_dp2(c, pl, q, 1, s);
+                CompactParams r{};
+                r.rgb_in = r.rgb_out = rgbx;
+                r.e_in = r.e_out = e;
+                r.pitch = pitch;
+                r.epitch = epitch;
+                r.W = cw;
+                r.H = H;
+                r.seam = seam;
+                r.stop = stop;
+                r.stamps = sk ? sk + 4 : nullptr;
+                launch_compact_inplace(r, 1, s);
+                k_fixup_energy<<<grid_for(H, 256), 256, 0, s>>>(e, epitch, rgbx, pitch, cw - 1, H, seam, stop,
+                                                                sk ? sk + 5 : nullptr);
+                LAUNCHED("k_fixup_energy");
+            }
+            int hv[2];
+            ck(cudaMemcpyAsync(hv, d_flags, 8, cudaMemcpyDeviceToHost, s), "D2H flags");
             sync(c);
-            if (*h_marked == 0) break;
-            if (cw < 2) fail(CARVE_E_WIDTH_TOO_SMALL, "mask cannot be carved out of a 1-pixel-wide image");
-            k_apply_mask<false><<<grid_for((long long)cw * H, 256), 256, 0, s>>>(e, epitch, nullptr, rgbx, pitch, cw,
-                                                                                H, st, eb, epitch, 1);
-            LAUNCHED("k_apply_mask");
-            int* seam = d_seams + size_t(ns) * H;
-            const Dp2Plan pl = dp2_plan(cw, H);
-            Dp2Params q{};
-            q.e = eb;
-            q.epitch = epitch;
-            q.W = cw;
-            q.H = H;
-            q.mbound = mb;
-            q.mpitch = mpitch;
-            q.seam = seam;
-            launch_dp2(c, pl, q, 1, s);
-            CompactParams r{};
-            r.rgb_in = r.rgb_out = rgbx;
-            r.e_in = r.e_out = e;
-            r.pitch = pitch;
-            r.epitch = epitch;
-            r.W = cw;
-            r.H = H;
-            r.seam = seam;
-            launch_compact_inplace(r, 1, s);
-            --cw;
-            k_fixup_energy<<<grid_for(H, 256), 256, 0, s>>>(e, epitch, rgbx, pitch, cw, H, seam);
-            LAUNCHED("k_fixup_energy");
-            ++ns;
+            done = hv[0];
+            ns = hv[1];
+            if (done) break;
+            if (cw < 2) {
+                // width 1 with marked pixels left (carver.hpp:298-299), unless the last
+                // batch's final seam removed them: one more stop test at width 1
+                ck(cudaMemsetAsync(st, 0, sizeof(MaskStats), s), "memset stats");
+                k_mask_stats<false><<<grid_for((long long)cw * H, 256), 256, 0, s>>>(e, epitch, nullptr, rgbx, pitch,
+                                                                                    cw, H, st, stop, nullptr);
+                LAUNCHED("k_mask_stats");
+                unsigned long long marked = 0;
+                ck(cudaMemcpyAsync(&marked, &st->marked, 8, cudaMemcpyDeviceToHost, s), "D2H marked");
+                sync(c);
+                if (marked) fail(CARVE_E_WIDTH_TOO_SMALL, "mask cannot be carved out of a 1-pixel-wide image");
+                break;
+            }
+            batch *= 2;
         }
+        cw = W - ns;  // the width after the last seam actually carved
         // restore (carver.hpp:309-313): enlarge_to_width back to the original width
         uint8_t* d_cur = static_cast<uint8_t*>(c.packed_out.ensure(n * 3));
         launch_pack(c, rgbx, pitch, cw, H, false, d_cur, 1, 0, 0, s);
@@ -1654,9 +1724,22 @@ carve_status carve_cuda_remove_object(const uint8_t* rgb, int w, int h, const ui
         ck(cudaMemcpyAsync(rgb_out, res, size_t(rw) * H * 3, cudaMemcpyDeviceToHost, s), "D2H");
         if (seams_out && ns)
             ck(cudaMemcpyAsync(seams_out, d_seams, size_t(ns) * H * 4, cudaMemcpyDeviceToHost, s), "D2H seams");
+        std::vector<unsigned long long> sth;
+        if (timings_out && ns) {
+            sth.resize(size_t(ns) * kStampsPerSeam);
+            ck(cudaMemcpyAsync(sth.data(), d_st, sth.size() * 8, cudaMemcpyDeviceToHost, s), "D2H stamps");
+        }
         sync(c);
+        if (timings_out && ns) stamps_to_timings(sth, ns, timings_out);
         if (nseams) *nseams = ns;
     });
+}
+
+carve_status carve_cuda_remove_object(const uint8_t* rgb, int w, int h, const uint8_t* mask,
+                                      const carve_cuda_config* cfg, int restore, uint8_t* rgb_out, int* out_w,
+                                      int* out_h, int32_t* seams_out, int* nseams) {
+    return carve_cuda_remove_object_ex(rgb, w, h, mask, cfg, restore, 0, rgb_out, out_w, out_h, seams_out, nseams,
+                                       nullptr);
 }
 
 carve_status carve_cuda_carve_device(const uint8_t* d_rgb, int w, int h, int target_w, int target_h, uint8_t* d_out,

@@ -49,6 +49,15 @@ __device__ __forceinline__ uint64_t globaltimer() {
     return t;
 }
 
+// Optional end-of-kernel timestamp: thread 0 of every block raises *p to its exit
+// time on every return path (the kernel's end = the last block's exit).
+struct EndStamp {
+    unsigned long long* p;
+    __device__ ~EndStamp() {
+        if (p && threadIdx.x == 0) atomicMax(p, (unsigned long long)globaltimer());
+    }
+};
+
 // raster.hpp:68 — 0.299*r + 0.587*g + 0.114*b, left to right, no contraction.
 // byte `B` of p as an exact double: one I2F.F64.U8 with a byte selector (R.B1,
 // R.B2) instead of shift + mask + I2F.F64.U32 (5 integer ops per pixel saved)
@@ -266,7 +275,12 @@ constexpr int K1S_C = 4, K1S_COLS = 32 * K1S_C;
 template <int MINB, int PF>
 __global__ void __launch_bounds__(256, MINB) k_energy_rows(const uint32_t* __restrict__ rgb, int pitch, int W, int H,
                                                      double* __restrict__ e, int epitch, long long rgb_istride,
-                                                     long long e_istride, int nstrips, int R) {
+                                                     long long e_istride, int nstrips, int R,
+                                                     unsigned long long* stamps = nullptr, long long st_is = 0) {
+    // optional [start, end] stamps of the phase's first seam (its energy_s)
+    if (stamps && blockIdx.x == 0 && threadIdx.x == 0)
+        atomicCAS(&stamps[blockIdx.y * st_is], 0ull, (unsigned long long)globaltimer());
+    EndStamp end_stamp{stamps ? stamps + blockIdx.y * st_is + 1 : nullptr};
     const int lane = threadIdx.x & 31;
     const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int strip = gw % nstrips, i0 = (gw / nstrips) * R;
@@ -469,6 +483,7 @@ struct CompactParams {
     const int* seam;
     unsigned long long* stamps;  // optional [start, end] per image (written by block 0 / last block)
     long long p_istride, e_istride, s_istride, st_istride;
+    const int* stop;  // optional device flag: nonzero = return at once (data-dependent loops)
 };
 
 // One thread per 4-pixel output chunk: 128-bit RGBX load + the next pixel,
@@ -905,6 +920,7 @@ __global__ void __launch_bounds__(128) k_compact_bulk(CompactParams p, int rows_
     __syncthreads();
     pdl_wait();  // the DP that produced this seam has completed
     pdl_launch_dependents();
+    if (p.stop && *p.stop) return;  // uniform over the grid (set by an earlier kernel)
     if (p.stamps && blockIdx.x == 0 && threadIdx.x == 0)
         atomicCAS(&p.stamps[img * p.st_istride + 0], 0ull, (unsigned long long)globaltimer());
     // row r's moving part: 16-byte aligned from a = floor4(s) to W (rounded up to 4 pixels;
@@ -1019,7 +1035,10 @@ __device__ __forceinline__ bool masked_at(const uint8_t* m8, const uint32_t* rgb
 
 template <bool U8>
 __global__ void k_mask_stats(const double* __restrict__ e, int epitch, const uint8_t* __restrict__ m8,
-                             const uint32_t* __restrict__ rgb, int rpitch, int W, int H, MaskStats* st) {
+                             const uint32_t* __restrict__ rgb, int rpitch, int W, int H, MaskStats* st,
+                             const int* stop = nullptr, unsigned long long* stamps = nullptr) {
+    if (stop && *stop) return;
+    if (stamps && blockIdx.x == 0 && threadIdx.x == 0) atomicCAS(stamps, 0ull, (unsigned long long)globaltimer());
     unsigned long long mu = 0, ma = 0, cnt = 0;
     int any = 0;
     const long long n = (long long)W * H;
@@ -1060,10 +1079,21 @@ __device__ __forceinline__ double mask_bias(const MaskStats* st, int H) {
 
 // biased map (energy.hpp:237-240): masked cells -> -k; in the carve loop also
 // column W (the one the last removal vacated) -> +inf pad
+// the removal loop's stop test, one thread: no marked pixel left -> *done = 1 (every
+// later kernel of the loop returns at once); else one more seam (*count)
+__global__ void k_mask_decide(const MaskStats* st, int* done, int* count) {
+    if (*done) return;
+    if (st->marked == 0) *done = 1;
+    else ++*count;
+}
+
 template <bool U8>
 __global__ void k_apply_mask(const double* __restrict__ e, int epitch, const uint8_t* __restrict__ m8,
                              const uint32_t* __restrict__ rgb, int rpitch, int W, int H, const MaskStats* st,
-                             double* __restrict__ out, int opitch, int pad_col) {
+                             double* __restrict__ out, int opitch, int pad_col, const int* stop = nullptr,
+                             unsigned long long* stamp_end = nullptr) {
+    if (stop && *stop) return;
+    EndStamp end_stamp{stamp_end};
     const double negk = -mask_bias(st, H);
     const long long n = (long long)W * H;
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
@@ -1077,7 +1107,10 @@ __global__ void k_apply_mask(const double* __restrict__ e, int epitch, const uin
 // Appendix A.4), standalone: the object-removal loop solves on a biased copy,
 // so the DP prologue's in-place fix-up does not apply there.
 __global__ void k_fixup_energy(double* __restrict__ e, int epitch, const uint32_t* __restrict__ rgb, int rpitch, int W,
-                               int H, const int* __restrict__ seam) {
+                               int H, const int* __restrict__ seam, const int* stop = nullptr,
+                               unsigned long long* stamp_end = nullptr) {
+    if (stop && *stop) return;
+    EndStamp end_stamp{stamp_end};
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < H; i += gridDim.x * blockDim.x) {
         const int sp = seam[i];
         const uint32_t* row = rgb + (long long)i * rpitch;

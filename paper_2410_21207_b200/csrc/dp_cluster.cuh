@@ -64,7 +64,8 @@ struct Dp2Params {
     int* seam;         // H ints, image stride s_istride
     double* m_out;     // optional full cost table (pitch W)
     int* b_out;        // optional predecessor table (pitch W)
-    unsigned long long* stamps;  // optional [start, end]
+    unsigned long long* stamps;  // optional per-seam record [energy start, energy end, solve start, solve end, ...]
+    const int* stop;             // optional device flag: nonzero = return at once (data-dependent loops)
     long long e_istride, mb_istride, s_istride, st_istride;
     int dbg;           // debugging: bit0 skips phase 2, bit1 skips phase 1, bit2 skips the walk
     long long* prof;   // MODE 2 only: [G][8] per-warp clock64 counters
@@ -347,7 +348,13 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
 
     pdl_wait();  // the previous removal has completed (its planes and seam log are visible)
     pdl_launch_dependents();
-    if (p.stamps && cta == 0 && threadIdx.x == 0) p.stamps[img * p.st_istride + 0] = globaltimer();
+    // a data-dependent loop (object removal) enqueued past its end: every CTA reads the
+    // same flag (set by a kernel that completed before this one), so all return together
+    if (p.stop && *p.stop) return;
+    // energy = the prologue's incremental fix-up (seams after a phase's first; the first
+    // seam's energy is the K1 launch), solve = the rest of this launch
+    if (p.stamps && cta == 0 && threadIdx.x == 0)
+        p.stamps[img * p.st_istride + (p.prev_seam ? 0 : 2)] = globaltimer();
 
     // K1 fix-up of the previous removal: rows are
     // spread over every thread of the cluster; made visible by the barrier below
@@ -411,6 +418,11 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
     // every fix-up store is visible before any energy row is read
     if (ncl > 1) cluster.sync();
     else __syncthreads();
+    if (p.stamps && p.prev_seam && cta == 0 && threadIdx.x == 0) {
+        const unsigned long long t = globaltimer();
+        p.stamps[img * p.st_istride + 1] = t;
+        p.stamps[img * p.st_istride + 2] = t;
+    }
 
     // fused mode: rolling luma rows (i-1, i, i+1) of my columns; rows clamp at the borders
     double Lp[C], Lc[C], Ln[C];
@@ -957,7 +969,7 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
     if (p.stamps) {
         if (ncl > 1) cluster.sync();
         else __syncthreads();
-        if (cta == 0 && threadIdx.x == 0) p.stamps[img * p.st_istride + 1] = globaltimer();
+        if (cta == 0 && threadIdx.x == 0) p.stamps[img * p.st_istride + 3] = globaltimer();
     }
 }
 

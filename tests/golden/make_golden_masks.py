@@ -56,6 +56,26 @@ def main() -> None:
         out[f"mfi{k}"] = ref.mask_from_image(img)
         k += 1
     out["n"] = np.array(k)
+    # round 2: detail::remove_object_vertical (carver.hpp:289-321) on masks of any
+    # shape, wider than tall and empty included (no orientation choice, no empty check)
+    rng2 = np.random.default_rng(0x3A5D)
+    nv = 0
+    for t in range(24):
+        h, w = (int(v) for v in rng2.integers(3, 18, 2))
+        img = rng2.integers(0, 256, (h, w, 3), dtype=np.uint8) if t % 2 else ref.make_test_image(w, h)
+        mask = np.zeros((h, w), np.uint8)
+        if t % 8:
+            top, left = int(rng2.integers(0, h)), int(rng2.integers(0, w))
+            mask[top:top + int(rng2.integers(1, 3)), left:left + int(rng2.integers(1, w - left + 1))] = 1  # wide
+        restore = bool(t % 3)
+        try:
+            res, seams, n = ref.remove_object_vertical(img, mask, restore)
+        except oracle.OracleError as ex:
+            res, seams, n = np.zeros((0, 0, 3), np.uint8), np.zeros(0, np.int32), -ex.status
+        out[f"vimg{nv}"], out[f"vmask{nv}"], out[f"vrestore{nv}"] = img, mask, np.array(int(restore), np.int32)
+        out[f"vres{nv}"], out[f"vseams{nv}"], out[f"vn{nv}"] = res, seams, np.array(n, np.int32)
+        nv += 1
+    out["nvert"] = np.array(nv)
     np.savez_compressed(os.path.join(HERE, "masks.npz"), **out)
 
     path = os.path.join(HERE, "golden.json")

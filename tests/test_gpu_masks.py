@@ -120,3 +120,35 @@ def test_remove_object_reference_cases():
     m = cv.mask_from_image(img)
     assert m.sum() == 2 and m[1, 2] and m[2, 1]
     assert cv.mask_bounds(m) == (1, 1, 2, 2)
+
+
+def test_remove_object_vertical_golden():
+    """detail::remove_object_vertical (carver.hpp:289-321) against the reference:
+    the column loop whatever the mask's shape, an empty mask carves nothing."""
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "masks.npz"))
+    for k in range(int(z["nvert"])):
+        img, mask, restore = z[f"vimg{k}"], z[f"vmask{k}"], bool(z[f"vrestore{k}"])
+        n = int(z[f"vn{k}"])
+        if n < 0:
+            with pytest.raises(cv.CarveError) as ei:
+                cv.remove_object_vertical(img, mask, restore=restore)
+            assert ei.value.code == -n, k
+            continue
+        out, rep = cv.remove_object_vertical(img, mask, restore=restore)
+        assert rep.seam_count == n, k
+        assert np.array_equal(out, z[f"vres{k}"]), k
+        flat = np.concatenate(rep.seams) if rep.seams else np.zeros(0, np.int32)
+        assert np.array_equal(flat, z[f"vseams{k}"][: flat.size]), k
+
+
+def test_remove_object_report_timings():
+    """The report's per-seam laps (carver.hpp:299-309) come from device timestamps:
+    energy (mask statistics + biased map), solve (DP), remove (removal + fix-up)."""
+    img = cv.make_test_image(96, 64)
+    mask = np.zeros((64, 96), np.uint8)
+    mask[10:50, 40:47] = 1
+    out, rep = cv.remove_object(img, mask, restore=False)
+    assert rep.seam_count >= 7 and len(rep.per_seam) == rep.seam_count
+    for t in rep.per_seam:
+        assert t.energy_s > 0 and t.solve_s > 0 and t.remove_s > 0
+    assert rep.total_s >= sum(t.energy_s + t.solve_s + t.remove_s for t in rep.per_seam)

@@ -405,3 +405,18 @@ def test_remove_seam_planes_errors():
             assert ei.value.code == cv.Errc.invalid_seam
     # width 1 -> width 0 (the reference's drop_columns yields an empty grid)
     assert cv.remove_seam(np.ones((5, 1)), [0] * 5).shape == (5, 0)
+
+
+def test_carve_report_timings_are_device_laps(monkeypatch):
+    """SeamTiming (carver.hpp:23-27) from device timestamps: a phase's first seam's
+    energy is the K1 map, later seams' the DP prologue's 2-column fix-up; solve is
+    the DP, remove the removal kernel. Fused batches compute energy inside the DP."""
+    img = cv.make_test_image(300, 200)
+    out, seams, tim = cv.carve(img, 280, 190, seams=True, timings=True)
+    assert len(tim) == 30
+    for t in tim:
+        assert t.energy_s > 0 and t.solve_s > 0 and t.remove_s > 0
+    _, rep = cv.carve_to_width(img, 290, cv.CarveConfig(forward=True))
+    assert all(t.energy_s == 0 and t.solve_s > 0 and t.remove_s > 0 for t in rep.per_seam)
+    _, rep = cv.enlarge_to_width(img, 310)
+    assert len(rep.per_seam) == 10 and all(t.solve_s > 0 for t in rep.per_seam)
