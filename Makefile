@@ -8,7 +8,8 @@ NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -fmad=false -Xcompiler -fPIC -Xptxas
 PKG := paper_2410_21207_b200
 LIB := $(PKG)/libcarve_cuda.so
 # the DP variant instances compile in their own translation units (in parallel: make -j)
-SRCS := $(PKG)/csrc/carve_cuda.cu $(PKG)/csrc/dp_variants_a.cu $(PKG)/csrc/dp_variants_b.cu $(PKG)/csrc/dp_variants_c.cu
+SRCS := $(PKG)/csrc/carve_cuda.cu $(PKG)/csrc/dp_variants_a.cu $(PKG)/csrc/dp_variants_b.cu $(PKG)/csrc/dp_variants_c.cu \
+        $(PKG)/csrc/dp_variants_d.cu
 OBJS := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRCS))
 HDR := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.h) include/carve_cuda.h
 

@@ -102,6 +102,7 @@ struct Ctx {
     cudaStream_t stream = nullptr;
     DevBuf packed_in, packed_out, rgb[2], e[2], dir, seams, stamps, scratch_a, scratch_b, mbound;
     DevBuf rec, enl[3];  // recorded seams (original coordinates), enlargement intermediates
+    DevBuf glab;         // DP label tables in global memory (images whose table exceeds shared memory)
     DevBuf stats;        // object removal: MaskStats
     int max_smem_optin = 0;
     std::map<const void*, int> smem_set;  // kernel -> dynamic smem attribute set
@@ -333,6 +334,7 @@ const std::vector<Dp2Variant>& dp2_variants() {
         dp2_variants_a(t);
         dp2_variants_b(t);
         dp2_variants_c(t);
+        dp2_variants_d(t);
         return t;
     }();
     return v;
@@ -360,6 +362,7 @@ struct Dp2Plan {
     int ncl, nblk;
     size_t smem;
     int gather;  // label table gathered into CTA 0 (fits in shared memory)
+    int glab;    // label table in global memory (does not fit in shared memory)
 };
 
 int env_int(const char* name, int dflt) {
@@ -371,13 +374,13 @@ int env_int(const char* name, int dflt) {
 // profiles/r01_dp_variant_sweep.jsonl): the first variant whose cluster fits
 // wins. Single images are latency-bound and favour one C=2 warp per
 // scheduler; batches are throughput-bound and favour less halo redundancy.
-const int kDp2Order[] = {0, 12, 1, 11, 10, 2, 3, 4, 6, 5, 7, 8};
+const int kDp2Order[] = {0, 12, 1, 11, 10, 2, 3, 4, 6, 5, 7, 8, 13, 14, 15, 16};
 // large batches (>= one image per SM): one 10-warp CTA per image, 2 per SM;
 // smaller batches spread each image over a 3-CTA cluster to fill the SMs
 // (measured, tools/sweep_batch.py: 1024 images 2.05 -> 1.58 ms per seam with
 // variant 9 <4,8,10,4>; 128 images 0.32 (v9) vs 0.28 ms (v5))
-const int kDp2BatchOrder[] = {9, 5, 6, 0, 1, 2, 3, 4, 7, 8};
-const int kDp2SmallBatchOrder[] = {5, 6, 0, 1, 2, 3, 4, 7, 8};
+const int kDp2BatchOrder[] = {9, 5, 6, 0, 1, 2, 3, 4, 7, 8, 13, 14, 15, 16};
+const int kDp2SmallBatchOrder[] = {5, 6, 0, 1, 2, 3, 4, 7, 8, 13, 14, 15, 16};
 
 int device_sm_count() {
     int dev = 0, nsm = 0;
@@ -398,7 +401,13 @@ Dp2Plan dp2_plan(int W, int H, bool batch = false, int ring = RING_ENERGY, int n
     const int nblk = H > 1 ? (H - 1 + LBLK - 1) / LBLK : 0;
     const int forced = env_int("CARVE_DP_VARIANT", -1);
     const int max_ncl = env_int("CARVE_DP_MAX_NCL", 16);
-    for (int pass = 0; pass < 2; ++pass) {
+    // passes: label table in shared memory (preferred cluster sizes, then up to 16
+    // CTAs), then the global-memory-table instances (tall or wide images; a forced
+    // CARVE_DP_VARIANT of those, or CARVE_DP_GLABELS=1, selects them directly)
+    const bool force_glab = env_int("CARVE_DP_GLABELS", 0) != 0 ||
+                            (forced >= 0 && forced < int(dp2_variants().size()) && dp2_variants()[forced].glab);
+    for (int pass = force_glab ? 2 : 0; pass < 3; ++pass) {
+        const bool glab = pass == 2;
         std::vector<int> order;
         if (forced >= 0 && forced < int(dp2_variants().size())) order.push_back(forced);
         else if (batch && (long long)nimg * t_concurrency >= device_sm_count()) order.assign(std::begin(kDp2BatchOrder), std::end(kDp2BatchOrder));
@@ -406,10 +415,12 @@ Dp2Plan dp2_plan(int W, int H, bool batch = false, int ring = RING_ENERGY, int n
         else order.assign(std::begin(kDp2Order), std::end(kDp2Order));
         for (int k : order) {
             const Dp2Variant& v = kDp2Variants[k];
+            if (v.glab != glab) continue;
             const int ncl = (W + v.cols() - 1) / v.cols();
-            const size_t smem = ring == RING_RGBX    ? v.smem_fused(nblk, v.D)
-                                : ring == RING_COSTS ? v.smem_costs(nblk, v.D)
-                                                     : v.smem(nblk, v.D);
+            const int nblk_smem = glab ? 0 : nblk;  // label rows kept on chip
+            const size_t smem = ring == RING_RGBX    ? v.smem_fused(nblk_smem, v.D)
+                                : ring == RING_COSTS ? v.smem_costs(nblk_smem, v.D)
+                                                     : v.smem(nblk_smem, v.D);
             if (ncl > (pass == 0 ? max_ncl : 16) || smem > size_t(kDpSmemBudget)) continue;
             // columns read past the image edge must stay inside the +inf pad
             if (ncl * v.cols() - W + v.K + 32 * v.C > EPAD_R) continue;
@@ -417,9 +428,9 @@ Dp2Plan dp2_plan(int W, int H, bool batch = false, int ring = RING_ENERGY, int n
             // batches, where the extra shared memory costs a CTA per SM (measured:
             // C5 2.33K -> 2.61K images/s without it) while phase 1 overlaps other images
             const size_t gbytes = round_up(size_t(nblk) * ncl * v.cols(), 16);
-            const bool gather = nblk > 0 && gbytes <= size_t(96) * 1024 && smem + gbytes <= size_t(kDpSmemBudget) &&
-                                env_int("CARVE_DP_GATHER", batch ? 0 : 1) != 0;
-            return Dp2Plan{&v, ncl, nblk, smem + (gather ? gbytes : 0), gather ? 1 : 0};
+            const bool gather = !glab && nblk > 0 && gbytes <= size_t(96) * 1024 &&
+                                smem + gbytes <= size_t(kDpSmemBudget) && env_int("CARVE_DP_GATHER", batch ? 0 : 1) != 0;
+            return Dp2Plan{&v, ncl, nblk, smem + (gather ? gbytes : 0), gather ? 1 : 0, glab ? 1 : 0};
         }
     }
     fail(CARVE_E_IMAGE_TOO_LARGE, "no DP cluster configuration fits width " + std::to_string(W) + " x height " +
@@ -432,6 +443,12 @@ void launch_dp2(Ctx& c, const Dp2Plan& pl, Dp2Params p, int nimg, cudaStream_t s
     p.G = pl.ncl * v.NW;
     p.nblk = pl.nblk;
     p.gather = pl.gather;
+    if (pl.glab) {
+        p.glab_istride = (long long)round_up(size_t(pl.nblk) * p.G * v.S(), 128);
+        p.glab = static_cast<int8_t*>(c.glab.ensure(size_t(std::max<long long>(p.glab_istride, 128)) * nimg));
+    } else {
+        p.glab = nullptr;
+    }
     p.dbg = env_int("CARVE_DP_DBG", 0);
     const void* fn = forward ? (fused ? (p.m_out ? v.fn_fwd_tables : v.fn_fwd) : (p.m_out ? v.fn_fwdp_tables : v.fn_fwdp))
                      : fused ? v.fn_fused : p.m_out ? v.fn_tables : (p.prof ? v.fn_prof : v.fn);
@@ -463,7 +480,14 @@ void launch_compact_bulk(cudaLaunchConfig_t cfg, const CompactParams& p, int nim
     // 2 slots; C4's 7680-wide rows: 2 slots, one CTA per SM)
     int slots = int(std::min<size_t>(CB_MAX_SLOTS, std::max<size_t>(2, (kCompactBulkSmem / 2) / slot_bytes)));
     slots = int(std::min<size_t>(size_t(slots), kCompactBulkSmem / slot_bytes));
-    if (slots < 1) fail(CARVE_E_IMAGE_TOO_LARGE, "row too wide for the bulk removal kernel");
+    if (slots < 1) {  // a row does not fit one shared-memory slot: warp-per-row removal
+        cfg.gridDim = dim3((p.H + 7) / 8, nimg);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = 0;
+        ck(cudaLaunchKernelEx(&cfg, k_compact_warp<4, HAS_E>, p), "launch k_compact_warp");
+        LAUNCHED("k_compact_warp");
+        return;
+    }
     cfg.gridDim = dim3((p.H + rpc - 1) / rpc, nimg);
     cfg.blockDim = dim3(128);
     cfg.dynamicSmemBytes = size_t(slots) * slot_bytes;

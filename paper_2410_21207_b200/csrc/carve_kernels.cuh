@@ -845,6 +845,7 @@ __global__ void __launch_bounds__(256) k_compact_warp(CompactParams p) {
     const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     pdl_wait();  // the DP that produced this seam has completed
     pdl_launch_dependents();
+    if (p.stop && *p.stop) return;  // uniform over the grid (set by an earlier kernel)
     if (p.stamps && blockIdx.x == 0 && threadIdx.x == 0)
         atomicCAS(&p.stamps[img * p.st_istride + 0], 0ull, (unsigned long long)globaltimer());
     if (i < p.H) {

@@ -79,6 +79,10 @@ struct Dp2Params {
     int gather;  // 1: CTA 0 holds a gathered copy of every CTA's block-end labels (phase 1 stays local)
     long long cplane;  // FWD without FUSED: element stride from the cost_left plane (e) to cost_up and
                        // from cost_up to cost_right (three padded planes of the same pitch)
+    // label table in global memory ([nblk][G*S] int8 offsets, image stride glab_istride)
+    // instead of shared memory: tall or wide images whose table does not fit on chip
+    int8_t* glab;
+    long long glab_istride;
 };
 
 // smem layout (dynamic): labels int8 [nblk][NWARP*S], aliased by the phase-2
@@ -308,7 +312,10 @@ __device__ __forceinline__ void argmin_combine(double& v, int& i, double ov, int
 // dp_seam_forward(gray, costs) API with arbitrary costs (solvers.hpp:294-326)
 // and the recompute=false forward loop, whose costs are carved, not recomputed
 // (carver.hpp:175-184).
-template <int C, int K, int NWARP, int D, int MODE, bool FUSED = false, bool FWD = false, int MINB = 1>
+// GLAB: the block-end label table lives in global memory (Dp2Params::glab) instead
+// of shared memory — separate instances for images whose table does not fit on chip.
+template <int C, int K, int NWARP, int D, int MODE, bool FUSED = false, bool FWD = false, int MINB = 1,
+          bool GLAB = false>
 __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
     constexpr bool TABLES = MODE == 1;
     constexpr bool PROF = MODE == 2;
@@ -337,7 +344,8 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
 
     int8_t* labels = reinterpret_cast<int8_t*>(dsm);
     uint8_t* p2 = dsm;  // phase-2 dirs alias the labels
-    double* mail_m = reinterpret_cast<double*>(dsm + SM::lp2_bytes(nblk));  // [2][NWARP][2][K]
+    int8_t* glab = GLAB ? p.glab + img * p.glab_istride : nullptr;  // global label table (else shared)
+    double* mail_m = reinterpret_cast<double*>(dsm + SM::lp2_bytes(GLAB ? 0 : nblk));  // [2][NWARP][2][K]
     int* mail_l = reinterpret_cast<int*>(mail_m + 2 * NWARP * 2 * K);
     double* red_v = reinterpret_cast<double*>(mail_l + 2 * NWARP * 2 * K);
     int* red_i = reinterpret_cast<int*>(red_v + 32);
@@ -582,12 +590,18 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
     const uint32_t lbl_s = smem_u32(labels + (col0 - cta_col0));
     double* mb_row = mbound + p.mpitch + col0;  // M row 32*(blk+1), advanced per label block
     auto block_end = [&](int i, int blk) {  // last row of a label block: labels to smem, M to global
+        if constexpr (GLAB) {  // the table lives in global memory
 #pragma unroll
-        for (int k = 0; k < C; ++k)
-            if (useful >> k & 1)
-                asm volatile("st.shared.u8 [%0], %1;" ::"r"(lbl_s + uint32_t(blk * SM::COLS + k)),
-                             "r"(uint32_t(lab[k] - (col0 + k)))
-                             : "memory");
+            for (int k = 0; k < C; ++k)
+                if (useful >> k & 1) glab[(long long)blk * (G * S) + col0 + k] = int8_t(lab[k] - (col0 + k));
+        } else {
+#pragma unroll
+            for (int k = 0; k < C; ++k)
+                if (useful >> k & 1)
+                    asm volatile("st.shared.u8 [%0], %1;" ::"r"(lbl_s + uint32_t(blk * SM::COLS + k)),
+                                 "r"(uint32_t(lab[k] - (col0 + k)))
+                                 : "memory");
+        }
         if (i != H - 1) {
 #pragma unroll
             for (int k = 0; k < C; ++k)
@@ -760,7 +774,12 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
         for (int r = 1; r < ncl; ++r) argmin_combine(bv, bi, cl_v[r], cl_i[r]);
         int c = bi;
         seam[H - 1] = c;
-        if (p.gather) {
+        if constexpr (GLAB) {  // written by every CTA before the cluster barrier: read through L2
+            for (int b = nblk - 1; b >= 0; --b) {
+                c += __ldcg(glab + (long long)b * GS + c);
+                if (b > 0) seam[LBLK * b] = c;  // row 32b = last row of block b-1
+            }
+        } else if (p.gather) {
             for (int b = nblk - 1; b >= 0; --b) {
                 c += gtab[b * GS + c];
                 if (b > 0) seam[LBLK * b] = c;  // row 32b = last row of block b-1

@@ -11,6 +11,7 @@ namespace carve_dev {
 
 struct Dp2Variant {
     int C, K, NW, D;
+    bool glab;             // label table in global memory (instances for oversized tables)
     const void* fn;        // hot kernel (no tables)
     const void* fn_tables; // parity-API kernel (writes the full cost / predecessor tables)
     const void* fn_prof;   // hot kernel + clock64 phase counters (tools)
@@ -27,25 +28,27 @@ struct Dp2Variant {
 };
 
 // MINB: resident CTAs per SM the register allocation must allow (batch variants)
-template <int C, int K, int NW, int D, int MINB = 1>
+// GLAB: label table in global memory
+template <int C, int K, int NW, int D, int MINB = 1, bool GLAB = false>
 Dp2Variant dp2_variant() {
-    return Dp2Variant{C, K, NW, D,
-                      (const void*)k_dp2<C, K, NW, D, 0, false, false, MINB>,
-                      (const void*)k_dp2<C, K, NW, D, 1, false, false, MINB>,
-                      (const void*)k_dp2<C, K, NW, D, 2, false, false, MINB>,
-                      (const void*)k_dp2<C, K, NW, D, 0, true, false, MINB>,
-                      (const void*)k_dp2<C, K, NW, D, 0, true, true, MINB>,
-                      (const void*)k_dp2<C, K, NW, D, 1, true, true, MINB>,
-                      (const void*)k_dp2<C, K, NW, D, 0, false, true, MINB>,
-                      (const void*)k_dp2<C, K, NW, D, 1, false, true, MINB>,
+    return Dp2Variant{C, K, NW, D, GLAB,
+                      (const void*)k_dp2<C, K, NW, D, 0, false, false, MINB, GLAB>,
+                      (const void*)k_dp2<C, K, NW, D, 1, false, false, MINB, GLAB>,
+                      (const void*)k_dp2<C, K, NW, D, 2, false, false, MINB, GLAB>,
+                      (const void*)k_dp2<C, K, NW, D, 0, true, false, MINB, GLAB>,
+                      (const void*)k_dp2<C, K, NW, D, 0, true, true, MINB, GLAB>,
+                      (const void*)k_dp2<C, K, NW, D, 1, true, true, MINB, GLAB>,
+                      (const void*)k_dp2<C, K, NW, D, 0, false, true, MINB, GLAB>,
+                      (const void*)k_dp2<C, K, NW, D, 1, false, true, MINB, GLAB>,
                       &Dp2Smem<C, K, NW, 8>::total,
                       &Dp2Smem<C, K, NW, 4>::total,
                       &Dp2Smem<C, K, NW, 24>::total};
 }
 
-// each appends its variants in index order (a: 0-3, b: 4-8, c: 9-)
+// each appends its variants in index order (a: 0-3, b: 4-8, c: 9-13, d: 14-)
 void dp2_variants_a(std::vector<Dp2Variant>& t);
 void dp2_variants_b(std::vector<Dp2Variant>& t);
 void dp2_variants_c(std::vector<Dp2Variant>& t);
+void dp2_variants_d(std::vector<Dp2Variant>& t);
 
 }  // namespace carve_dev

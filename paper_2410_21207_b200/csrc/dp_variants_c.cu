@@ -14,5 +14,7 @@ void dp2_variants_c(std::vector<Dp2Variant>& t) {
     t.push_back(dp2_variant<4, 16, 5, 8>());   // 10: S=96, 480 cols/CTA (smem fallback of 11)
     t.push_back(dp2_variant<4, 16, 5, 16>());  // 11: S=96, 480 cols/CTA, 16-row ring (C4: 16 CTAs)
     t.push_back(dp2_variant<2, 16, 5, 16>());  // 12: S=32, 160 cols/CTA (C3 height phase: 14 CTAs)
+    // 13: S=96, 1536 cols/CTA: widths above 12288 (up to 24576 in 16 CTAs)
+    t.push_back(dp2_variant<4, 16, 16, 8>());
 }
 }  // namespace carve_dev

@@ -305,7 +305,7 @@ def test_batch_two_pipelines_match_oracle(port):
             assert np.array_equal(outs[k], want[k % 41]), k
 
 
-@pytest.mark.parametrize("variant", range(13))
+@pytest.mark.parametrize("variant", range(17))
 def test_every_dp_variant_bitexact(port, monkeypatch, variant):
     """Each DP shape of the variant table (forced with CARVE_DP_VARIANT; the
     default order only reaches some of them at a given width): cost tables and
@@ -420,3 +420,31 @@ def test_carve_report_timings_are_device_laps(monkeypatch):
     assert all(t.energy_s == 0 and t.solve_s > 0 and t.remove_s > 0 for t in rep.per_seam)
     _, rep = cv.enlarge_to_width(img, 310)
     assert len(rep.per_seam) == 10 and all(t.solve_s > 0 for t in rep.per_seam)
+
+
+@pytest.mark.parametrize("w,h,tw,th", [(13000, 40, 12995, 37), (18000, 20, 17996, 20), (64, 40000, 60, 40000),
+                                       (300, 9000, 296, 9000)])
+def test_size_envelope_matches_oracle(port, w, h, tw, th):
+    """Beyond the on-chip limits of round 1: widths above 12288 (the 1536-column
+    CTA shape), rows wider than a removal slot (the warp-per-row removal), label
+    tables larger than shared memory (kept in global memory)."""
+    img = port.make_test_image(w, h)
+    want, ws = port.carve(img, tw, th, seams=True)
+    got, gs, _ = cv.carve(img, tw, th, seams=True)
+    assert np.array_equal(got, want)
+    assert np.array_equal(np.concatenate(gs), ws)
+
+
+def test_global_label_table_forced(port, monkeypatch):
+    """The global-memory label table (CARVE_DP_GLABELS=1) on ordinary sizes: tables,
+    seams and carves identical."""
+    monkeypatch.setenv("CARVE_DP_GLABELS", "1")
+    e = port.energy_e1_rgb(port.make_test_image(700, 300))
+    seam, m, b = port.dp_seam(e)
+    r = cv.dp_seam(e)
+    assert np.array_equal(r.seam, seam) and np.array_equal(r.table.b, b)
+    img = port.make_test_image(260, 140)
+    assert np.array_equal(cv.carve(img, 240, 120), port.carve(img, 240, 120))
+    imgs = [port.make_test_image(90, 60, k) for k in range(3)]
+    for o, x in zip(cv.carve_batch(imgs, 80, 55), imgs):
+        assert np.array_equal(o, port.carve(x, 80, 55))
