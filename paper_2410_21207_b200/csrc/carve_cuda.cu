@@ -21,6 +21,8 @@
 #include <thread>
 #include <vector>
 
+#include <unistd.h>  // environ
+
 namespace {
 
 using namespace carve_dev;
@@ -135,6 +137,14 @@ struct Ctx {
         max_smem_optin = int(prop.sharedMemPerBlockOptin);
         ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
     }
+    // CUDA graphs of whole device-resident carves (run_graphed), keyed by geometry, the
+    // buffers they touch and the CARVE_* environment
+    struct GraphEntry {
+        std::vector<uintptr_t> key;
+        cudaGraphExec_t exec;
+        uint64_t launches;
+    };
+    std::vector<GraphEntry> graphs;
     // batch pipelining: host->device and device->host copies on their own streams
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t pipe_ev[3][2] = {};  // [h2d done, compute done, d2h done][buffer]
@@ -147,6 +157,7 @@ struct Ctx {
             for (auto& e : row) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     }
     ~Ctx() {
+        for (auto& ge : graphs) cudaGraphExecDestroy(ge.exec);
         for (auto& row : pipe_ev)
             for (auto& e : row)
                 if (e) cudaEventDestroy(e);
@@ -906,6 +917,56 @@ void check_enlarge(int w, int target) {
     if (target > 2 * w - 1) fail(CARVE_E_TARGET_TOO_LARGE, "single-pass enlargement is limited to 2*width-1");
 }
 
+// One device-resident carve as a CUDA graph: the first call for a key captures the
+// launches (stream capture on the context stream, programmatic dependencies kept), later
+// calls replay the instantiated graph — no per-launch host work. The key also holds the
+// context's buffer addresses and the CARVE_* environment (which can change the plan);
+// kernel-event profiling and CARVE_SYNC_DEBUG run uncaptured, and so does any body that
+// fails to capture (e.g. a buffer growing mid-capture), retried once uncaptured.
+template <class F>
+void run_graphed(Ctx& c, std::vector<uintptr_t> key, F&& body) {
+    if (c.prof || sync_debug() || env_int("CARVE_GRAPH", 1) == 0) {
+        body();
+        return;
+    }
+    for (const DevBuf* b : {&c.rgb[0], &c.rgb[1], &c.e[0], &c.e[1], &c.mbound, &c.glab, &c.seams})
+        key.push_back(uintptr_t(b->p));
+    for (char** ev = environ; *ev; ++ev)
+        if (std::strncmp(*ev, "CARVE_", 6) == 0) key.push_back(std::hash<std::string>{}(*ev));
+    for (auto& ge : c.graphs)
+        if (ge.key == key) {
+            ck(cudaGraphLaunch(ge.exec, c.stream), "cudaGraphLaunch");
+            t_launches += ge.launches;
+            return;
+        }
+    const uint64_t l0 = t_launches;
+    cudaGraph_t graph = nullptr;
+    ck(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+    bool ok = true;
+    try {
+        body();
+    } catch (...) {
+        ok = false;
+    }
+    const cudaError_t ec = cudaStreamEndCapture(c.stream, &graph);
+    cudaGetLastError();  // a failed capture leaves a sticky-free error behind; clear it
+    cudaGraphExec_t exec = nullptr;
+    if (ok && ec == cudaSuccess && graph && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+        cudaGraphDestroy(graph);
+        ck(cudaGraphLaunch(exec, c.stream), "cudaGraphLaunch");
+        if (c.graphs.size() >= 8) {
+            cudaGraphExecDestroy(c.graphs.front().exec);
+            c.graphs.erase(c.graphs.begin());
+        }
+        c.graphs.push_back({std::move(key), exec, t_launches - l0});
+        return;
+    }
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    t_launches = l0;
+    body();  // uncaptured
+}
+
 void carve_one_host(Ctx& c, const uint8_t* rgb, int w, int h, int tw, int th, uint8_t* out, int32_t* seams_out,
                     carve_seam_timing* timings, CarveOpts o = {}) {
     const CarveGeometry g = geometry(w, h, tw, th);
@@ -921,7 +982,9 @@ void carve_one_host(Ctx& c, const uint8_t* rgb, int w, int h, int tw, int th, ui
         ck(cudaMemsetAsync(d_st, 0, stamp_words(g) * 8, s), "memset stamps");
     }
     ck(cudaMemcpyAsync(d_in, rgb, in_bytes, cudaMemcpyHostToDevice, s), "H2D rgb");
-    run_carve(c, d_in, d_out, 1, g, d_seams, g.seam_ints, d_st, s, o);
+    run_graphed(c, {uintptr_t(w), uintptr_t(h), uintptr_t(tw), uintptr_t(th), uintptr_t(d_in), uintptr_t(d_out),
+                    uintptr_t(d_seams), uintptr_t(d_st), uintptr_t(o.forward), uintptr_t(o.recompute)},
+                [&] { run_carve(c, d_in, d_out, 1, g, d_seams, g.seam_ints, d_st, s, o); });
     ck(cudaMemcpyAsync(out, d_out, out_bytes, cudaMemcpyDeviceToHost, s), "D2H rgb");
     if (seams_out && g.seam_ints)
         ck(cudaMemcpyAsync(seams_out, d_seams, g.seam_ints * 4, cudaMemcpyDeviceToHost, s), "D2H seams");
@@ -1778,7 +1841,9 @@ carve_status carve_cuda_carve_device(const uint8_t* d_rgb, int w, int h, int tar
         // into the caller's stream (NULL = the legacy default stream), so a later call on
         // any stream of this thread cannot overwrite scratch this carve still uses
         StreamFork f(static_cast<cudaStream_t>(stream), c.stream);
-        run_carve(c, d_rgb, d_out, 1, g, seams, g.seam_ints, nullptr, c.stream);
+        const std::vector<uintptr_t> key = {uintptr_t(w), uintptr_t(h), uintptr_t(target_w), uintptr_t(target_h),
+                                            uintptr_t(d_rgb), uintptr_t(d_out), uintptr_t(seams)};
+        run_graphed(c, key, [&] { run_carve(c, d_rgb, d_out, 1, g, seams, g.seam_ints, nullptr, c.stream); });
         f.join();
     });
 }
