@@ -289,7 +289,10 @@ void launch_energy(const uint32_t* rgb, int pitch, int W, int H, double* e, int 
     // C4 0.52 -> 0.61), 2 CTAs/SM with longer runs below 4 Mpx (C2 0.31 vs 0.22).
     // CARVE_K1V forces one: 0 = 2 CTAs/SM, 1 = prefetch 4, 2 = 3 CTAs/SM, 3 = half runs.
     const int k1v_env = env_int("CARVE_K1V", -1);  // read per call (tests switch it)
-    const int k1v = k1v_env >= 0 ? k1v_env : ((long long)W * H * nimg >= (4ll << 20) ? 2 : 0);
+    // >= 4 Mpx: the shared-memory row ring with 8 rows in flight per warp, 3 CTAs/SM
+    // (tools/k1_sweep.sh, B200: C3 0.46 -> 0.52, C4 0.59 -> 0.67 of the measured HBM peak;
+    // 12 or 16 rows in flight measured lower)
+    const int k1v = k1v_env >= 0 ? k1v_env : ((long long)W * H * nimg >= (4ll << 20) ? 4 : 0);
     static const long long resident_warps2 = [] {
         int dev = 0, nsm = 0, per_sm = 0;
         ck(cudaGetDevice(&dev), "cudaGetDevice");
@@ -299,12 +302,35 @@ void launch_energy(const uint32_t* rgb, int pitch, int W, int H, double* e, int 
     }();
     const int nstrips = (W + K1S_COLS - 1) / K1S_COLS;
     const long long units = (long long)nstrips * H * nimg;  // warp-rows of work
-    const long long rw = k1v == 2 ? resident_warps2 : resident_warps;
+    const long long rw = (k1v == 2 || k1v >= 4) ? resident_warps2 : resident_warps;
     int R = int(std::max<long long>(4, (units + rw - 1) / rw));
     if (k1v == 3) R = std::max(4, R / 2);
     R = k1v == 1 ? ((R + 3) & ~3) : ((R + 1) & ~1);
     const long long warps = (long long)nstrips * ((H + R - 1) / R);
     dim3 grid(unsigned((warps + 7) / 8), nimg);
+    if (k1v >= 4 && k1v <= 6) {  // shared-memory row ring: 8 / 12 / 16 rows in flight per warp
+        static const bool attrs = [] {
+            ck(cudaFuncSetAttribute(k_energy_ring<3, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    8 * 12 * (K1S_COLS + 4) * 4),
+               "cudaFuncSetAttribute(k_energy_ring)");
+            ck(cudaFuncSetAttribute(k_energy_ring<3, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    8 * 16 * (K1S_COLS + 4) * 4),
+               "cudaFuncSetAttribute(k_energy_ring)");
+            return true;
+        }();
+        (void)attrs;
+        if (k1v == 4)
+            k_energy_ring<3, 8><<<grid, 256, 8 * 8 * (K1S_COLS + 4) * 4, s>>>(rgb, pitch, W, H, e, epitch, rgb_is, e_is,
+                                                                          nstrips, R, st, st_is);
+        else if (k1v == 5)
+            k_energy_ring<3, 12><<<grid, 256, 8 * 12 * (K1S_COLS + 4) * 4, s>>>(rgb, pitch, W, H, e, epitch, rgb_is,
+                                                                            e_is, nstrips, R, st, st_is);
+        else
+            k_energy_ring<3, 16><<<grid, 256, 8 * 16 * (K1S_COLS + 4) * 4, s>>>(rgb, pitch, W, H, e, epitch, rgb_is,
+                                                                            e_is, nstrips, R, st, st_is);
+        LAUNCHED("k_energy_ring");
+        return;
+    }
     if (k1v == 1) k_energy_rows<1, 4><<<grid, 256, 0, s>>>(rgb, pitch, W, H, e, epitch, rgb_is, e_is, nstrips, R, st, st_is);
     else if (k1v == 2)
         k_energy_rows<3, 2><<<grid, 256, 0, s>>>(rgb, pitch, W, H, e, epitch, rgb_is, e_is, nstrips, R, st, st_is);

@@ -360,6 +360,107 @@ __global__ void __launch_bounds__(256, MINB) k_energy_rows(const uint32_t* __res
     }
 }
 
+// K1 with a shared-memory row ring (CARVE_K1V=4 / the large-plane default): the same
+// strip decomposition and arithmetic as k_energy_rows, but each lane's 4 RGBX pixels of
+// rows i+1 .. i+DK (and lanes 0/31's strip-edge pixel) are in flight through cp.async
+// instead of registers: DK x 512 B per warp, so a 3-CTA SM has ~100 KB of loads in
+// flight (Little's law at HBM latency) where the register version had ~24 KB. Pixels
+// right of the image (the padded pitch, or the next 4-pixel group of an unpadded row)
+// are loaded but never used: the right-edge column clamps to itself.
+template <int MINB, int DK>
+__global__ void __launch_bounds__(256, MINB) k_energy_ring(const uint32_t* __restrict__ rgb, int pitch, int W, int H,
+                                                     double* __restrict__ e, int epitch, long long rgb_istride,
+                                                     long long e_istride, int nstrips, int R,
+                                                     unsigned long long* stamps = nullptr, long long st_is = 0) {
+    extern __shared__ __align__(16) uint32_t kr_sm[];  // [8 warps][DK][K1S_COLS + 4]
+    if (stamps && blockIdx.x == 0 && threadIdx.x == 0)
+        atomicCAS(&stamps[blockIdx.y * st_is], 0ull, (unsigned long long)globaltimer());
+    EndStamp end_stamp{stamps ? stamps + blockIdx.y * st_is + 1 : nullptr};
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int gw = blockIdx.x * (blockDim.x >> 5) + wib;
+    const int strip = gw % nstrips, i0 = (gw / nstrips) * R;
+    if (i0 >= H) return;
+    rgb += blockIdx.y * rgb_istride;
+    e += blockIdx.y * e_istride;
+    const int s0 = strip * K1S_COLS, col0 = s0 + lane * K1S_C;
+    constexpr int RS = K1S_COLS + 4;  // ring row stride (words): 128 strip pixels + the edge pixel
+    uint32_t* ring = kr_sm + wib * DK * RS;
+    const uint32_t ring_s = uint32_t(__cvta_generic_to_shared(ring));
+    uint32_t lcl = 0, rcl = 0, live = 0;
+#pragma unroll
+    for (int k = 0; k < K1S_C; ++k) {
+        if (col0 + k == 0) lcl |= 1u << k;
+        if (col0 + k == W - 1) rcl |= 1u << k;
+        if (col0 + k < W) live |= 1u << k;
+    }
+    const bool xl = lane == 0 || lane == 31;
+    const int xcol = lane == 0 ? max(s0 - 1, 0) : min(s0 + K1S_COLS, W - 1);
+    const bool in_row = col0 < W;  // groups fully right of the image read nothing
+    auto fetch = [&](int r, int slot) {  // row r (clamped) -> ring slot, one commit group per row
+        const uint32_t* row = rgb + (long long)min(max(r, 0), H - 1) * pitch;
+        const uint32_t dst = ring_s + uint32_t((slot * RS + lane * K1S_C) * 4);
+        if (in_row) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(row + col0) : "memory");
+        if (xl)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(ring_s + uint32_t((slot * RS + K1S_COLS +
+                                                                                                (lane == 31)) * 4)),
+                         "l"(row + xcol)
+                         : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    auto take = [&](int slot, double (&L)[K1S_C], double& xlum) {  // ring slot -> lumas
+        const uint4 v = *reinterpret_cast<const uint4*>(ring + slot * RS + lane * K1S_C);
+        const uint32_t px[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < K1S_C; ++k) L[k] = luma(px[k]);
+        if (xl) xlum = luma(ring[slot * RS + K1S_COLS + (lane == 31)]);
+    };
+    double Lp[K1S_C], Lc[K1S_C], Ln[K1S_C], xc = 0.0, xn = 0.0, xp = 0.0;
+    const int i1 = min(i0 + R, H);
+    // slots: row i0 - 1 + t lives in slot t % DK; rows i0-1 .. i0-2+DK in flight at first
+#pragma unroll
+    for (int t = 0; t < DK; ++t) fetch(i0 - 1 + t, t);
+    asm volatile("cp.async.wait_group %0;" ::"n"(DK - 1) : "memory");
+    take(0, Lp, xp);
+    fetch(i0 - 1 + DK, 0);
+    asm volatile("cp.async.wait_group %0;" ::"n"(DK - 1) : "memory");
+    take(1, Lc, xc);
+    fetch(i0 + DK, 1);
+    for (int i = i0; i < i1; ++i) {
+        const int t = i - i0 + 2;  // ring index of row i + 1
+        asm volatile("cp.async.wait_group %0;" ::"n"(DK - 1) : "memory");
+        take(t % DK, Ln, xn);
+        fetch(i + 1 + DK, t % DK);  // refill the slot with row i + 1 + DK
+        double lL = __shfl_up_sync(FULL, Lc[K1S_C - 1], 1);
+        double lR = __shfl_down_sync(FULL, Lc[0], 1);
+        if (lane == 0) lL = xc;
+        if (lane == 31) lR = xc;
+        double out[K1S_C];
+#pragma unroll
+        for (int k = 0; k < K1S_C; ++k) {
+            double left = k > 0 ? Lc[k - 1] : lL;
+            double right = k + 1 < K1S_C ? Lc[k + 1] : lR;
+            if (lcl >> k & 1) left = Lc[k];
+            if (rcl >> k & 1) right = Lc[k];
+            out[k] = e1(left, right, Lp[k], Ln[k]);
+        }
+        double* erow = e + (long long)i * epitch + col0;
+        if (live == (1u << K1S_C) - 1) {
+            *reinterpret_cast<double2*>(erow) = make_double2(out[0], out[1]);
+            *reinterpret_cast<double2*>(erow + 2) = make_double2(out[2], out[3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < K1S_C; ++k)
+                if (live >> k & 1) erow[k] = out[k];
+        }
+#pragma unroll
+        for (int k = 0; k < K1S_C; ++k) { Lp[k] = Lc[k]; Lc[k] = Ln[k]; }
+        xp = xc;
+        xc = xn;
+    }
+    (void)xp;
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 // +inf into the left/right pad columns of rows [0, H) (e points at logical column 0)
 __global__ void k_fill_pads(double* __restrict__ e, int epitch, int W, int H, long long e_istride) {
     e += blockIdx.y * e_istride;

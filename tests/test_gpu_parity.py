@@ -42,7 +42,7 @@ def test_energy_rgb_bitexact(port, w, h):
         assert np.array_equal(bits(cv.to_grayscale(img)), bits(port.to_grayscale(img)))
 
 
-@pytest.mark.parametrize("k1v", ["0", "1", "2", "3", "-1"])
+@pytest.mark.parametrize("k1v", ["0", "1", "2", "3", "4", "5", "6", "-1"])
 def test_energy_every_k1_shape_bitexact(port, monkeypatch, k1v):
     """Each K1 launch shape (CARVE_K1V: 2 or 3 CTAs/SM, prefetch depth, run
     length; -1 = the size-based default, which switches shape at 4 Mpx)."""
