@@ -6,11 +6,13 @@
 //   carve enlarge --input X --output Y [--scale S | --width W] [--height H] [solver flags]
 //   carve seams   --input X --output Y --count N [solver flags]
 //   carve remove-object --input X --mask M --output Y [--no-restore] [solver flags]
+//   carve energy  --input X --output Y.png --energy e1|e2|hog|entropy
 // Exit codes as the reference: 0 success, 1 usage error, 2 runtime error.
 // CARVE_WORKERS is validated like the reference (cli.hpp:109-126) but never
 // changes output. Other subcommands report usage_error (not on the B200 path).
 #pragma once
 
+#include <cctype>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -96,6 +98,8 @@ inline ResizeCmd parse_resize(const std::vector<std::string>& a) {
     if (a[0] == "remove-object" && c.mask.empty()) fail(Errc::usage_error, "--mask is required");
     if (a[0] == "remove-object" && (c.scale || c.width || c.height))
         fail(Errc::usage_error, "remove-object takes no size options");
+    if (a[0] == "energy" && (c.scale || c.width || c.height || c.forward))
+        fail(Errc::usage_error, "energy takes --input, --output and --energy only");
     return c;
 }
 
@@ -154,6 +158,23 @@ inline int run_seams(const SeamsCmd& cmd) {
     return 0;
 }
 
+/// cli.hpp:288-299 run_energy: the normalised energy map of the input as a gray PNG
+/// (e1 on the device; the other energy functions are not on the B200 path).
+inline int run_energy(const ResizeCmd& cmd) {
+    auto ends_with_png = [](const std::string& s) {
+        if (s.size() < 4) return false;
+        std::string t = s.substr(s.size() - 4);
+        for (char& ch : t) ch = char(std::tolower(static_cast<unsigned char>(ch)));
+        return t == ".png";
+    };
+    if (!ends_with_png(cmd.output)) fail(Errc::usage_error, "energy output must be a .png path");
+    PixelGrid img = load_image(cmd.input);
+    if (cmd.energy != "e1") ::carve::detail::unsupported("energy " + cmd.energy);
+    const EnergyMap energy = energy_e1(img);  // compute_energy(to_grayscale(img), e1), fused on the device
+    save_gray_png(normalize_to_gray(energy), energy.width, energy.height, cmd.output);
+    return 0;
+}
+
 /// cli.hpp:279-287 run_remove_object: mask_from_image of --mask, remove_object.
 inline int run_remove_object(const ResizeCmd& cmd) {
     detail::check_env_workers();
@@ -173,12 +194,21 @@ inline int cli_main(int argc, char** argv) {
                         "                     [--solver dp|pardp] [--energy e1]\n"
                         "       carve enlarge --input X --output Y [--scale S | --width W] [--height H]\n"
                         "       carve seams   --input X --output Y --count N\n"
-                        "       carve remove-object --input X --mask M --output Y [--no-restore]\n");
+                        "       carve remove-object --input X --mask M --output Y [--no-restore]\n"
+                        "       carve energy  --input X --output Y.png --energy e1\n");
             return args.empty() ? 1 : 0;
         }
         if (args[0] == "resize") return run_resize(parse_resize(args));
         if (args[0] == "enlarge") return run_enlarge(parse_resize(args));
         if (args[0] == "remove-object") return run_remove_object(parse_resize(args));
+        if (args[0] == "energy") {
+            const ResizeCmd c = parse_resize(args);
+            if (c.input.empty() || c.output.empty()) fail(Errc::usage_error, "energy needs --input and --output");
+            bool has_energy = false;
+            for (const auto& a : args) has_energy = has_energy || a == "--energy";
+            if (!has_energy) fail(Errc::usage_error, "energy: --energy is required");
+            return run_energy(c);
+        }
         if (args[0] == "seams") {
             SeamsCmd c;
             static_cast<ResizeCmd&>(c) = parse_resize(args);
@@ -186,7 +216,7 @@ inline int cli_main(int argc, char** argv) {
         }
         fail(Errc::usage_error,
              "subcommand '" + args[0] +
-                 "' is not supported by the B200 engine (resize, enlarge, seams, remove-object)");
+                 "' is not supported by the B200 engine (resize, enlarge, seams, remove-object, energy)");
     } catch (const Error& err) {
         std::fprintf(stderr, "carve: %s\n", err.what());
         return err.code() == Errc::usage_error ? 1 : 2;

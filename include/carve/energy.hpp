@@ -5,6 +5,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -107,6 +108,23 @@ inline RemovalMask mask_from_image(const PixelGrid& img) {
     mask.flags.resize(img.pixels.size());
     detail::check(carve_cuda_mask_from_rgb(img.bytes(), img.width, img.height, mask.flags.data()));
     return mask;
+}
+
+/// energy.hpp:285-299: min-max normalisation to 8-bit gray (constant maps -> 0), the
+/// `carve energy` export. Host arithmetic in the reference's operation order.
+inline std::vector<std::uint8_t> normalize_to_gray(const EnergyMap& energy) {
+    double lo = energy.values.empty() ? 0.0 : energy.values[0];
+    double hi = lo;
+    for (double v : energy.values) {
+        lo = std::min(lo, v);
+        hi = std::max(hi, v);
+    }
+    std::vector<std::uint8_t> out(energy.values.size(), 0);
+    const double span = hi - lo;
+    if (span > 0.0)
+        for (size_t i = 0; i < out.size(); ++i)
+            out[i] = std::uint8_t(std::lround((energy.values[i] - lo) / span * 255.0));
+    return out;
 }
 
 inline RemovalMask transpose(const RemovalMask& mask) {

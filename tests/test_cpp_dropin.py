@@ -54,6 +54,65 @@ def test_cli_usage_errors_exit_1(tmp_path):
     assert r.returncode == 1 and "carve:" in r.stderr
 
 
+def test_cli_energy_usage_errors_exit_1(tmp_path):
+    # cli.hpp:184-187, 288-291: --energy required, output must be .png, e1 only on the B200 path
+    p = tmp_path / "a.ppm"
+    write_ppm(p, np.zeros((4, 4, 3), np.uint8))
+    assert run("energy", "--input", str(p), "--output", str(tmp_path / "o.png")).returncode == 1
+    assert run("energy", "--input", str(p), "--output", str(tmp_path / "o.ppm"), "--energy", "e1").returncode == 1
+    assert run("energy", "--input", str(p), "--output", str(tmp_path / "o.png"), "--energy", "x").returncode == 1
+    assert run("energy", "--input", str(p), "--output", str(tmp_path / "o.png"), "--energy", "e1",
+               "--scale", "0.5").returncode == 1
+
+
+def read_png_gray(path):
+    import struct
+    import zlib
+    data = open(path, "rb").read()
+    assert data[:8] == b"\x89PNG\r\n\x1a\n"
+    pos, idat, w, h = 8, b"", None, None
+    while pos < len(data):
+        n, kind = struct.unpack(">I4s", data[pos:pos + 8])
+        body = data[pos + 8:pos + 8 + n]
+        if kind == b"IHDR":
+            w, h, depth, ctype = struct.unpack(">IIBB", body[:10])
+            assert depth == 8 and ctype == 0
+        elif kind == b"IDAT":
+            idat += body
+        pos += 12 + n
+    raw = zlib.decompress(idat)
+    out, prev = np.zeros((h, w), np.uint8), np.zeros(w, np.int32)
+    for i in range(h):
+        f, row = raw[i * (w + 1)], np.frombuffer(raw[i * (w + 1) + 1:(i + 1) * (w + 1)], np.uint8).astype(np.int32)
+        cur = np.zeros(w, np.int32)
+        for j in range(w):
+            a = cur[j - 1] if j else 0
+            b, c = prev[j], (prev[j - 1] if j else 0)
+            pred = {0: 0, 1: a, 2: b, 3: (a + b) // 2}.get(f)
+            if f == 4:
+                pa, pb, pc = abs(b - c), abs(a - c), abs(a + b - 2 * c)
+                pred = a if pa <= pb and pa <= pc else (b if pb <= pc else c)
+            cur[j] = (row[j] + pred) & 255
+        out[i], prev = cur, cur
+    return out
+
+
+@pytest.mark.gpu
+def test_cli_energy_matches_oracle(tmp_path):
+    """`carve energy` (cli.hpp:288-299): normalize_to_gray(e1) as an 8-bit gray PNG."""
+    img = oracle.port().make_test_image(67, 41)
+    src = tmp_path / "in.ppm"
+    write_ppm(src, img)
+    r = run("energy", "--input", str(src), "--output", str(tmp_path / "e.png"), "--energy", "e1")
+    assert r.returncode == 0, r.stderr
+    e = oracle.port().energy_e1_rgb(img)
+    lo, hi = e.min(), e.max()
+    want = np.floor((e - lo) / (hi - lo) * 255.0 + 0.5).astype(np.uint8)  # std::lround, non-negative
+    assert np.array_equal(read_png_gray(tmp_path / "e.png"), want)
+    r = run("energy", "--input", str(src), "--output", str(tmp_path / "h.png"), "--energy", "hog")
+    assert r.returncode == 1 and "not supported" in r.stderr
+
+
 def test_cli_runtime_errors_exit_2(tmp_path):
     r = run("resize", "--input", str(tmp_path / "missing.ppm"), "--output", str(tmp_path / "o.ppm"), "--scale", "0.5")
     assert r.returncode == 2 and "no such file" in r.stderr
