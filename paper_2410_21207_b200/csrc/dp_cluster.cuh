@@ -239,6 +239,12 @@ __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
 __device__ __forceinline__ void cp_async8(uint32_t saddr, const void* g) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(saddr), "l"(g) : "memory");
 }
+// predicated form: a lane whose bytes are never used skips the global read
+__device__ __forceinline__ void cp_async16_if(bool pred, uint32_t saddr, const void* g) {
+    asm volatile("{.reg .pred q; setp.ne.b32 q, %0, 0; @q cp.async.cg.shared.global [%1], [%2], 16;}" ::"r"(int(pred)),
+                 "r"(saddr), "l"(g)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -818,6 +824,14 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
             // 16-byte aligned lane slices: even column for double2 energies, multiple of 4 for RGBX
             const int wbase = (c1 - P2_COLS / 2) & (FUSED ? ~3 : ~1);
             const int wc0 = wbase + lane * 4;
+            // fused: the backtrack from c1 at row r1 only reads cells within c1 +- 32 of
+            // the block's cone (LBLK rows), which need RGBX columns c1 +- 33; lanes clear of
+            // c1 +- (LBLK + 4) (and of the image) skip their reads — the wrong values their
+            // stale stage bytes produce spread one column per row and stay outside the cone.
+            // Only in the two-CTAs-per-SM batch shape (MINB 2), where it measured faster
+            // (C5 DP 1.555 -> 1.541 ms, DRAM 4.46 -> 4.29 GB per launch); the small-batch
+            // cluster shape measured 6 % slower with it (tools/ab_libs.sh)
+            const bool qneed = MINB < 2 || (wc0 + 3 >= max(c1 - (LBLK + 4), -1) && wc0 <= min(c1 + LBLK + 4, W));
             double mm[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -837,11 +851,11 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
                 uint32_t px[4];
                 const uint32_t* ra = wrgb + (long long)(r0 - 1) * p.rpitch;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) px[k] = __ldg(ra + k);
+                for (int k = 0; k < 4; ++k) px[k] = qneed ? __ldg(ra + k) : 0u;
                 luma_cols<4>(px, QLp);
                 const uint32_t* rb = wrgb + (long long)r0 * p.rpitch;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) px[k] = __ldg(rb + k);
+                for (int k = 0; k < 4; ++k) px[k] = qneed ? __ldg(rb + k) : 0u;
                 luma_cols<4>(px, QLc);
             } else if constexpr (FWD) {  // cost planes: columns outside the image are +inf
 #pragma unroll
@@ -851,7 +865,7 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
             auto p2fetch = [&](int r, int slot) {
                 const uint32_t dst = p2ring + uint32_t(slot * P2STAGE);
                 if constexpr (FUSED) {
-                    cp_async16(dst, wrgb + (long long)min(r + 1, H - 1) * p.rpitch);
+                    cp_async16_if(qneed, dst, wrgb + (long long)min(r + 1, H - 1) * p.rpitch);
                 } else {
                     const double* src = e + (long long)min(r, r1) * p.epitch + wc0;
 #pragma unroll
