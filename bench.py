@@ -453,6 +453,16 @@ def measured_traffic(kernel, cfg_name):
     return None
 
 
+def measured_inst(kernel, cfg_name):
+    """Warp instructions per launch (ncu smsp__inst_executed.sum) from the committed capture
+    (profiles/r02_traffic.json `inst_per_launch`), for the workload it was taken on."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "r02_traffic.json")))
+        return t.get("inst_per_launch", {}).get(cfg_name, {}).get(kernel)
+    except Exception:
+        return None
+
+
 # DP rows per launch (the DP is a row-serial chain: its real bound is latency per row)
 DP_ROWS = {"c1": 512, "c2": 1080, "c3": (768 * 2160 + 432 * 3072) / 1200, "c4": 4320, "c5": 768}
 # one warp's dependent row step (2 shuffles + 2 compare/selects + DADD), measured on B200 by
@@ -502,6 +512,23 @@ def roofline_of(kern, cfg_name="c2", sm_mhz=None):
                          ncu_source="profiles/r01_dp_ncu_metrics.json")
         except Exception:
             pass
+    elif dom == "k_dp_seam" and measured_inst(dom, cfg_name):
+        # the batch DP is issue-bound (ncu: FP64 and XU pipes below half busy, issue slots
+        # ~70 % busy): instruction issue rate against one warp-instruction per scheduler per
+        # cycle, 4 schedulers per SM, at the sampled SM clock
+        inst = measured_inst(dom, cfg_name)
+        try:
+            import torch
+            nsm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        except Exception:
+            nsm = 148
+        achieved = inst / (kd["avg_us"] * 1e-6) / 1e9
+        ipeak = nsm * 4 * (sm_mhz or 1965.0) / 1e3
+        r.update(bound="issue", achieved=achieved, peak=ipeak, unit="G warp-instructions/s", frac=achieved / ipeak,
+                 inst_per_launch=inst, hbm_frac=kd["gbs"] / peak,
+                 note=f"issue-bound fused DP: {inst:.4g} warp instructions per launch (ncu, profiles/r02_traffic.json) "
+                      f"over the live launch time; peak = {nsm} SMs x 4 schedulers x SM clock; its HBM view: "
+                      f"{kd['gbs']:.0f} GB/s = {kd['gbs'] / peak:.3f} of {peak:.0f} GB/s")
     else:
         r.update(bound="hbm", achieved=kd["gbs"], peak=peak, unit="GB/s", frac=kd["gbs"] / peak)
     return r

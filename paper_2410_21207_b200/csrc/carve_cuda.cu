@@ -1108,10 +1108,10 @@ struct BatchPlan {
 
 BatchPlan batch_plan(int n, int ndev, const CarveGeometry& g) {
     const int share = (n + ndev - 1) / ndev;
-    // measured on B200 (tools/share_sweep.py --grid, profiles/r02_share_grid.txt): 128-image
-    // chunks on up to 4 pipelines for shares >= 256 (1024: 3.42K e2e images/s vs 3.34K with
-    // 2 x 256; 512: 3.25K vs 2.90K), two 64-image chunks for a 128-image share (2.32K vs
-    // 2.12K); 32-image chunks lose (a 32-image carve cannot fill the SMs)
+    // measured on B200 (tools/share_sweep.py --grid, profiles/r02_share_grid_b.txt, batches
+    // without PDL): 4 pipelines, chunks of a quarter share up to 128 images — 1024: 3.56K
+    // e2e images/s (2 x 256: 3.47K), 512: 3.38K, 256 as 4 x 64: 2.92K (2 x 128: 2.85K),
+    // 128 as 4 x 32: 2.46K (2 x 64: 2.32K)
     int P = std::max(1, std::min(CARVE_MAX_PIPELINES, env_int("CARVE_PIPELINES", 4)));
     // per-image device footprint (planes, energy, M rows, packed in/out double
     // buffers, seam log): the chunks in flight stay well inside 180 GB of HBM
@@ -1120,7 +1120,7 @@ BatchPlan batch_plan(int n, int ndev, const CarveGeometry& g) {
                            g.seam_ints * 4;
     const int cap = int(std::max<size_t>(1, (size_t(48) << 30) / (per_img * size_t(P))));
     int ch = env_int("CARVE_PIPE_CHUNK", 0);
-    if (ch <= 0) ch = std::max(16, std::min(128, (share + 1) / 2));
+    if (ch <= 0) ch = std::max(16, std::min(128, (share + 3) / 4));
     ch = std::max(1, std::min({ch, cap, share}));
     const int nchunks = (share + ch - 1) / ch;
     P = std::max(1, std::min(P, nchunks));
@@ -1897,10 +1897,10 @@ carve_status carve_cuda_carve_batch_device(const uint8_t* d_rgb, int n, int w, i
         // stream, forked from and joined back into `s`, so one sub-batch's per-seam
         // launches fill the other's wave tails. Per-kernel event profiling (c.prof) keeps
         // the calling thread's context (one stream, serial launch timings).
-        const int want = std::max(1, std::min(CARVE_MAX_PIPELINES, env_int("CARVE_DEVICE_SPLIT", 2)));
-        // measured (profiles/r02_share_grid.txt): 128 images as 2 x 64 2.70K vs 2.61K images/s;
-        // 256 as 2 x 128 or 1 x 256 the same
-        const int min_sub = std::max(1, env_int("CARVE_DEVICE_SPLIT_MIN", 64));
+        const int want = std::max(1, std::min(CARVE_MAX_PIPELINES, env_int("CARVE_DEVICE_SPLIT", 4)));
+        // measured (profiles/r02_share_grid_b.txt): 128 images as 4 x 32 2.82K vs 2 x 64 2.71K
+        // images/s, 512 as 4 x 128 3.78K vs 2 x 256 3.75K, 1024 as 4 or 2 sub-batches the same
+        const int min_sub = std::max(1, env_int("CARVE_DEVICE_SPLIT_MIN", 32));
         const int P = c.prof ? 1 : std::max(1, std::min(want, n / min_sub));
         const size_t in_bytes = size_t(w) * h * 3, out_bytes = size_t(target_w) * target_h * 3;
         if (c.prof) {
