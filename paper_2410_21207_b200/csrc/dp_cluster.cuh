@@ -224,6 +224,11 @@ __device__ __forceinline__ void st_async_v2_b64_if(bool pr, uint32_t raddr, doub
         "l"(__double_as_longlong(a)), "l"(__double_as_longlong(b)), "r"(rmbar), "r"(uint32_t(pr))
         : "memory");
 }
+__device__ __forceinline__ int ld_shared_s32(uint32_t a) {
+    int v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
 __device__ __forceinline__ void st_async_v2_b32_if(bool pr, uint32_t raddr, uint32_t a, uint32_t b, uint32_t rmbar) {
     asm volatile(
         "{ .reg .pred p; setp.ne.u32 p, %4, 0;\n"
@@ -423,9 +428,14 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
     const int* my_l = mail_l + (warp * 2) * K;
     const uint32_t my_b = smem_u32(mbar + warp * 2);  // + parity*8
     const uint32_t halo_tx = uint32_t(((gl >= 0) + (gr < G)) * K * (8 + 4));
+    // phase 1 hand-off (label tables left distributed): a (block, column) token message
+    // slot and its mbarrier, after the argmin scratch (red_v[120..122))
+    uint64_t* p1bar = reinterpret_cast<uint64_t*>(red_v + 120);
+    int* p1msg = reinterpret_cast<int*>(red_v + 121);
     if (lane == 0) {
         mbar_init(my_b, 1);
         mbar_init(my_b + 8, 1);
+        if (threadIdx.x == 0) mbar_init(smem_u32(p1bar), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // every mbarrier of the cluster is initialised before any halo is sent, and
@@ -773,8 +783,50 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
     if (ncl > 1) cluster.sync();
     else __syncthreads();
 
-    // ---- K3b phase 1 (CTA 0, one thread): block-boundary columns through the labels
-    if (cta == 0 && threadIdx.x == 0 && !(p.dbg & 2)) {
+    // ---- K3b phase 1: block-boundary columns through the labels. Tables left
+    // distributed over the cluster: the walk moves with the seam — each CTA's thread 0
+    // follows the labels while the column is its own and hands the (block, column)
+    // token to the owning CTA (st.async + mbarrier) when the seam crosses over, so hops
+    // read local shared memory instead of one remote DSMEM load each.
+    // The whole of warp 0 runs the walk (uniform control flow, lane 0 stores and sends):
+    // a single diverged lane left warp 0 running phase 2 split, 3x slower.
+    const bool handoff = !GLAB && !p.gather && ncl > 1 && nblk > 0 && !(p.dbg & 2);
+    if (handoff && warp == 0) {
+        constexpr int DONE = -2;
+        auto send = [&](int to, int b, int c) {
+            st_async_v2_b32_if(lane == 0, mapa_u32(smem_u32(p1msg), uint32_t(to)), uint32_t(b), uint32_t(c),
+                               mapa_u32(smem_u32(p1bar), uint32_t(to)));
+        };
+        if (cta == 0) {
+            bv = cl_v[0];
+            bi = cl_i[0];
+            for (int r = 1; r < ncl; ++r) argmin_combine(bv, bi, cl_v[r], cl_i[r]);
+            if (lane == 0) seam[H - 1] = bi;
+            send((bi / S) / NWARP, nblk - 1, bi);
+        }
+        const uint32_t bar = smem_u32(p1bar);
+        for (uint32_t ph = 0;; ph ^= 1) {
+            if (lane == 0) mbar_arrive_expect_tx(bar, 8);
+            while (!mbar_try_wait(bar, ph)) {
+            }
+            int b = ld_shared_s32(smem_u32(p1msg)), c = ld_shared_s32(smem_u32(p1msg) + 4);
+            if (b == DONE) break;
+            while (b >= 0 && (c / S) / NWARP == cta) {
+                c += labels[b * SM::COLS + (c - cta * SM::COLS)];
+                if (b > 0 && lane == 0) seam[LBLK * b] = c;  // row 32b = last row of block b-1
+                --b;
+            }
+            if (b >= 0) {
+                send((c / S) / NWARP, b, c);
+                continue;
+            }
+            if (lane == 0) seam[0] = c;
+            for (int r = 0; r < ncl; ++r)
+                if (r != cta) send(r, DONE, 0);
+            break;
+        }
+    }
+    if (!handoff && cta == 0 && threadIdx.x == 0 && !(p.dbg & 2)) {
         bv = cl_v[0];
         bi = cl_i[0];
         for (int r = 1; r < ncl; ++r) argmin_combine(bv, bi, cl_v[r], cl_i[r]);
