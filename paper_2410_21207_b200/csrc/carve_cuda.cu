@@ -2004,10 +2004,15 @@ carve_status carve_cuda_carve_batch(const uint8_t* const* rgb, int n, int w, int
                     if (t >= 2 * P) ck(cudaEventSynchronize(cq.pipe_ev[D2H][b]), "wait d2h");
                     uint8_t* d_in = cq.pin_in[b].as<uint8_t>();
                     uint8_t* d_out = cq.pin_out[b].as<uint8_t>();
-                    for (int i = 0; i < m; ++i)
-                        ck(cudaMemcpyAsync(d_in + in_bytes * i, rgb[b0 + i], in_bytes, cudaMemcpyHostToDevice,
-                                           c0.h2d),
+                    // one copy per run of images that are contiguous in host memory
+                    for (int i = 0; i < m;) {
+                        int j = i + 1;
+                        while (j < m && rgb[b0 + j] == rgb[b0 + j - 1] + in_bytes) ++j;
+                        ck(cudaMemcpyAsync(d_in + in_bytes * i, rgb[b0 + i], in_bytes * (j - i),
+                                           cudaMemcpyHostToDevice, c0.h2d),
                            "H2D");
+                        i = j;
+                    }
                     ck(cudaEventRecord(cq.pipe_ev[H2D][b], c0.h2d), "record h2d");
                     ck(cudaStreamWaitEvent(cq.stream, cq.pipe_ev[H2D][b], 0), "wait h2d");
                     // the DP shape counts the other pipelines' carves (they fill the SMs
@@ -2017,10 +2022,14 @@ carve_status carve_cuda_carve_batch(const uint8_t* const* rgb, int n, int w, int
                               cq.stream);
                     ck(cudaEventRecord(cq.pipe_ev[COMP][b], cq.stream), "record comp");
                     ck(cudaStreamWaitEvent(c0.d2h, cq.pipe_ev[COMP][b], 0), "wait comp");
-                    for (int i = 0; i < m; ++i)
-                        ck(cudaMemcpyAsync(rgb_out[b0 + i], d_out + out_bytes * i, out_bytes,
+                    for (int i = 0; i < m;) {
+                        int j = i + 1;
+                        while (j < m && rgb_out[b0 + j] == rgb_out[b0 + j - 1] + out_bytes) ++j;
+                        ck(cudaMemcpyAsync(rgb_out[b0 + i], d_out + out_bytes * i, out_bytes * (j - i),
                                            cudaMemcpyDeviceToHost, c0.d2h),
                            "D2H");
+                        i = j;
+                    }
                     ck(cudaEventRecord(cq.pipe_ev[D2H][b], c0.d2h), "record d2h");
                 }
                 ck(cudaStreamSynchronize(c0.d2h), "sync d2h");
