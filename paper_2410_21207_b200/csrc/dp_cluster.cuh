@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
         p.stamps[img * p.st_istride + (p.prev_seam ? 0 : 2)] = globaltimer();
 
     // K1 fix-up of the previous removal: rows are
-    // spread over every thread of the cluster; made visible by the barrier below
+    // spread over every thread of the cluster; made visible by the cluster barrier below
     if (p.prev_seam) {
         const int* ps = p.prev_seam + img * p.s_istride;
         const uint32_t* rgb = p.rgb + img * p.rgb_istride;
@@ -392,7 +392,9 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
                     e[(long long)i * p.epitch + x] =
                         e1(luma(row[max(x - 1, 0)]), luma(row[min(x + 1, W - 1)]), luma(up[x]), luma(dn[x]));
         }
-        __threadfence();
+        // no gpu-scope fence: every reader of these energies is in this cluster, and the
+        // cluster barrier below (arrive.release / wait.acquire) orders global writes at
+        // cluster scope (measured: fix-up lap 2.59 -> 2.30 us per seam at C2)
     }
 
     // which of my C columns are useful (inside my segment and the image)
