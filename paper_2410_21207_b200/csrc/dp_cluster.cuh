@@ -365,6 +365,12 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
     // this lane's C columns of stage u: ring_b[(((warp * D + u) * 32 + lane) * C) * RE]
     const uint32_t ring_lane = smem_u32(ring_b + (size_t(warp) * D * 32 + lane) * C * RE);
 
+    // the previous seam was written by the DP before the removal this launch depends on
+    // (that DP had completed before the removal ran), so its column of my first fix-up
+    // row is read before the grid dependency wait, off the prologue's latency chain
+    const int fx_nthr = ncl * NWARP * 32, fx_tid = cta * NWARP * 32 + threadIdx.x;
+    int fx_sp0 = 0;
+    if (p.prev_seam && fx_tid < H) fx_sp0 = __ldcg(p.prev_seam + img * p.s_istride + fx_tid);
     pdl_wait();  // the previous removal has completed (its planes and seam log are visible)
     pdl_launch_dependents();
     // a data-dependent loop (object removal) enqueued past its end: every CTA reads the
@@ -380,9 +386,9 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
     if (p.prev_seam) {
         const int* ps = p.prev_seam + img * p.s_istride;
         const uint32_t* rgb = p.rgb + img * p.rgb_istride;
-        const int nthr = ncl * NWARP * 32, tid = cta * NWARP * 32 + threadIdx.x;
+        const int nthr = fx_nthr, tid = fx_tid;
         for (int i = tid; i < H; i += nthr) {
-            const int sp = __ldg(ps + i);
+            const int sp = i == tid ? fx_sp0 : __ldg(ps + i);
             const uint32_t* row = rgb + (long long)i * p.rpitch;
             const uint32_t* up = rgb + (long long)max(i - 1, 0) * p.rpitch;
             const uint32_t* dn = rgb + (long long)min(i + 1, H - 1) * p.rpitch;
