@@ -359,7 +359,7 @@ def measure(cfg_name, args, rk, inputs=None, n_share=None, profile=True):
     # ---- kernel attribution pass (same workload, per-kernel CUDA events) ------------
     kern = {}
     if profile:
-        kern = kernel_profile(cv, lambda: enqueue(seams=True), W, H, TW, TH, n_local)
+        kern = kernel_profile(cv, lambda: enqueue(seams=True), W, H, TW, TH, n_local, flush)
         if not batch:
             moved = inplace_removal_bytes(d_seams.cpu().numpy(), W, H, TW, TH)
             k = kern.get("k_compact")
@@ -416,14 +416,22 @@ def inplace_removal_bytes(seams, W, H, TW, TH):
     return {"bytes": total}
 
 
-def kernel_profile(cv, enqueue, W, H, TW, TH, n_local):
+def kernel_profile(cv, enqueue, W, H, TW, TH, n_local, flush=None):
     """One extra carve with per-kernel CUDA events (library profiling mode):
     average launch duration, share of the step and algorithmic GB/s per kernel
-    (algorithmic bytes per SURVEY.md §8d)."""
+    (algorithmic bytes per SURVEY.md §8d). Like a timed step it starts
+    from a flushed L2 (the flush buffer is then read back, so its dirty lines are written
+    out before the carve instead of during its first kernels), and the GPU is held in a
+    sleep kernel while the host enqueues the carve, so no event pair measures host
+    submission latency (the first launches of an idle GPU otherwise do)."""
     import torch
 
+    if flush is not None:
+        flush.zero_()
+        flush.sum(dtype=torch.int64)
     cv.set_kernel_events(True)
     try:
+        torch.cuda._sleep(50_000_000)  # ~25 ms at 2 GHz: covers the enqueue of every launch
         enqueue()
         torch.cuda.synchronize()
         stats = cv.kernel_event_stats()
