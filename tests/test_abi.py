@@ -103,6 +103,11 @@ def test_batch_plan_host_logic(monkeypatch):
         share = -(-n // ndev)
         assert 1 <= ch <= share and 1 <= p <= 4
         assert p <= -(-share // ch)
+    # the measured default shape (profiles/r02_share_grid_b.txt): 4 pipelines, quarter-share
+    # chunks up to 128 images, at least 16
+    assert [cv.batch_plan(n, 1024, 768, 896, 768, nd) for n, nd in [(1024, 1), (256, 1), (128, 1), (1024, 8)]] == \
+        [(4, 128), (4, 64), (4, 32), (4, 32)]
+    assert cv.batch_plan(20, 1024, 768, 896, 768, 1) == (2, 16)
     monkeypatch.setenv("CARVE_PIPE_CHUNK", "16")
     monkeypatch.setenv("CARVE_PIPELINES", "3")
     assert cv.batch_plan(1025, 64, 48, 56, 48, 2) == (3, 16)
