@@ -510,7 +510,13 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
     const double* nrow = e + p.epitch + col0;  // my slice of the next row to fetch (spare rows past H-1 are harmless)
     static_assert(C % 2 == 0, "cp.async moves 16-byte pairs of doubles");
     int frow = 2;  // fused: next RGBX row to fetch (the ring feeds luma row i+1 at row i)
-    auto fetch = [&](int u) {  // this lane's C values of the next row -> ring stage u, one commit group per row
+    // energy / cost-plane rows travel in commit groups of two: one commit and one wait per
+    // two rows (C2 DP 62.6 -> 61.4 us; groups of four measured 66.6: the refill burst stalls
+    // the row). The fused RGBX ring keeps one row per group.
+    constexpr int RG = FUSED ? 1 : 2;
+    constexpr bool PAIRS = RG > 1;
+    static_assert(D % RG == 0 && K % RG == 0, "commit groups tile the ring and the K-blocks");
+    auto fetch = [&](int u, bool commit = true) {  // this lane's C values of the next row -> ring stage u
         if constexpr (FUSED) {
             const uint32_t* src = rgbf + (long long)min(frow, H - 1) * p.rpitch;
             const uint32_t dst = ring_lane + uint32_t(u * 32 * C * RE);
@@ -529,13 +535,22 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
                     cp_async16(ring_lane + uint32_t(u * 32 * C * RE + (pl * C + k) * 8), nrow + pl * p.cplane + k);
             nrow += p.epitch;
         }
-        cp_async_commit();
+        if (commit) cp_async_commit();
     };
+    if constexpr (PAIRS) {
 #pragma unroll
-    for (int u = 0; u < D; ++u) fetch(u);
+        for (int u = 0; u < D; ++u) fetch(u, u % RG == RG - 1);
+    } else {
+#pragma unroll
+        for (int u = 0; u < D; ++u) fetch(u);
+    }
 
-    auto step = [&](int u, int i) {
-        cp_async_wait<D - 1>();  // the oldest of the D groups in flight has landed
+    auto step = [&](int u, int i, int t) {
+        if constexpr (PAIRS) {
+            if (t % RG == 0) cp_async_wait<D / RG - 1>();  // the oldest group of rows has landed
+        } else {
+            cp_async_wait<D - 1>();  // the oldest of the D groups in flight has landed
+        }
         double ev[C], fcl[C], fcu[C], fcr[C];  // energies, or forward transition costs (FWD)
         if constexpr (FUSED) {
             const uint32_t* src = reinterpret_cast<const uint32_t*>(ring_b + ((size_t(warp) * D + u) * 32 + lane) * C * RE);
@@ -607,7 +622,14 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
                 }
         }
         (void)dbits;
-        fetch(u);  // refill this stage with row i + D (own lane's bytes only: no cross-lane hazard)
+        if constexpr (PAIRS) {
+            if (t % RG == RG - 1) {  // every row of the group consumed: refill the group
+#pragma unroll
+                for (int r = RG - 1; r >= 0; --r) fetch(u - r, r == 0);
+            }
+        } else {
+            fetch(u);  // refill this stage with row i + D (own lane's bytes only: no cross-lane hazard)
+        }
     };
     // block-end stores: shared-space label address and a running M-boundary
     // pointer, both hoisted (the generic->shared conversion was per call)
@@ -709,7 +731,7 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
     constexpr int QB = D > K ? D / K : 1;
     auto kblock = [&](auto qq, int i0) {
 #pragma unroll
-        for (int t = 0; t < K; ++t) step((decltype(qq)::value * K + t) % D, i0 + t);
+        for (int t = 0; t < K; ++t) step((decltype(qq)::value * K + t) % D, i0 + t, t);
     };
     const int nkb = (H - 1) / K;  // full K-row blocks
     for (int q = 0; q < nkb; ++q) {
@@ -744,7 +766,7 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
 #pragma unroll
             for (int t = 0; t < K; ++t) {
                 if (i0 + t >= H) break;
-                step(((nkb % QB) * K + t) % D, i0 + t);
+                step(((nkb % QB) * K + t) % D, i0 + t, t);
             }
             block_end(H - 1, blk);  // the tail always ends the image (and its label block)
         }
