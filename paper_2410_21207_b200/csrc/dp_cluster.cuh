@@ -510,10 +510,10 @@ __global__ void __launch_bounds__(NWARP * 32, MINB) k_dp2(Dp2Params p) {
     const double* nrow = e + p.epitch + col0;  // my slice of the next row to fetch (spare rows past H-1 are harmless)
     static_assert(C % 2 == 0, "cp.async moves 16-byte pairs of doubles");
     int frow = 2;  // fused: next RGBX row to fetch (the ring feeds luma row i+1 at row i)
-    // energy / cost-plane rows travel in commit groups of two: one commit and one wait per
-    // two rows (C2 DP 62.6 -> 61.4 us; groups of four measured 66.6: the refill burst stalls
-    // the row). The fused RGBX ring keeps one row per group.
-    constexpr int RG = FUSED ? 1 : 2;
+    // ring rows travel in commit groups of two: one commit and one wait per two rows
+    // (C2 DP 62.6 -> 61.4 us, C5 fused DP 1.53 -> 1.52 ms, 128 images 47.9 -> 46.8 ms;
+    // groups of four measured 66.6 us at C2: the refill burst stalls the row)
+    constexpr int RG = 2;
     constexpr bool PAIRS = RG > 1;
     static_assert(D % RG == 0 && K % RG == 0, "commit groups tile the ring and the K-blocks");
     auto fetch = [&](int u, bool commit = true) {  // this lane's C values of the next row -> ring stage u
