@@ -511,15 +511,17 @@ def roofline_of(kern, cfg_name="c2", sm_mhz=None):
                  frac=floor / ns_row, frac_of_chain_floor=floor / ns_row,
                  note="row-serial DP chain; peak = measured 59-cycle chain floor at the sampled SM clock; "
                       "its HBM view: " + f"{kd['gbs']:.0f} GB/s = {kd['gbs'] / peak:.3f} of {peak:.0f} GB/s")
-        try:  # shared-memory fraction and barrier stalls of the committed C2 ncu capture
-            nm = json.load(open(os.path.join(ROOT, "profiles", "r01_dp_ncu_metrics.json")))
+        for f in ("r02_dp_ncu_metrics.json", "r01_dp_ncu_metrics.json"):
+            try:  # shared-memory fraction and barrier stalls of the committed C2 ncu capture
+                nm = json.load(open(os.path.join(ROOT, "profiles", f)))
+            except Exception:
+                continue
             if cfg_name == "c2":
                 r.update(smem_frac_active_sms=nm["smem_wavefronts_frac_of_peak_active_sms"],
                          barrier_stall_share=nm["barrier_stall_share"],
                          halo_wait_stall_share=nm["stall_share"].get("long_scoreboard"),
-                         ncu_source="profiles/r01_dp_ncu_metrics.json")
-        except Exception:
-            pass
+                         ncu_source="profiles/" + f)
+            break
     elif dom == "k_dp_seam" and measured_inst(dom, cfg_name):
         # the batch DP is issue-bound (ncu: FP64 and XU pipes below half busy, issue slots
         # ~70 % busy): instruction issue rate against one warp-instruction per scheduler per
