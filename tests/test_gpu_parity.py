@@ -334,6 +334,18 @@ def test_every_dp_variant_bitexact(port, monkeypatch, variant):
     assert np.array_equal(outs[1], port.carve(imgs[1], 480, 70))
 
 
+@pytest.mark.parametrize("variant", ["0", "8", "12"])
+def test_phase1_handoff_carves_match_oracle(port, monkeypatch, variant):
+    """Phase 1 with the label table left distributed (CARVE_DP_GATHER=0): the backtrack
+    token moves between the cluster's CTAs whenever the seam crosses a 128- or 160-column
+    CTA boundary. Whole carves (100 seams, both orientations) against the oracle."""
+    monkeypatch.setenv("CARVE_DP_GATHER", "0")
+    monkeypatch.setenv("CARVE_DP_VARIANT", variant)
+    for k, (w, h, tw, th) in enumerate([(700, 300, 600, 300), (640, 200, 600, 140)]):
+        img = port.make_test_image(w, h, k + 5)
+        assert np.array_equal(cv.carve(img, tw, th), port.carve(img, tw, th))
+
+
 def _right_heavy_image(w, h):
     # grey ramp flattening towards the right edge: the last column has the least energy,
     # so seams run down column W-1 (the removal's "nothing moves" case, incl. W-1 = 0 mod 4)
